@@ -1,0 +1,349 @@
+"""ctypes view of the parity checkers (TEST INFRASTRUCTURE ONLY).
+
+* ``C``   — oracle/_build/libsgml_oracle.so, the C restatement of the
+  reference solve path (oracle/sgml_oracle.c).  Builds anywhere.
+* ``REF`` — oracle/_ref/libsgml_ref.so, the UNMODIFIED reference core compiled
+  in place from /root/reference (oracle/Makefile ``ref``), or None when that
+  tree was not available at build time.
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's cpu_baseline /
+``--impl reference`` legs may import this module.  The product package
+(paper_1703_07206_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+C_LIB_PATH = os.path.join(HERE, "_build", "libsgml_oracle.so")
+REF_LIB_PATH = os.path.join(HERE, "_ref", "libsgml_ref.so")
+REF_SOURCE = "/root/reference/proj/core"
+
+DIRICHLET, NEUMANN = 0, 1
+
+
+class Grid(C.Structure):
+    _fields_ = [("dim", C.c_int), ("n", C.c_int), ("N", C.c_int), ("pad_", C.c_int),
+                ("h", C.c_double), ("total", C.c_uint64)]
+
+
+class Bc(C.Structure):
+    _fields_ = [("kind", C.c_int * 6), ("value", C.c_double * 6)]
+
+
+class Row(C.Structure):
+    _fields_ = [("cycle", C.c_int), ("pad_", C.c_int), ("work_units", C.c_uint64),
+                ("residual", C.c_double), ("diag_min", C.c_double)]
+
+
+class Sample(C.Structure):
+    _fields_ = [("cycle", C.c_int), ("pass_", C.c_int), ("level", C.c_int), ("pad_", C.c_int),
+                ("value", C.c_double)]
+
+
+class Report(C.Structure):
+    _fields_ = [("rows", C.POINTER(Row)), ("rows_cap", C.c_int64), ("n_rows", C.c_int64),
+                ("trace", C.POINTER(Sample)), ("trace_cap", C.c_int64), ("n_trace", C.c_int64),
+                ("converged", C.c_int), ("nan_detected", C.c_int), ("stagnated", C.c_int),
+                ("pad_", C.c_int), ("normalization", C.c_double), ("node_updates", C.c_uint64)]
+
+
+def build(with_ref: bool | None = None) -> None:
+    """Compile the C restatement (and the reference when its tree exists)."""
+    subprocess.check_call(["make", "-s", "-C", HERE], stdout=subprocess.DEVNULL)
+    if with_ref is None:
+        with_ref = os.path.isdir(REF_SOURCE)
+    if with_ref:
+        subprocess.check_call(["make", "-s", "-C", HERE, "ref"], stdout=subprocess.DEVNULL)
+
+
+_D = C.POINTER(C.c_double)
+_U64P = C.POINTER(C.c_uint64)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_D)
+
+
+def _load_c():
+    if not os.path.exists(C_LIB_PATH):
+        build(with_ref=False)
+    lib = C.CDLL(C_LIB_PATH)
+    G, B = C.POINTER(Grid), C.POINTER(Bc)
+    lib.og_make_grid.argtypes = [C.c_int, C.c_int, G]
+    lib.og_restrict_pass.argtypes = [G, B, _D, _D, C.c_int]
+    lib.og_restriction_into.argtypes = [G, B, _D, C.c_int, _D, _D, _U64P]
+    lib.og_relaxation_interpolation.argtypes = [G, B, _D, _D, _D, _D, C.c_int, _D, _D, C.c_double,
+                                                C.c_double, C.c_int, _D, _U64P]
+    lib.og_residual_update.argtypes = [G, B, _D, _D, _D, C.c_double]
+    lib.og_apply_operator.argtypes = [G, B, _D, _D, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int]
+    lib.og_apply_operator.restype = C.c_double
+    lib.og_max_abs.argtypes = [_D, C.c_uint64]
+    lib.og_max_abs.restype = C.c_double
+    lib.og_trapezoid_mean.argtypes = [G, _D]
+    lib.og_trapezoid_mean.restype = C.c_double
+    lib.og_zero_mean_projection.argtypes = [G, _D]
+    lib.og_apply_boundary.argtypes = [G, B, _D, C.c_int]
+    lib.og_build_schedule.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int), C.c_int]
+    lib.og_closed_form_work_units.argtypes = [C.c_int, C.c_int]
+    lib.og_closed_form_work_units.restype = C.c_uint64
+    lib.og_restrict_sigma_levels.argtypes = [G, _D, _D]
+    lib.og_single_cycle.argtypes = [G, B, _D, _D, _D, _D, _D, _D, C.c_double, C.c_int, C.c_int,
+                                    C.c_double, C.c_int, C.c_double, C.POINTER(Report), _U64P]
+    lib.og_solve.argtypes = [G, B, _D, _D, C.c_double, C.c_int, C.c_double, C.c_int, C.c_double,
+                             _D, C.POINTER(Report)]
+    for fn in ("og_fill_poisson2d", "og_fill_poisson3d", "og_fill_sinsin2d"):
+        getattr(lib, fn).argtypes = [G, _D]
+    lib.og_fill_capacitor_sigma.argtypes = [G, C.c_double, _D]
+    lib.og_lcg_fill.argtypes = [_D, C.c_uint64, C.c_uint64]
+    return lib
+
+
+def _load_ref():
+    if not os.path.exists(REF_LIB_PATH):
+        if not os.path.isdir(REF_SOURCE):
+            return None
+        build(with_ref=True)
+    lib = C.CDLL(REF_LIB_PATH)
+    G, B = C.POINTER(Grid), C.POINTER(Bc)
+    lib.ref_restriction_into.argtypes = [G, B, _D, C.c_int, _D, _U64P]
+    lib.ref_relaxation_interpolation.argtypes = [G, B, _D, _D, _D, _D, C.c_int, _D, _D, C.c_double,
+                                                 C.c_double, C.c_int, _D, _U64P]
+    lib.ref_residual_update.argtypes = [G, B, _D, _D, _D, C.c_double]
+    lib.ref_max_abs.argtypes = [G, _D]
+    lib.ref_max_abs.restype = C.c_double
+    lib.ref_trapezoid_mean.argtypes = [G, _D]
+    lib.ref_trapezoid_mean.restype = C.c_double
+    lib.ref_closed_form_work_units.argtypes = [C.c_int, C.c_int]
+    lib.ref_closed_form_work_units.restype = C.c_uint64
+    lib.ref_single_cycle.argtypes = [G, B, _D, _D, _D, C.c_double, C.c_int, C.c_int, C.c_double,
+                                     C.c_int, C.c_double, C.POINTER(Report), _U64P]
+    lib.ref_solve.argtypes = [G, B, _D, _D, C.c_double, C.c_int, C.c_double, C.c_int, C.c_double,
+                              _D, C.POINTER(Report)]
+    lib.ref_problem_fields.argtypes = [C.c_char_p, C.c_int, _D, _D, C.POINTER(C.c_int), _D, _D]
+    return lib
+
+
+_c_lib = None
+_ref_lib = None
+_ref_probed = False
+
+
+def c_lib():
+    global _c_lib
+    if _c_lib is None:
+        _c_lib = _load_c()
+    return _c_lib
+
+
+def ref_lib():
+    """The compiled reference, or None when it is unavailable on this host."""
+    global _ref_lib, _ref_probed
+    if not _ref_probed:
+        _ref_probed = True
+        _ref_lib = _load_ref()
+    return _ref_lib
+
+
+# ------------------------------------------------------------ helpers ----
+
+def make_grid(dim: int, n: int) -> Grid:
+    g = Grid()
+    if c_lib().og_make_grid(dim, n, C.byref(g)) != 0:
+        raise ValueError("make_grid: dim must be 2 or 3 and n in [1, 13]")
+    return g
+
+
+def make_bc(kinds, values=None) -> Bc:
+    b = Bc()
+    values = values if values is not None else [0.0] * 6
+    for f in range(6):
+        b.kind[f] = int(kinds[f])
+        b.value[f] = float(values[f])
+    return b
+
+
+def all_dirichlet(value=0.0) -> Bc:
+    return make_bc([DIRICHLET] * 6, [value] * 6)
+
+
+def all_neumann() -> Bc:
+    return make_bc([NEUMANN] * 6)
+
+
+def shape_of(g: Grid):
+    return (g.N,) * g.dim
+
+
+def lcg(g_or_total, seed: int) -> np.ndarray:
+    total = g_or_total.total if isinstance(g_or_total, Grid) else int(g_or_total)
+    out = np.empty(total, np.float64)
+    c_lib().og_lcg_fill(_ptr(out), total, seed)
+    return out
+
+
+@dataclass
+class SolveOut:
+    u: np.ndarray
+    rows: list = field(default_factory=list)        # (cycle, work_units, residual, diag_min)
+    trace: list = field(default_factory=list)       # (cycle, pass, level, value)
+    converged: bool = False
+    nan_detected: bool = False
+    stagnated: bool = False
+    normalization: float = 0.0
+    node_updates: int = 0
+    status: int = 0
+
+
+def _report(rows_cap=4096, trace_cap=1 << 20):
+    rows = (Row * rows_cap)()
+    trace = (Sample * trace_cap)()
+    rep = Report()
+    rep.rows, rep.rows_cap = C.cast(rows, C.POINTER(Row)), rows_cap
+    rep.trace, rep.trace_cap = C.cast(trace, C.POINTER(Sample)), trace_cap
+    return rep, rows, trace
+
+
+def _collect(u, rep, rows, trace, status) -> SolveOut:
+    out = SolveOut(u=u, status=status)
+    out.rows = [(rows[i].cycle, rows[i].work_units, rows[i].residual, rows[i].diag_min)
+                for i in range(min(rep.n_rows, rep.rows_cap))]
+    out.trace = [(trace[i].cycle, trace[i].pass_, trace[i].level, trace[i].value)
+                 for i in range(min(rep.n_trace, rep.trace_cap))]
+    out.converged, out.nan_detected, out.stagnated = bool(rep.converged), bool(rep.nan_detected), \
+        bool(rep.stagnated)
+    out.normalization, out.node_updates = rep.normalization, rep.node_updates
+    return out
+
+
+def solve(g: Grid, bc: Bc, f, sigma=None, a=0.0, n_r=2, tol=1e-12, max_cycles=50, safety=0.9,
+          impl: str = "c") -> SolveOut:
+    """Run the oracle solve ('c' restatement or 'ref' compiled reference)."""
+    u = np.zeros(g.total, np.float64)
+    rep, rows, trace = _report()
+    f = np.ascontiguousarray(f, np.float64).reshape(-1)
+    sig = None if sigma is None else np.ascontiguousarray(sigma, np.float64).reshape(-1)
+    if impl == "c":
+        st = c_lib().og_solve(C.byref(g), C.byref(bc), _ptr(f), _ptr(sig), a, n_r, tol,
+                              max_cycles, safety, _ptr(u), C.byref(rep))
+    else:
+        st = ref_lib().ref_solve(C.byref(g), C.byref(bc), _ptr(f), _ptr(sig), a, n_r, tol,
+                                 max_cycles, safety, _ptr(u), C.byref(rep))
+    return _collect(u, rep, rows, trace, st)
+
+
+def relax(g: Grid, bc: Bc, u_prev, du_prev, level, gsrc, sigma=None, a=0.0, safety=0.9,
+          homogeneous=False, impl: str = "c"):
+    """One relaxation-interpolation pass; returns (status, u, du, diag)."""
+    u = np.zeros(g.total, np.float64)
+    du = np.zeros(g.total, np.float64)
+    diag = C.c_double(0.0)
+    work = C.c_uint64(0)
+    args = (C.byref(g), C.byref(bc), _ptr(u), _ptr(u_prev), _ptr(du), _ptr(du_prev), level,
+            _ptr(gsrc), _ptr(sigma), a, safety, int(homogeneous), C.byref(diag), C.byref(work))
+    fn = c_lib().og_relaxation_interpolation if impl == "c" else ref_lib().ref_relaxation_interpolation
+    st = fn(*args)
+    return st, u, du, diag.value
+
+
+def restriction(g: Grid, bc: Bc, f, v, impl: str = "c"):
+    out = np.zeros(g.total, np.float64)
+    work = C.c_uint64(0)
+    if impl == "c":
+        scratch = np.zeros(g.total, np.float64)
+        c_lib().og_restriction_into(C.byref(g), C.byref(bc), _ptr(f), v, _ptr(out), _ptr(scratch),
+                                    C.byref(work))
+    else:
+        ref_lib().ref_restriction_into(C.byref(g), C.byref(bc), _ptr(f), v, _ptr(out), C.byref(work))
+    return out, work.value
+
+
+def residual_update(g: Grid, bc: Bc, r, e, sigma=None, a=0.0, impl: str = "c"):
+    r = np.array(r, np.float64, copy=True)
+    fn = c_lib().og_residual_update if impl == "c" else ref_lib().ref_residual_update
+    fn(C.byref(g), C.byref(bc), _ptr(r), _ptr(e), _ptr(sigma), a)
+    return r
+
+
+def single_cycle(g: Grid, bc: Bc, source, sigma_levels=None, a=0.0, homogeneous=False, n_r=2,
+                 safety=0.9, cycle_index=0, normalization=1.0, impl: str = "c"):
+    """Returns (status, state.u, trace, work) of one cycle from the zero state."""
+    T = g.total
+    u = np.zeros(T, np.float64)
+    rep, rows, trace = _report()
+    work = C.c_uint64(0)
+    sl = None if sigma_levels is None else np.ascontiguousarray(sigma_levels, np.float64).reshape(-1)
+    if impl == "c":
+        up = np.zeros(T, np.float64)
+        du = np.zeros(T, np.float64)
+        dup = np.zeros(T, np.float64)
+        st = c_lib().og_single_cycle(C.byref(g), C.byref(bc), _ptr(u), _ptr(up), _ptr(du), _ptr(dup),
+                                     _ptr(source), _ptr(sl), a, int(homogeneous), n_r, safety,
+                                     cycle_index, normalization, C.byref(rep), C.byref(work))
+    else:
+        st = ref_lib().ref_single_cycle(C.byref(g), C.byref(bc), _ptr(u), _ptr(source), _ptr(sl), a,
+                                        int(homogeneous), n_r, safety, cycle_index, normalization,
+                                        C.byref(rep), C.byref(work))
+    out = _collect(u, rep, rows, trace, st)
+    return st, u, out.trace, work.value
+
+
+def sigma_levels(g: Grid, sigma) -> np.ndarray:
+    out = np.zeros(g.n * g.total, np.float64)
+    st = c_lib().og_restrict_sigma_levels(C.byref(g), _ptr(np.ascontiguousarray(sigma)), _ptr(out))
+    if st != 0:
+        raise ValueError("restrict_sigma_levels: coefficient must stay positive")
+    return out
+
+
+def fill(name: str, g: Grid, sign: float = 1.0) -> np.ndarray:
+    out = np.zeros(g.total, np.float64)
+    lib = c_lib()
+    if name == "capacitor_sigma":
+        lib.og_fill_capacitor_sigma(C.byref(g), sign, _ptr(out))
+    else:
+        getattr(lib, "og_fill_" + name)(C.byref(g), _ptr(out))
+    return out
+
+
+def ref_problem(name: str, n: int):
+    """(grid, bc, f, sigma|None, a) exactly as the reference's builders make them."""
+    lib = ref_lib()
+    if lib is None:
+        raise RuntimeError("reference build unavailable")
+    dim = 2 if name in ("poisson2d", "deformation_circle") else 3
+    g = make_grid(dim, n)
+    f = np.zeros(g.total, np.float64)
+    sig = np.zeros(g.total, np.float64)
+    kinds = (C.c_int * 6)()
+    vals = (C.c_double * 6)()
+    a = C.c_double(0.0)
+    rc = lib.ref_problem_fields(name.encode(), n, _ptr(f), _ptr(sig), kinds, vals, C.byref(a))
+    if rc not in (2, 3):
+        raise ValueError(name)
+    bc = make_bc(list(kinds), list(vals))
+    return g, bc, f, (sig if rc == 3 else None), a.value
+
+
+def closed_form_work_units(n: int, n_r: int) -> int:
+    return int(c_lib().og_closed_form_work_units(n, n_r))
+
+
+def build_schedule(n: int, n_r: int):
+    cap = 4096
+    k = (C.c_int * cap)()
+    lv = (C.c_int * cap)()
+    cn = (C.c_int * cap)()
+    c = c_lib().og_build_schedule(n, n_r, k, lv, cn, cap)
+    if c < 0:
+        raise ValueError("build_schedule: n and n_r must be >= 1")
+    return [(k[i], lv[i], cn[i]) for i in range(c)]

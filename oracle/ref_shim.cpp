@@ -1,0 +1,206 @@
+// ref_shim.cpp — extern "C" view of the UNMODIFIED reference core.
+//
+// TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file together
+// with /root/reference/proj/core/src/{grid,stencil,kernels,cycle,problems,io}.cpp
+// (in place, never copied) into oracle/_ref/libsgml_ref.so with
+// -Dsgml=sgml_ref, so the reference's namespace cannot collide with
+// anything else loaded in the process.  The functions mirror
+// oracle/sgml_oracle.h (prefix ref_ instead of og_) so tests can run the
+// restatement and the reference side by side on identical inputs.
+#include <cstring>
+#include <stdexcept>
+
+#include "sgml/cycle.hpp"
+#include "sgml/kernels.hpp"
+#include "sgml/problems.hpp"
+
+extern "C" {
+#include "sgml_oracle.h"
+}
+
+namespace R = sgml;  // expands to sgml_ref under -Dsgml=sgml_ref
+
+namespace {
+
+R::BoundarySpec to_bc(const og_bc* bc) {
+    R::BoundarySpec b;
+    for (int f = 0; f < 6; ++f)
+        b.faces[f] = {bc->kind[f] == 1 ? R::BcKind::neumann : R::BcKind::dirichlet, bc->value[f]};
+    return b;
+}
+
+R::Field to_field(const R::Grid& g, const double* p) {
+    R::Field f(g);
+    std::memcpy(f.data(), p, g.total * sizeof(double));
+    return f;
+}
+
+void from_field(const R::Field& f, double* p) { std::memcpy(p, f.data(), f.size() * sizeof(double)); }
+
+R::Grid grid_of(const og_grid* g) { return R::make_grid(g->dim, g->n); }
+
+}  // namespace
+
+extern "C" {
+
+void ref_restriction_into(const og_grid* g, const og_bc* bc, const double* f, int v, double* out,
+                          uint64_t* work) {
+    const R::Grid gr = grid_of(g);
+    R::Field fo(gr), sc(gr);
+    std::uint64_t w = work ? *work : 0;
+    R::restriction_into(to_field(gr, f), v, to_bc(bc), fo, sc, &w);
+    if (work) *work = w;
+    from_field(fo, out);
+}
+
+int ref_relaxation_interpolation(const og_grid* g, const og_bc* bc, double* u, const double* u_prev,
+                                 double* du, const double* du_prev, int level, const double* gsrc,
+                                 const double* sigma, double a, double safety, int homogeneous,
+                                 double* diag_out, uint64_t* work) {
+    const R::Grid gr = grid_of(g);
+    R::SolveState st(gr);
+    st.level = level;
+    std::memcpy(st.u_prev.data(), u_prev, gr.total * sizeof(double));
+    std::memcpy(st.du_prev.data(), du_prev, gr.total * sizeof(double));
+    R::Field gf = to_field(gr, gsrc);
+    R::Field sf = sigma ? to_field(gr, sigma) : R::Field();
+    std::uint64_t w = work ? *work : 0;
+    int status = 0;
+    try {
+        *diag_out = R::relaxation_interpolation(st, gf, sigma ? &sf : nullptr, a, safety,
+                                                to_bc(bc), homogeneous != 0, &w);
+    } catch (const R::kernel_error& e) {
+        status = std::strstr(e.what(), "step") ? OG_BADSTEP : OG_NONFINITE;
+    }
+    if (work) *work = w;
+    from_field(st.u, u);
+    from_field(st.du, du);
+    return status;
+}
+
+void ref_residual_update(const og_grid* g, const og_bc* bc, double* r, const double* e,
+                         const double* sigma, double a) {
+    const R::Grid gr = grid_of(g);
+    R::Field rf = to_field(gr, r);
+    R::Field sf = sigma ? to_field(gr, sigma) : R::Field();
+    R::residual_update(rf, to_field(gr, e), R::OperatorCoefficients{sigma ? &sf : nullptr, a},
+                       to_bc(bc));
+    from_field(rf, r);
+}
+
+double ref_max_abs(const og_grid* g, const double* f) {
+    return R::max_abs(to_field(grid_of(g), f));
+}
+
+double ref_trapezoid_mean(const og_grid* g, const double* f) {
+    return R::trapezoid_mean(to_field(grid_of(g), f));
+}
+
+uint64_t ref_closed_form_work_units(int n, int n_r) { return R::closed_form_work_units(n, n_r); }
+
+int ref_single_cycle(const og_grid* g, const og_bc* bc, double* u_out, const double* source,
+                     const double* sigma_levels, double a, int homogeneous, int n_r, double safety,
+                     int cycle_index, double normalization, og_report* rep, uint64_t* work) {
+    const R::Grid gr = grid_of(g);
+    R::SolveState st(gr);
+    std::vector<R::Field> levels;
+    if (sigma_levels)
+        for (int v = 0; v < gr.n; ++v) levels.push_back(to_field(gr, sigma_levels + (size_t)v * gr.total));
+    R::SolveReport report;
+    std::uint64_t w = work ? *work : 0;
+    int status = 0;
+    try {
+        R::single_cycle(st, to_field(gr, source), levels, a, to_bc(bc), homogeneous != 0,
+                        R::build_schedule(gr.n, n_r), safety, cycle_index, normalization, report, w);
+    } catch (const R::kernel_error&) {
+        status = OG_NONFINITE;
+    }
+    if (work) *work = w;
+    from_field(st.u, u_out);
+    rep->n_trace = 0;
+    for (const auto& s : report.trace) {
+        if (rep->n_trace < rep->trace_cap)
+            rep->trace[rep->n_trace] = og_sample{s.cycle, s.pass, s.level, 0, s.value};
+        rep->n_trace++;
+    }
+    return status;
+}
+
+int ref_solve(const og_grid* g, const og_bc* bc, const double* f, const double* sigma, double a,
+              int n_r, double tol, int max_cycles, double safety, double* u_out, og_report* rep) {
+    const R::Grid gr = grid_of(g);
+    R::ProblemSpec prob;
+    prob.grid = gr;
+    prob.f = to_field(gr, f);
+    if (sigma) prob.sigma = to_field(gr, sigma);
+    prob.a = a;
+    prob.bc = to_bc(bc);
+    R::SolverConfig cfg;
+    cfg.n_r = n_r;
+    cfg.tol = tol;
+    cfg.max_cycles = max_cycles;
+    cfg.safety = safety;
+    R::SolveResult res;
+    try {
+        res = R::solve(prob, cfg);
+    } catch (const std::invalid_argument&) {
+        return OG_INVALID;
+    }
+    from_field(res.u, u_out);
+    const R::SolveReport& r = res.report;
+    rep->n_rows = 0;
+    for (const auto& row : r.rows) {
+        if (rep->n_rows < rep->rows_cap)
+            rep->rows[rep->n_rows] = og_row{row.cycle, 0, row.work_units, row.residual, row.diag_min};
+        rep->n_rows++;
+    }
+    rep->n_trace = 0;
+    for (const auto& s : r.trace) {
+        if (rep->n_trace < rep->trace_cap)
+            rep->trace[rep->n_trace] = og_sample{s.cycle, s.pass, s.level, 0, s.value};
+        rep->n_trace++;
+    }
+    rep->converged = r.converged;
+    rep->nan_detected = r.nan_detected;
+    rep->stagnated = r.stagnated;
+    rep->normalization = r.normalization;
+    rep->node_updates = r.node_updates;
+    return 0;
+}
+
+// Reference problem builders: the exact source/coefficient bits the
+// reference solves (used for golden vectors and the cpu baseline).
+int ref_problem_fields(const char* name, int n, double* f_out, double* sigma_out, int* bc_kind,
+                       double* bc_value, double* a_out) {
+    R::ProblemSpec p;
+    const std::string s(name);
+    if (s == "poisson2d") p = R::poisson2d_problem(n);
+    else if (s == "poisson3d") p = R::poisson3d_problem(n);
+    else if (s == "capacitor_high") p = R::capacitor_problem(n, "high");
+    else if (s == "capacitor_low") p = R::capacitor_problem(n, "low");
+    else if (s == "trifoil_x" || s == "trifoil_y" || s == "trifoil_z") {
+        const R::TrifoilSetup t = R::trifoil_problem(n, 0.14);
+        p = t.psi[s == "trifoil_x" ? 0 : s == "trifoil_y" ? 1 : 2];
+    } else if (s == "deformation_circle") {
+        // the CLI smoke circle: 32 points, centre (1/2, 1/2), radius 1/4, closed
+        R::Curve c;
+        c.closed = true;
+        for (int q = 0; q < 32; ++q) {
+            const double t = 2.0 * 3.14159265358979323846 * q / 32.0;
+            c.points.push_back({0.5 + 0.25 * std::cos(t), 0.5 + 0.25 * std::sin(t), 0.0});
+        }
+        p = R::deformation_problem(c, 0.1, n).problem;
+    } else {
+        return 1;
+    }
+    if (f_out) std::memcpy(f_out, p.f.data(), p.f.size() * sizeof(double));
+    if (sigma_out && p.sigma.size()) std::memcpy(sigma_out, p.sigma.data(), p.sigma.size() * sizeof(double));
+    for (int f = 0; f < 6; ++f) {
+        bc_kind[f] = p.bc.faces[f].kind == R::BcKind::neumann ? 1 : 0;
+        bc_value[f] = p.bc.faces[f].value;
+    }
+    *a_out = p.a;
+    return p.sigma.size() ? 3 : 2;
+}
+
+}  // extern "C"
