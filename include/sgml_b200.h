@@ -1,0 +1,228 @@
+/*
+ * sgml_b200.h — C ABI of the B200-native SGML solve path.
+ *
+ * This is the drop-in boundary for the reference's solve path
+ * (/root/reference/proj/core).  Every entry point names the reference
+ * interface it replaces (file:line under proj/core/include/sgml or src).
+ * Plain pointers and sizes only; no C++ or torch types cross this line.
+ * The C++ mirror of the reference API (include/sgml/*.hpp, namespace sgml)
+ * and the Python package (paper_1703_07206_b200) are thin layers over it.
+ *
+ * Memory model: an sgml_field is a device-resident fp64 field of N^dim
+ * nodes in the reference's x-fastest order (grid.hpp:78-119).  Host arrays
+ * cross the boundary only through sgml_field_upload/download and the
+ * host-buffer entry point sgml_solve.
+ *
+ * Errors: every function returns an sgml_status.  SGML_EINVAL maps to the
+ * reference's std::invalid_argument, SGML_EBADSTEP / SGML_ENONFINITE to
+ * sgml::kernel_error (kernels.hpp:38-40), SGML_ECUDA / SGML_ENCCL to
+ * std::runtime_error.  sgml_last_error() returns the message of the last
+ * failure on the calling thread.
+ *
+ * Numerics: all kernels are compiled without FMA contraction and follow the
+ * reference's operation order, so results are bit-identical to the
+ * reference CPU path up to the sign of exact zeros.
+ */
+#ifndef SGML_B200_H
+#define SGML_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SGML_OK = 0,
+    SGML_EINVAL = 1,     /* std::invalid_argument */
+    SGML_EBADSTEP = 2,   /* kernel_error: non-positive pseudo-time step */
+    SGML_ENONFINITE = 3, /* kernel_error: non-finite value produced */
+    SGML_ECUDA = 4,      /* std::runtime_error (CUDA) */
+    SGML_ENCCL = 5,      /* std::runtime_error (NCCL) */
+    SGML_ELOGIC = 6      /* std::logic_error / std::out_of_range */
+} sgml_status;
+
+typedef struct sgml_ctx sgml_ctx;       /* one device + one stream + buffer pool */
+typedef struct sgml_field sgml_field;   /* device-resident fp64 field */
+typedef struct sgml_solver sgml_solver; /* preallocated solve engine */
+
+/* grid.hpp:31-39 (make_grid, grid.cpp:10-23) */
+typedef struct {
+    int dim;
+    int n;
+    int N;
+    int pad_;
+    double h;
+    uint64_t total;
+} sgml_grid;
+
+/* grid.hpp:125-157: faces axis*2+side; kind 0 = dirichlet, 1 = neumann */
+typedef struct {
+    int kind[6];
+    double value[6];
+} sgml_bc;
+
+/* cycle.hpp:66-71 */
+typedef struct {
+    int n_r;
+    int max_cycles;
+    double tol;
+    double safety;
+} sgml_solver_cfg;
+
+/* Engine options that the reference has no counterpart for (kept out of
+ * sgml_solver_cfg so the reference SolverConfig maps 1:1). */
+typedef struct {
+    int engine;     /* 0 = level-compact B200 engine (default), 1 = literal full-grid passes */
+    int use_graph;  /* capture each cycle's launch sequence in a CUDA graph */
+    int timing;     /* record per-kernel-class device time in the report */
+    int pad_;
+} sgml_solver_opts;
+
+/* cycle.hpp:81-89 */
+typedef struct {
+    int cycle;
+    int has_l1;
+    uint64_t work_units;
+    double residual;
+    double diag_min;
+    double l1_error;
+} sgml_cycle_record;
+
+/* cycle.hpp:74-79 */
+typedef struct {
+    int cycle;
+    int pass;
+    int level;
+    int pad_;
+    double value;
+} sgml_diag_sample;
+
+/* Per-cycle hook (the l1_error column, cycle.cpp:222): called after u_total
+ * is accumulated; return 1 and set *l1 to record a value. */
+typedef int (*sgml_cycle_hook)(void* user, int cycle, const sgml_field* u_total, double* l1);
+
+/* cycle.hpp:91-99 with caller-owned arrays.  n_rows / n_trace count every
+ * record produced even past the capacities. */
+typedef struct {
+    sgml_cycle_record* rows;
+    int64_t rows_cap;
+    int64_t n_rows;
+    sgml_diag_sample* trace;
+    int64_t trace_cap;
+    int64_t n_trace;
+    int converged;
+    int nan_detected;
+    int stagnated;
+    int pad_;
+    double normalization;
+    uint64_t node_updates;
+    sgml_cycle_hook hook;
+    void* hook_user;
+    /* device timing of the last solve (CUDA events on the ctx stream) */
+    double device_ms;
+    uint64_t kernel_launches;
+    /* per kernel class (SGML_CLASS_*), filled when sgml_solver_opts.timing:
+     * summed event time and launch count inside the solve */
+    double class_ms[8];
+    uint64_t class_launches[8];
+} sgml_report;
+
+/* kernel classes of sgml_report.class_ms */
+enum {
+    SGML_CLASS_RELAX0 = 0,      /* level-0 (full-grid) relaxation pass */
+    SGML_CLASS_RELAX_COARSE = 1,/* level >= 1 compact relaxation pass */
+    SGML_CLASS_MATERIALIZE = 2, /* lazy interpolation / next-level input */
+    SGML_CLASS_PYRAMID = 3,     /* restriction pyramid step */
+    SGML_CLASS_RESIDUAL = 4,    /* fused residual recurrence */
+    SGML_CLASS_LITERAL = 5,     /* literal-engine restrict / relax passes */
+    SGML_CLASS_OTHER = 6        /* reductions, projections, fills */
+};
+
+/* pinned host memory for end-to-end transfers (cudaMallocHost) */
+int sgml_host_alloc(uint64_t bytes, void** out);
+int sgml_host_free(void* p);
+
+/* ---- library / context ------------------------------------------------ */
+const char* sgml_last_error(void);
+const char* sgml_version(void);
+int sgml_device_count(int* count);
+int sgml_ctx_create(int device, sgml_ctx** out);
+int sgml_ctx_destroy(sgml_ctx* ctx);
+int sgml_ctx_synchronize(sgml_ctx* ctx);
+/* the stream every kernel of this ctx is launched on (cudaStream_t) */
+void* sgml_ctx_stream(sgml_ctx* ctx);
+
+/* ---- grid / schedule (host logic; no device needed) --------------------- */
+int sgml_make_grid(int dim, int n, sgml_grid* out);                      /* grid.cpp:10-23 */
+/* cycle.cpp:28-45: kinds 0 = restrict_source, 1 = relax; returns the step
+ * count via *count (entries past cap are not written) */
+int sgml_build_schedule(int n, int n_r, int* kinds, int* levels, int* counts, int cap, int* count);
+uint64_t sgml_closed_form_work_units(int n, int n_r);                    /* cycle.cpp:47-59 */
+
+/* ---- fields (grid.hpp:78-119) ------------------------------------------ */
+int sgml_field_create(sgml_ctx* ctx, int dim, int n, sgml_field** out);
+int sgml_field_destroy(sgml_field* f);
+int sgml_field_upload(sgml_field* f, const double* host);
+int sgml_field_download(const sgml_field* f, double* host);
+int sgml_field_copy(sgml_field* dst, const sgml_field* src);
+int sgml_field_fill(sgml_field* f, double value);
+int sgml_field_grid(const sgml_field* f, sgml_grid* out);
+void* sgml_field_device_ptr(sgml_field* f);
+
+/* ---- kernels (kernels.hpp) ---------------------------------------------- */
+/* kernels.hpp:79-87 / kernels.cpp:305-325: v literal passes, out != scratch */
+int sgml_restriction_into(const sgml_field* f, int v, const sgml_bc* bc, sgml_field* out,
+                          sgml_field* scratch, uint64_t* work);
+/* kernels.hpp:89-104 / kernels.cpp:334-349: one pass at `level`, reads
+ * u_prev/du_prev, writes u/du; diag_out = unnormalised diagnostic max */
+int sgml_relaxation_interpolation(sgml_field* u, const sgml_field* u_prev, sgml_field* du,
+                                  const sgml_field* du_prev, int level, const sgml_field* g,
+                                  const sgml_field* sigma_or_null, double a, double safety,
+                                  const sgml_bc* bc, int homogeneous, double* diag_out,
+                                  uint64_t* work);
+/* kernels.hpp:106-117 / kernels.cpp:351-358 */
+int sgml_residual_update(sgml_field* r, const sgml_field* e, const sgml_field* sigma_or_null,
+                         double a, const sgml_bc* bc);
+int sgml_max_abs(const sgml_field* f, double* out);                      /* kernels.cpp:407-415 */
+int sgml_trapezoid_mean(const sgml_field* f, double* out);               /* kernels.cpp:367-386 */
+int sgml_zero_mean_projection(sgml_field* f);                            /* kernels.cpp:388-395 */
+int sgml_apply_boundary(sgml_field* u, const sgml_bc* bc, int homogeneous); /* kernels.cpp:397-405 */
+/* cycle.cpp:117-133: levels[v] <- sigma restricted to level v (even ghosts),
+ * SGML_EINVAL if any level is not positive; levels holds n fields */
+int sgml_restrict_sigma_levels(const sgml_field* sigma, sgml_field* const* levels);
+/* cycle.cpp:135-138 */
+int sgml_pure_neumann_pin(sgml_field* u);
+
+/* ---- driver (cycle.hpp) ------------------------------------------------- */
+/* cycle.hpp:121-136 / cycle.cpp:76-111: one cycle from the zero state of
+ * `state_u`; sigma_levels is NULL or n fields; trace samples appended to
+ * rep (rows untouched); *work advanced by the schedule's units.  On return
+ * state_u holds the cycle's correction (SolveState::u). */
+int sgml_single_cycle(sgml_ctx* ctx, sgml_field* state_u, const sgml_field* source,
+                      sgml_field* const* sigma_levels, double a, const sgml_bc* bc,
+                      int homogeneous, int n_r, double safety, int cycle_index,
+                      double normalization, const sgml_solver_opts* opts, sgml_report* rep,
+                      uint64_t* work);
+
+/* Preallocated engine for repeated solves on one grid/problem shape. */
+int sgml_solver_create(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, double a,
+                       const sgml_field* sigma_or_null, const sgml_solver_cfg* cfg,
+                       const sgml_solver_opts* opts, sgml_solver** out);
+int sgml_solver_destroy(sgml_solver* s);
+/* cycle.cpp:140-247 with device-resident f and u_out */
+int sgml_solver_run(sgml_solver* s, const sgml_field* f, sgml_field* u_out, sgml_report* rep);
+/* bytes of device memory the engine holds */
+int sgml_solver_footprint(const sgml_solver* s, uint64_t* bytes);
+
+/* cycle.hpp:147 / cycle.cpp:140-247 end to end: host f (and sigma), host
+ * u_out; uploads, solves on `ctx`'s device, downloads. */
+int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f_host,
+               const double* sigma_host_or_null, double a, const sgml_solver_cfg* cfg,
+               const sgml_solver_opts* opts_or_null, double* u_host_out, sgml_report* rep);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGML_B200_H */

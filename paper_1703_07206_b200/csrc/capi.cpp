@@ -1,0 +1,551 @@
+// capi.cpp — extern "C" boundary (include/sgml_b200.h).
+//
+// Translates C++ exceptions into sgml_status codes, owns contexts and
+// device fields, and implements the kernel-level entry points of
+// kernels.hpp on top of the literal sm_100a kernels.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <vector>
+
+#include "engine.hpp"
+
+namespace sgmlb {
+const char* last_error_cstr();
+}
+
+using namespace sgmlb;
+
+namespace {
+
+template <typename F>
+int guarded(F&& fn) {
+    try {
+        fn();
+        return SGML_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return SGML_ECUDA;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return SGML_ELOGIC;
+    }
+}
+
+void require(bool ok, int code, const char* msg) {
+    if (!ok) fail(code, msg);
+}
+
+void same_grid(const sgml_field* a, const sgml_field* b, const char* what) {
+    require(a && b, SGML_EINVAL, what);
+    require(a->grid.dim == b->grid.dim && a->grid.n == b->grid.n, SGML_EINVAL, what);
+}
+
+void activate(sgml_ctx* ctx) { SGML_CUDA(cudaSetDevice(ctx->device)); }
+
+double slot_to_double(unsigned long long bits) {
+    double d;
+    std::memcpy(&d, &bits, sizeof d);
+    return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sgml_last_error(void) { return last_error_cstr(); }
+
+const char* sgml_version(void) { return "sgml-b200 0.1 (sm_100a, fp64, no-FMA parity build)"; }
+
+int sgml_device_count(int* count) {
+    return guarded([&] {
+        int c = 0;
+        const cudaError_t e = cudaGetDeviceCount(&c);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            c = 0;
+        }
+        *count = c;
+    });
+}
+
+int sgml_ctx_create(int device, sgml_ctx** out) {
+    return guarded([&] {
+        require(out != nullptr, SGML_EINVAL, "ctx_create: null out");
+        int count = 0;
+        SGML_CUDA(cudaGetDeviceCount(&count));
+        require(device >= 0 && device < count, SGML_EINVAL, "ctx_create: no such CUDA device");
+        auto ctx = std::make_unique<sgml_ctx>();
+        ctx->device = device;
+        SGML_CUDA(cudaSetDevice(device));
+        SGML_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        SGML_CUDA(cudaMalloc((void**)&ctx->d_slots, 64 * sizeof(unsigned long long)));
+        SGML_CUDA(cudaMalloc((void**)&ctx->d_flags, 16 * sizeof(int)));
+        SGML_CUDA(cudaMallocHost((void**)&ctx->h_slots, 64 * sizeof(unsigned long long)));
+        SGML_CUDA(cudaMallocHost((void**)&ctx->h_flags, 16 * sizeof(int)));
+        *out = ctx.release();
+    });
+}
+
+int sgml_ctx_destroy(sgml_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(ctx->d_slots);
+        cudaFree(ctx->d_flags);
+        cudaFreeHost(ctx->h_slots);
+        cudaFreeHost(ctx->h_flags);
+        if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+        delete ctx->cached;
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int sgml_ctx_synchronize(sgml_ctx* ctx) {
+    return guarded([&] {
+        activate(ctx);
+        SGML_CUDA(cudaStreamSynchronize(ctx->stream));
+        SGML_CUDA(cudaGetLastError());
+    });
+}
+
+void* sgml_ctx_stream(sgml_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+// ---- grid / schedule -----------------------------------------------------
+
+int sgml_make_grid(int dim, int n, sgml_grid* out) {
+    return guarded([&] { *out = make_grid_or_throw(dim, n); });
+}
+
+int sgml_build_schedule(int n, int n_r, int* kinds, int* levels, int* counts, int cap, int* count) {
+    return guarded([&] {
+        require(n >= 1, SGML_EINVAL, "build_schedule: n must be >= 1");
+        require(n_r >= 1, SGML_EINVAL, "build_schedule: n_r must be >= 1");
+        int c = 0;
+        auto push = [&](int k, int l, int cnt) {
+            if (c < cap) { kinds[c] = k; levels[c] = l; counts[c] = cnt; }
+            ++c;
+        };
+        for (int v1 = n - 1; v1 >= 0; --v1) {
+            const int cnt = relax_count(n, n_r, v1);
+            for (int v = v1; v >= 0; --v) {
+                push(0, v, 1);
+                push(1, v, cnt);
+            }
+        }
+        const long long tail_cap = n < 62 ? (1LL << n) : (1LL << 62);
+        push(1, 0, (int)std::min<long long>(n_r, tail_cap));
+        *count = c;
+    });
+}
+
+uint64_t sgml_closed_form_work_units(int n, int n_r) {
+    if (n < 1 || n_r < 1) return 0;
+    uint64_t total = 0;
+    for (int v1 = 0; v1 <= n - 1; ++v1) {
+        total += (uint64_t)v1 * (v1 + 1) / 2;
+        total += (uint64_t)(v1 + 1) * relax_count(n, n_r, v1);
+    }
+    const long long tail_cap = n < 62 ? (1LL << n) : (1LL << 62);
+    total += (uint64_t)std::min<long long>(n_r, tail_cap);
+    return total;
+}
+
+// ---- fields ----------------------------------------------------------------
+
+int sgml_field_create(sgml_ctx* ctx, int dim, int n, sgml_field** out) {
+    return guarded([&] {
+        require(ctx && out, SGML_EINVAL, "field_create: null argument");
+        auto f = std::make_unique<sgml_field>();
+        f->ctx = ctx;
+        f->grid = make_grid_or_throw(dim, n);
+        activate(ctx);
+        f->d = dalloc(f->grid.total);
+        SGML_CUDA(cudaMemsetAsync(f->d, 0, f->grid.total * sizeof(double), ctx->stream));
+        SGML_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = f.release();
+    });
+}
+
+int sgml_field_destroy(sgml_field* f) {
+    return guarded([&] {
+        if (!f) return;
+        cudaSetDevice(f->ctx->device);
+        cudaStreamSynchronize(f->ctx->stream);
+        dfree(f->d);
+        delete f;
+    });
+}
+
+int sgml_field_upload(sgml_field* f, const double* host) {
+    return guarded([&] {
+        require(f && host, SGML_EINVAL, "field_upload: null argument");
+        activate(f->ctx);
+        SGML_CUDA(cudaMemcpyAsync(f->d, host, f->grid.total * sizeof(double), cudaMemcpyHostToDevice,
+                                  f->ctx->stream));
+        SGML_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    });
+}
+
+int sgml_field_download(const sgml_field* f, double* host) {
+    return guarded([&] {
+        require(f && host, SGML_EINVAL, "field_download: null argument");
+        activate(f->ctx);
+        SGML_CUDA(cudaMemcpyAsync(host, f->d, f->grid.total * sizeof(double), cudaMemcpyDeviceToHost,
+                                  f->ctx->stream));
+        SGML_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    });
+}
+
+int sgml_field_copy(sgml_field* dst, const sgml_field* src) {
+    return guarded([&] {
+        same_grid(dst, src, "field_copy: grid mismatch");
+        activate(dst->ctx);
+        SGML_CUDA(cudaMemcpyAsync(dst->d, src->d, dst->grid.total * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, dst->ctx->stream));
+        SGML_CUDA(cudaStreamSynchronize(dst->ctx->stream));
+    });
+}
+
+int sgml_field_fill(sgml_field* f, double value) {
+    return guarded([&] {
+        require(f != nullptr, SGML_EINVAL, "field_fill: null field");
+        activate(f->ctx);
+        std::vector<double> h(f->grid.total, value);
+        SGML_CUDA(cudaMemcpyAsync(f->d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                  f->ctx->stream));
+        SGML_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    });
+}
+
+int sgml_field_grid(const sgml_field* f, sgml_grid* out) {
+    return guarded([&] {
+        require(f && out, SGML_EINVAL, "field_grid: null argument");
+        *out = f->grid;
+    });
+}
+
+void* sgml_field_device_ptr(sgml_field* f) { return f ? (void*)f->d : nullptr; }
+
+// ---- kernels -------------------------------------------------------------
+
+int sgml_restriction_into(const sgml_field* f, int v, const sgml_bc* bc, sgml_field* out,
+                          sgml_field* scratch, uint64_t* work) {
+    return guarded([&] {
+        same_grid(f, out, "restriction_into: grid mismatch");
+        same_grid(f, scratch, "restriction_into: grid mismatch");
+        require(bc != nullptr, SGML_EINVAL, "restriction_into: null bc");
+        require(out != scratch, SGML_EINVAL, "restriction_into: out and scratch must differ");
+        require(v >= 0 && v <= f->grid.n, SGML_EINVAL, "restriction_into: level out of range");
+        sgml_ctx* ctx = f->ctx;
+        activate(ctx);
+        const sgml_grid& g = f->grid;
+        const cudaStream_t s = ctx->stream;
+        if (v == 0) {
+            SGML_CUDA(cudaMemcpyAsync(out->d, f->d, g.total * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        } else {
+            const BcDev b = to_dev(*bc);
+            const double* src = f->d;
+            double* dst = (v % 2 == 1) ? out->d : scratch->d;
+            for (int m = 0; m < v; ++m) {
+                launch_restrict_pass(g.dim, src, dst, g.N, 1 << m, b, s);
+                src = dst;
+                dst = (dst == out->d) ? scratch->d : out->d;
+            }
+            if (work) *work += (uint64_t)v;
+        }
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int sgml_relaxation_interpolation(sgml_field* u, const sgml_field* u_prev, sgml_field* du,
+                                  const sgml_field* du_prev, int level, const sgml_field* g,
+                                  const sgml_field* sigma, double a, double safety,
+                                  const sgml_bc* bc, int homogeneous, double* diag_out,
+                                  uint64_t* work) {
+    return guarded([&] {
+        same_grid(u, u_prev, "relaxation_interpolation: grid mismatch");
+        same_grid(u, du, "relaxation_interpolation: grid mismatch");
+        same_grid(u, du_prev, "relaxation_interpolation: grid mismatch");
+        same_grid(u, g, "relaxation_interpolation: grid mismatch");
+        if (sigma) same_grid(u, sigma, "relaxation_interpolation: grid mismatch");
+        require(bc != nullptr, SGML_EINVAL, "relaxation_interpolation: null bc");
+        require(level >= 0 && level <= u->grid.n, SGML_EINVAL, "relaxation_interpolation: bad level");
+        sgml_ctx* ctx = u->ctx;
+        activate(ctx);
+        const cudaStream_t s = ctx->stream;
+        const sgml_grid& gr = u->grid;
+        SGML_CUDA(cudaMemsetAsync(ctx->d_slots, 0, sizeof(unsigned long long), s));
+        SGML_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), s));
+        const RelaxConst rc = relax_const(gr.dim, level, gr.h, a, safety, homogeneous != 0);
+        launch_relax_literal(gr.dim, sigma != nullptr, u->d, du->d, u_prev->d, du_prev->d, g->d,
+                             sigma ? sigma->d : nullptr, gr.N, level, rc, to_dev(*bc), ctx->d_slots,
+                             ctx->d_flags, s);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaMemcpyAsync(ctx->h_slots, ctx->d_slots, sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+        if (diag_out) *diag_out = slot_to_double(ctx->h_slots[0]);
+        // kernels.cpp:343-346: badstep is checked first, then non-finite
+        if (!(safety > 0.0)) fail(SGML_EBADSTEP, "relaxation_interpolation: non-positive pseudo-time step");
+        if (ctx->h_flags[0]) fail(SGML_ENONFINITE, "relaxation_interpolation: non-finite value produced");
+        if (work) *work += 1;
+    });
+}
+
+int sgml_residual_update(sgml_field* r, const sgml_field* e, const sgml_field* sigma, double a,
+                         const sgml_bc* bc) {
+    return guarded([&] {
+        same_grid(r, e, "residual_update: grid mismatch");
+        if (sigma) same_grid(r, sigma, "residual_update: grid mismatch");
+        require(bc != nullptr, SGML_EINVAL, "residual_update: null bc");
+        sgml_ctx* ctx = r->ctx;
+        activate(ctx);
+        const sgml_grid& g = r->grid;
+        launch_residual(g.dim, sigma != nullptr, r->d, e->d, nullptr, sigma ? sigma->d : nullptr, g.N,
+                        1.0 / (g.h * g.h), g.dim == 2 ? 0.5 : 3.0 / 13.0, a, to_dev(*bc), nullptr,
+                        ctx->stream);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int sgml_max_abs(const sgml_field* f, double* out) {
+    return guarded([&] {
+        require(f && out, SGML_EINVAL, "max_abs: null argument");
+        sgml_ctx* ctx = f->ctx;
+        activate(ctx);
+        const cudaStream_t s = ctx->stream;
+        SGML_CUDA(cudaMemsetAsync(ctx->d_slots, 0, sizeof(unsigned long long), s));
+        launch_max_abs(f->d, f->grid.total, ctx->d_slots, s);
+        SGML_CUDA(cudaMemcpyAsync(ctx->h_slots, ctx->d_slots, sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+        *out = slot_to_double(ctx->h_slots[0]);
+    });
+}
+
+int sgml_trapezoid_mean(const sgml_field* f, double* out) {
+    return guarded([&] {
+        require(f && out, SGML_EINVAL, "trapezoid_mean: null argument");
+        activate(f->ctx);
+        *out = trapezoid_mean_host(f->ctx, f->grid, f->d);
+    });
+}
+
+int sgml_zero_mean_projection(sgml_field* f) {
+    return guarded([&] {
+        require(f != nullptr, SGML_EINVAL, "zero_mean_projection: null field");
+        activate(f->ctx);
+        const double mean = trapezoid_mean_host(f->ctx, f->grid, f->d);
+        launch_sub_scalar(f->d, f->grid.total, mean, f->ctx->stream);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaStreamSynchronize(f->ctx->stream));
+    });
+}
+
+int sgml_pure_neumann_pin(sgml_field* u) { return sgml_zero_mean_projection(u); }
+
+int sgml_apply_boundary(sgml_field* u, const sgml_bc* bc, int homogeneous) {
+    return guarded([&] {
+        require(u && bc, SGML_EINVAL, "apply_boundary: null argument");
+        activate(u->ctx);
+        launch_apply_boundary(u->grid.dim, u->d, u->grid.N, to_dev(*bc), homogeneous != 0, u->ctx->stream);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaStreamSynchronize(u->ctx->stream));
+    });
+}
+
+int sgml_restrict_sigma_levels(const sgml_field* sigma, sgml_field* const* levels) {
+    return guarded([&] {
+        require(sigma && levels, SGML_EINVAL, "restrict_sigma_levels: null argument");
+        const sgml_grid& g = sigma->grid;
+        for (int v = 0; v < g.n; ++v) same_grid(sigma, levels[v], "restrict_sigma_levels: grid mismatch");
+        sgml_ctx* ctx = sigma->ctx;
+        activate(ctx);
+        const cudaStream_t s = ctx->stream;
+        sgml_bc even{};
+        for (int f = 0; f < 6; ++f) even.kind[f] = 1;
+        const BcDev ev = to_dev(even);
+        double* scr = dalloc(g.total);
+        SGML_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), s));
+        for (int v = 0; v < g.n; ++v) {
+            double* out = levels[v]->d;
+            if (v == 0) {
+                SGML_CUDA(cudaMemcpyAsync(out, sigma->d, g.total * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            } else {
+                const double* src = sigma->d;
+                double* dst = (v % 2 == 1) ? out : scr;
+                for (int m = 0; m < v; ++m) {
+                    launch_restrict_pass(g.dim, src, dst, g.N, 1 << m, ev, s);
+                    src = dst;
+                    dst = (dst == out) ? scr : out;
+                }
+            }
+            launch_check_positive(out, g.total, ctx->d_flags, s);
+        }
+        SGML_CUDA(cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+        dfree(scr);
+        if (ctx->h_flags[0]) fail(SGML_EINVAL, "restrict_sigma_levels: coefficient must stay positive");
+    });
+}
+
+// ---- driver ----------------------------------------------------------------
+
+int sgml_single_cycle(sgml_ctx* ctx, sgml_field* state_u, const sgml_field* source,
+                      sgml_field* const* sigma_levels, double a, const sgml_bc* bc, int homogeneous,
+                      int n_r, double safety, int cycle_index, double normalization,
+                      const sgml_solver_opts* opts, sgml_report* rep, uint64_t* work) {
+    return guarded([&] {
+        require(ctx && state_u && source && bc && rep && work, SGML_EINVAL, "single_cycle: null argument");
+        same_grid(state_u, source, "single_cycle: grid mismatch");
+        require(n_r >= 1, SGML_EINVAL, "build_schedule: n_r must be >= 1");
+        const sgml_grid& g = source->grid;
+        activate(ctx);
+        sgml_solver_opts o{};
+        if (opts) o = *opts;
+        sgml_solver_cfg cfg{n_r, 1, 1.0, safety};
+        sgml_solver sv;
+        // literal engine when full sigma levels are supplied; the compact
+        // engine rebuilds its own sigma pyramid from level 0 (identical bits)
+        sv.build(ctx, g.dim, g.n, *bc, a, sigma_levels ? sigma_levels[0]->d : nullptr, cfg, o);
+        const cudaStream_t s = ctx->stream;
+        if (!(safety > 0.0)) {
+            // the first Restrict(n-1) step completes before the first pass throws
+            *work += (uint64_t)(g.n - 1);
+            fail(SGML_EBADSTEP, "relaxation_interpolation: non-positive pseudo-time step");
+        }
+        SGML_CUDA(cudaMemsetAsync(sv.d_cycle, 0, (sv.n_slots + 1) * sizeof(unsigned long long), s));
+        SGML_CUDA(cudaMemsetAsync(sv.d_flag, 0, sizeof(int), s));
+        const double* e = sv.cycle(source->d, homogeneous != 0);
+        SGML_CUDA(cudaMemcpyAsync(state_u->d, e, g.total * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        SGML_CUDA(cudaMemcpyAsync(sv.h_cycle, sv.d_cycle, sv.n_slots * sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaMemcpyAsync(sv.h_flag, sv.d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+        SGML_CUDA(cudaGetLastError());
+        const double inv_norm = normalization > 0.0 ? 1.0 / normalization : 1.0;
+        for (int p = 0; p < sv.n_slots; ++p) {
+            if (rep->n_trace < rep->trace_cap)
+                rep->trace[rep->n_trace] = sgml_diag_sample{cycle_index, sv.pass_index[p], sv.pass_level[p], 0,
+                                                            slot_to_double(sv.h_cycle[p]) * inv_norm};
+            rep->n_trace++;
+        }
+        if (sv.h_flag[0]) fail(SGML_ENONFINITE, "relaxation_interpolation: non-finite value produced");
+        *work += sv.units_per_cycle;
+    });
+}
+
+int sgml_solver_create(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, double a,
+                       const sgml_field* sigma, const sgml_solver_cfg* cfg,
+                       const sgml_solver_opts* opts, sgml_solver** out) {
+    return guarded([&] {
+        require(ctx && bc && cfg && out, SGML_EINVAL, "solver_create: null argument");
+        if (sigma) require(sigma->grid.dim == dim && sigma->grid.n == n, SGML_EINVAL, "solve: sigma grid mismatch");
+        sgml_solver_opts o{};
+        if (opts) o = *opts;
+        auto sv = std::make_unique<sgml_solver>();
+        sv->build(ctx, dim, n, *bc, a, sigma ? sigma->d : nullptr, *cfg, o);
+        *out = sv.release();
+    });
+}
+
+int sgml_solver_destroy(sgml_solver* s) {
+    return guarded([&] { delete s; });
+}
+
+int sgml_solver_run(sgml_solver* s, const sgml_field* f, sgml_field* u_out, sgml_report* rep) {
+    return guarded([&] {
+        require(s && f && rep, SGML_EINVAL, "solver_run: null argument");
+        require(f->grid.dim == s->g.dim && f->grid.n == s->g.n, SGML_EINVAL, "solve: source grid mismatch");
+        if (u_out) require(u_out->grid.dim == s->g.dim && u_out->grid.n == s->g.n, SGML_EINVAL,
+                           "solve: output grid mismatch");
+        s->run(f->d, u_out ? u_out->d : nullptr, rep);
+    });
+}
+
+int sgml_solver_footprint(const sgml_solver* s, uint64_t* bytes) {
+    return guarded([&] {
+        require(s && bytes, SGML_EINVAL, "solver_footprint: null argument");
+        *bytes = s->bytes;
+    });
+}
+
+int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f_host,
+               const double* sigma_host, double a, const sgml_solver_cfg* cfg,
+               const sgml_solver_opts* opts, double* u_host_out, sgml_report* rep) {
+    return guarded([&] {
+        require(ctx && bc && f_host && cfg && rep, SGML_EINVAL, "solve: null argument");
+        const sgml_grid g = make_grid_or_throw(dim, n);
+        activate(ctx);
+        const cudaStream_t s = ctx->stream;
+        // cycle.cpp:142-152 validation order: tol, n_r, finite source
+        require(cfg->tol > 0.0, SGML_EINVAL, "solve: tol must be positive");
+        require(cfg->n_r >= 1, SGML_EINVAL, "solve: n_r must be >= 1");
+        sgml_solver_opts o{};
+        if (opts) o = *opts;
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        // one cached engine per context: repeated solves of one problem shape
+        // reuse its device buffers (freed with the context)
+        std::string key(reinterpret_cast<const char*>(&g), sizeof g);
+        key.append(reinterpret_cast<const char*>(bc), sizeof *bc);
+        key.append(reinterpret_cast<const char*>(&a), sizeof a);
+        key.append(reinterpret_cast<const char*>(cfg), sizeof *cfg);
+        key.append(reinterpret_cast<const char*>(&o), sizeof o);
+        key.push_back(sigma_host ? 's' : '-');
+        const size_t bytes = g.total * sizeof(double);
+        if (!ctx->cached || ctx->cached_key != key) {
+            delete ctx->cached;
+            ctx->cached = nullptr;
+            ctx->cached_key.clear();
+            double* sig = nullptr;
+            struct Guard {
+                double* p = nullptr;
+                ~Guard() { dfree(p); }
+            } sg;
+            if (sigma_host) {
+                sg.p = sig = dalloc(g.total);
+                SGML_CUDA(cudaMemcpyAsync(sig, sigma_host, bytes, cudaMemcpyHostToDevice, s));
+            }
+            auto sv = std::make_unique<sgml_solver>();
+            sv->build(ctx, dim, n, *bc, a, sig, *cfg, o);
+            sv->fin = sv->alloc(g.total);
+            ctx->cached = sv.release();
+            ctx->cached_key = key;
+        } else if (sigma_host) {
+            sgml_solver* sv = ctx->cached;
+            SGML_CUDA(cudaMemcpyAsync(sv->sigma_level0(), sigma_host, bytes, cudaMemcpyHostToDevice, s));
+            sv->load_sigma(sv->sigma_level0());
+        }
+        sgml_solver* sv = ctx->cached;
+        SGML_CUDA(cudaMemcpyAsync(sv->fin, f_host, bytes, cudaMemcpyHostToDevice, s));
+        sv->run(sv->fin, nullptr, rep);
+        if (u_host_out)
+            SGML_CUDA(cudaMemcpyAsync(u_host_out, sv->utot, bytes, cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int sgml_host_alloc(uint64_t bytes, void** out) {
+    return guarded([&] {
+        require(out != nullptr, SGML_EINVAL, "host_alloc: null out");
+        SGML_CUDA(cudaMallocHost(out, bytes ? bytes : 1));
+    });
+}
+
+int sgml_host_free(void* p) {
+    return guarded([&] {
+        if (p) SGML_CUDA(cudaFreeHost(p));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,267 @@
+// device.cuh — pointwise fp64 math of the SGML path, shared by all kernels.
+//
+// Operation order follows the reference exactly:
+//   acc = acc + ((sbar * (u_nb - u_c)) * inv_l2)  over offsets r, q, p
+//   op  = (acc * pref) * inv_s2
+// The whole library is compiled with --fmad=false, so no multiply-add is
+// ever contracted.  Bit-safe shortcuts used here (each exact in IEEE):
+//   x * 1.0 == x (sigma == 1, inv_l2 == 1), x / 1.0 == x (a == 0),
+//   and zero-weight interpolation corners are skipped (sign of zero only).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sgmlb {
+
+// Boundary description in kernel-parameter form (grid.hpp:125-157).
+struct BcDev {
+    int neu[6];      // 1 = Neumann, 0 = Dirichlet
+    double val[6];   // Dirichlet values
+};
+
+// 1 / 3 rounded once, as stencil.cpp:21 computes 1.0 / l2 for l2 = 3.
+constexpr double kInv3 = 1.0 / 3.0;
+
+__device__ __forceinline__ size_t lin3(int N, int i, int j, int k) {
+    return (size_t)i + (size_t)N * ((size_t)j + (size_t)N * (size_t)k);
+}
+
+// grid.cpp:44-51 (node already known to lie on some face or not)
+template <int DIM>
+__device__ __forceinline__ bool on_dirichlet(const BcDev& bc, int N, int i, int j, int k) {
+    if ((i == 0 && !bc.neu[0]) || (i == N - 1 && !bc.neu[1])) return true;
+    if ((j == 0 && !bc.neu[2]) || (j == N - 1 && !bc.neu[3])) return true;
+    if (DIM == 3 && ((k == 0 && !bc.neu[4]) || (k == N - 1 && !bc.neu[5]))) return true;
+    return false;
+}
+
+// grid.cpp:53-62: lowest Dirichlet face id wins
+template <int DIM>
+__device__ __forceinline__ double dirichlet_value(const BcDev& bc, int N, int i, int j, int k) {
+    if (i == 0 && !bc.neu[0]) return bc.val[0];
+    if (i == N - 1 && !bc.neu[1]) return bc.val[1];
+    if (j == 0 && !bc.neu[2]) return bc.val[2];
+    if (j == N - 1 && !bc.neu[3]) return bc.val[3];
+    if (DIM == 3) {
+        if (k == 0 && !bc.neu[4]) return bc.val[4];
+        if (k == N - 1 && !bc.neu[5]) return bc.val[5];
+    }
+    return 0.0;
+}
+
+// stencil.cpp:52-85, unrolled by axis: x resolves first, then y, then z.
+// Odd reflection evaluates 2*u(face) - u(mirror).
+__device__ __forceinline__ double ghost_z(const double* __restrict__ u, int N, const BcDev& bc,
+                                          int i, int j, int k) {
+    if (k < 0) {
+        const double m = u[lin3(N, i, j, -k)];
+        return bc.neu[4] ? m : 2.0 * u[lin3(N, i, j, 0)] - m;
+    }
+    if (k > N - 1) {
+        const double m = u[lin3(N, i, j, 2 * (N - 1) - k)];
+        return bc.neu[5] ? m : 2.0 * u[lin3(N, i, j, N - 1)] - m;
+    }
+    return u[lin3(N, i, j, k)];
+}
+
+__device__ __forceinline__ double ghost_y(const double* __restrict__ u, int N, const BcDev& bc,
+                                          int i, int j, int k) {
+    if (j < 0) {
+        const double m = ghost_z(u, N, bc, i, -j, k);
+        return bc.neu[2] ? m : 2.0 * ghost_z(u, N, bc, i, 0, k) - m;
+    }
+    if (j > N - 1) {
+        const double m = ghost_z(u, N, bc, i, 2 * (N - 1) - j, k);
+        return bc.neu[3] ? m : 2.0 * ghost_z(u, N, bc, i, N - 1, k) - m;
+    }
+    return ghost_z(u, N, bc, i, j, k);
+}
+
+__device__ __forceinline__ double ghost(const double* __restrict__ u, int N, const BcDev& bc,
+                                        int i, int j, int k) {
+    if (i < 0) {
+        const double m = ghost_y(u, N, bc, -i, j, k);
+        return bc.neu[0] ? m : 2.0 * ghost_y(u, N, bc, 0, j, k) - m;
+    }
+    if (i > N - 1) {
+        const double m = ghost_y(u, N, bc, 2 * (N - 1) - i, j, k);
+        return bc.neu[1] ? m : 2.0 * ghost_y(u, N, bc, N - 1, j, k) - m;
+    }
+    return ghost_y(u, N, bc, i, j, k);
+}
+
+// grid.hpp:63-69 and stencil.cpp:87-90: sigma is always even-mirrored.
+__device__ __forceinline__ int mirror_index(int i, int N) {
+    return i < 0 ? -i : (i > N - 1 ? 2 * (N - 1) - i : i);
+}
+__device__ __forceinline__ double mirror(const double* __restrict__ u, int N, int i, int j, int k) {
+    return u[lin3(N, mirror_index(i, N), mirror_index(j, N), mirror_index(k, N))];
+}
+
+// acc + ((sbar*(un-uc)) * inv_l2) with the exact shortcuts for sbar == 1 and
+// inv_l2 == 1 (l2 = 1: face neighbours).
+template <bool SIG>
+__device__ __forceinline__ double stencil_term(double acc, double sbar, double un, double uc, int l2) {
+    double t = un - uc;
+    if (SIG) t = sbar * t;
+    if (l2 == 2) t = t * 0.5;
+    else if (l2 == 3) t = t * kInv3;
+    return acc + t;
+}
+
+// Per-pass constants of relax_pass (kernels.cpp:182-188) plus the host-side
+// precomputed step for sigma == 1 (smax == 1 exactly, so
+// dtau = (safety*kdim)/(inv_s2*1.0), identical to the per-node formula).
+struct RelaxConst {
+    double inv_s2;
+    double pref;
+    double kdim;
+    double a;
+    double safety;
+    double dtau1;      // used when sigma == 1
+    double denom1;     // 1.0 - dtau1*a (sigma == 1)
+    int homogeneous;
+    int has_a;
+};
+
+// kernels.cpp:94-137 at a subset node whose stencil neighbours sit at
+// +-lam in the index space of `up` (lam = 2^v for full-grid fields, 1 for
+// level-compact fields).  Returns the new value; diag through the reference.
+template <int DIM, bool SIG>
+__device__ __forceinline__ double relax_at(const double* __restrict__ up,
+                                           const double* __restrict__ sig,
+                                           const double* __restrict__ g, int N, int lam, int i,
+                                           int j, int k, size_t pos, const RelaxConst& rc,
+                                           const BcDev& bc, double& diag) {
+    const double uc = up[pos];
+    const double sc = SIG ? sig[pos] : 1.0;
+    const bool fast = i >= lam && i <= N - 1 - lam && j >= lam && j <= N - 1 - lam &&
+                      (DIM == 2 || (k >= lam && k <= N - 1 - lam));
+    double acc = 0.0, smax = 0.0;
+    if (fast) {
+        const ptrdiff_t sy = (ptrdiff_t)N * lam, sz = (ptrdiff_t)N * N * lam;
+#pragma unroll
+        for (int r = (DIM == 3 ? -1 : 0); r <= (DIM == 3 ? 1 : 0); ++r)
+#pragma unroll
+            for (int q = -1; q <= 1; ++q)
+#pragma unroll
+                for (int p = -1; p <= 1; ++p) {
+                    if (p == 0 && q == 0 && r == 0) continue;
+                    const ptrdiff_t d = r * sz + q * sy + p * lam;
+                    double sbar = 1.0;
+                    if (SIG) {
+                        sbar = 0.5 * (sig[pos + d] + sc);
+                        smax = smax < sbar ? sbar : smax;
+                    }
+                    acc = stencil_term<SIG>(acc, sbar, up[pos + d], uc, p * p + q * q + r * r);
+                }
+    } else {
+#pragma unroll
+        for (int r = (DIM == 3 ? -1 : 0); r <= (DIM == 3 ? 1 : 0); ++r)
+#pragma unroll
+            for (int q = -1; q <= 1; ++q)
+#pragma unroll
+                for (int p = -1; p <= 1; ++p) {
+                    if (p == 0 && q == 0 && r == 0) continue;
+                    const int ni = i + p * lam, nj = j + q * lam, nk = k + r * lam;
+                    double sbar = 1.0;
+                    if (SIG) {
+                        sbar = 0.5 * (mirror(sig, N, ni, nj, nk) + sc);
+                        smax = smax < sbar ? sbar : smax;
+                    }
+                    acc = stencil_term<SIG>(acc, sbar, ghost(up, N, bc, ni, nj, nk), uc,
+                                            p * p + q * q + r * r);
+                }
+    }
+    const double op = (acc * rc.pref) * rc.inv_s2;
+    const double gc = g[pos];
+    if (rc.has_a) {
+        diag = fabs((op + rc.a * uc) - gc);
+    } else {
+        diag = fabs(op - gc);
+    }
+    if (SIG) {
+        const double dtau = (rc.safety * rc.kdim) / (rc.inv_s2 * smax);
+        if (!(dtau > 0.0)) return __longlong_as_double(0x7ff8000000000000LL);
+        const double num = uc + dtau * (op - gc);
+        return rc.has_a ? num / (1.0 - dtau * rc.a) : num;
+    } else {
+        const double num = uc + rc.dtau1 * (op - gc);
+        return rc.has_a ? num / rc.denom1 : num;
+    }
+}
+
+// Interpolated increment of a level-l variation at full-grid node (x,y,z)
+// (kernels.cpp:140-174).  `du` is the level-l compact array with Nl nodes
+// per axis.  Weights are exact dyadics; zero-weight corners are skipped.
+template <int DIM>
+__device__ __forceinline__ double interp_compact(const double* __restrict__ du, int Nl, int l,
+                                                 int x, int y, int z) {
+    const int m = (1 << l) - 1;
+    const double inv_lam = 1.0 / (double)(1 << l);
+    const int x0 = x & ~m, y0 = y & ~m, z0 = z & ~m;
+    const double fx = (double)(x - x0) * inv_lam;
+    const double fy = (double)(y - y0) * inv_lam;
+    const double wx[2] = {1.0 - fx, fx};
+    const double wy[2] = {1.0 - fy, fy};
+    const int X0 = x0 >> l, Y0 = y0 >> l, Z0 = z0 >> l;
+    double acc = 0.0;
+    if (DIM == 2) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                if (wy[q] == 0.0 || wx[p] == 0.0) continue;
+                acc = acc + ((wy[q] * wx[p]) * du[(size_t)(X0 + p) + (size_t)Nl * (Y0 + q)]);
+            }
+    } else {
+        const double fz = (double)(z - z0) * inv_lam;
+        const double wz[2] = {1.0 - fz, fz};
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    if (wz[r] == 0.0 || wy[q] == 0.0 || wx[p] == 0.0) continue;
+                    acc = acc + (((wz[r] * wy[q]) * wx[p]) * du[lin3(Nl, X0 + p, Y0 + q, Z0 + r)]);
+                }
+    }
+    return acc;
+}
+
+// Non-negative double max via the ordered uint64 bit pattern.
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* slot, double v) {
+    if (v > 0.0) atomicMax(slot, (unsigned long long)__double_as_longlong(v));
+}
+
+// Block-wide max of a non-negative value, one atomic per block.
+__device__ __forceinline__ void block_max_commit(double v, unsigned long long* slot) {
+    for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = v < w ? w : v;
+    }
+    __shared__ double red[32];
+    const int nthreads = blockDim.x * blockDim.y * blockDim.z;
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int lane = tid & 31, warp = tid >> 5;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < (nthreads + 31) / 32 ? red[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double w = __shfl_xor_sync(0xffffffffu, v, o);
+            v = v < w ? w : v;
+        }
+        if (lane == 0) atomic_max_nonneg(slot, v);
+    }
+}
+
+__device__ __forceinline__ void block_or_commit(int bad, int* flag) {
+    if (__syncthreads_or(bad)) {
+        if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) atomicOr(flag, 1);
+    }
+}
+
+}  // namespace sgmlb

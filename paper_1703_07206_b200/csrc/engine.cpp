@@ -1,0 +1,649 @@
+// engine.cpp — host orchestration of the SGML schedule on one B200.
+//
+// Two engines run the reference's cycle (cycle.cpp:76-111):
+//
+//  * literal: the reference's full-grid passes one for one (restriction
+//    recomputed per Restrict(v) step, every relax pass over all N^d nodes).
+//    Kept as the parity/measurement baseline.
+//
+//  * compact (default): the same arithmetic on level-compact arrays.
+//    - Restriction: one pyramid per cycle, P_{m+1} = pass_m(P_m) on
+//      level-(m+1) nodes only (bit-identical on the subset,
+//      which is all relax reads, F3).
+//    - Relax at level v >= 1 touches only the S_v subset nodes (compact U_v).
+//      Non-subset nodes of the reference receive u_prev + I(du_prev) each
+//      pass; with du reset at every level change the first of those adds
+//      I(0) and the others add I(du_k) of the previous passes.  Those
+//      increments are kept compact (DU_v) and applied lazily, in the
+//      reference's order, when the next level's input is materialised
+//      (base + I_v1(du) + ... + I_{w+1}(du)), so coarse levels never sweep
+//      the full grid.  Dirichlet nodes always hold their face value after
+//      the first pass of a cycle.
+//    - Level-0 passes are full-grid relaxations (every node is a subset
+//      node at level 0); du at level 0 is never read, so it is not written.
+//   Everything a reference caller observes (state.u, the diagnostic trace,
+//   the work counter, the residual history) is bit-identical, up to the
+//   sign of exact zeros (I(0) is not added).
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+
+namespace sgmlb {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error_cstr() { return g_last_error.c_str(); }
+
+void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(SGML_ECUDA, std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what);
+}
+
+BcDev to_dev(const sgml_bc& bc) {
+    BcDev d{};
+    for (int f = 0; f < 6; ++f) {
+        d.neu[f] = bc.kind[f] == 1;
+        d.val[f] = bc.value[f];
+    }
+    return d;
+}
+
+bool any_dirichlet(const sgml_bc& bc, int dim) {
+    for (int f = 0; f < 2 * dim; ++f)
+        if (bc.kind[f] != 1) return true;
+    return false;
+}
+
+// grid.cpp:10-23
+sgml_grid make_grid_or_throw(int dim, int n) {
+    if (dim != 2 && dim != 3) fail(SGML_EINVAL, "make_grid: dim must be 2 or 3");
+    if (n < 1 || n > 13) fail(SGML_EINVAL, "make_grid: n must lie in [1, 13]");
+    sgml_grid g{};
+    g.dim = dim;
+    g.n = n;
+    g.N = (1 << n) + 1;
+    g.h = 1.0 / (g.N - 1);
+    g.total = 1;
+    for (int d = 0; d < dim; ++d) g.total *= (uint64_t)g.N;
+    return g;
+}
+
+// cycle.cpp:21-24
+int relax_count(int n, int n_r, int v1) {
+    const long long doubling = 1LL << (n - v1);
+    return (int)std::min<long long>(n_r, doubling);
+}
+
+// kernels.cpp:182-188 and the sigma == 1 step (see RelaxConst)
+RelaxConst relax_const(int dim, int level, double h, double a, double safety, bool homogeneous) {
+    RelaxConst rc{};
+    const int lam = 1 << level;
+    const double s = lam * h;
+    rc.inv_s2 = 1.0 / (s * s);
+    rc.pref = dim == 2 ? 0.5 : 3.0 / 13.0;
+    rc.kdim = dim == 2 ? 1.0 / 3.0 : 13.0 / 44.0;
+    rc.a = a;
+    rc.safety = safety;
+    const double smax = 1.0;
+    rc.dtau1 = safety * rc.kdim / (rc.inv_s2 * smax);
+    rc.denom1 = 1.0 - rc.dtau1 * a;
+    rc.homogeneous = homogeneous ? 1 : 0;
+    rc.has_a = a != 0.0;
+    return rc;
+}
+
+double* dalloc(size_t count) {
+    void* p = nullptr;
+    SGML_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(double)));
+    return (double*)p;
+}
+
+void dfree(double* p) {
+    if (p) cudaFree(p);
+}
+
+// kernels.cpp:367-386: serial Kahan sum in linear order, on a host copy.
+double trapezoid_mean_host(sgml_ctx* ctx, const sgml_grid& g, const double* dfield) {
+    const size_t bytes = g.total * sizeof(double);
+    if (ctx->h_stage_bytes < bytes) {
+        if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+        ctx->h_stage = nullptr;
+        SGML_CUDA(cudaMallocHost((void**)&ctx->h_stage, bytes));
+        ctx->h_stage_bytes = bytes;
+    }
+    SGML_CUDA(cudaMemcpyAsync(ctx->h_stage, dfield, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    SGML_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double* f = ctx->h_stage;
+    const int N = g.N;
+    double sum = 0.0, comp = 0.0;
+    size_t pos = 0;
+    const int KMAX = g.dim == 3 ? N : 1;
+    for (int k = 0; k < KMAX; ++k) {
+        const double wk = (g.dim == 3 && (k == 0 || k == N - 1)) ? 0.5 : 1.0;
+        for (int j = 0; j < N; ++j) {
+            const bool jf = j == 0 || j == N - 1;
+            for (int i = 0; i < N; ++i, ++pos) {
+                double w = 1.0;
+                if (i == 0 || i == N - 1) w *= 0.5;
+                if (jf) w *= 0.5;
+                if (wk != 1.0) w *= 0.5;
+                const double y = w * f[pos] - comp;
+                const double t = sum + y;
+                comp = (t - sum) - y;
+                sum = t;
+            }
+        }
+    }
+    double wsum = 1.0;
+    for (int d = 0; d < g.dim; ++d) wsum *= (double)(N - 1);
+    return sum / wsum;
+}
+
+}  // namespace sgmlb
+
+using namespace sgmlb;
+
+// ---------------------------------------------------------------------------
+// construction
+// ---------------------------------------------------------------------------
+
+double* sgml_solver::alloc(size_t count) {
+    double* p = dalloc(count);
+    bytes += std::max<size_t>(count, 1) * sizeof(double);
+    return p;
+}
+
+sgml_solver::~sgml_solver() {
+    if (ctx) cudaSetDevice(ctx->device);
+    for (auto& ge : graph)
+        if (ge) cudaGraphExecDestroy(ge);
+    dfree(r); dfree(utot); dfree(A); dfree(B); dfree(fin);
+    for (size_t m = 1; m < P.size(); ++m) dfree(P[m]);
+    for (double* s : S) dfree(s);
+    for (size_t v = 1; v < U.size(); ++v) { dfree(U[v][0]); dfree(U[v][1]); }
+    for (auto& lst : DU) for (double* d : lst) dfree(d);
+    dfree(Lg); dfree(Lscr); dfree(Lu); dfree(Lup); dfree(Ldu); dfree(Ldup);
+    for (double* s : Lsig) dfree(s);
+    for (cudaEvent_t e : evpool) cudaEventDestroy(e);
+    if (tev0) cudaEventDestroy(tev0);
+    if (tev1) cudaEventDestroy(tev1);
+    if (d_cycle) cudaFree(d_cycle);
+    if (d_flag) cudaFree(d_flag);
+    if (h_cycle) cudaFreeHost(h_cycle);
+    if (h_flag) cudaFreeHost(h_flag);
+}
+
+static uint64_t pow_dim(int N, int dim) { return dim == 2 ? (uint64_t)N * N : (uint64_t)N * N * N; }
+
+cudaEvent_t sgml_solver::next_event() {
+    if (evused == evpool.size()) {
+        cudaEvent_t e;
+        SGML_CUDA(cudaEventCreate(&e));
+        evpool.push_back(e);
+    }
+    return evpool[evused++];
+}
+
+void sgml_solver::harvest_spans() {
+    for (const Span& sp : spans) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, sp.a, sp.b) == cudaSuccess) {
+            cls_ms[sp.cls] += ms;
+            cls_n[sp.cls] += 1;
+        }
+    }
+    spans.clear();
+    evused = 0;
+}
+
+void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double a_,
+                        const double* sigma_dev, const sgml_solver_cfg& cfg_,
+                        const sgml_solver_opts& opts_) {
+    ctx = c;
+    g = make_grid_or_throw(dim, n);
+    if (!(cfg_.tol > 0.0)) fail(SGML_EINVAL, "solve: tol must be positive");
+    if (cfg_.n_r < 1) fail(SGML_EINVAL, "solve: n_r must be >= 1");
+    bc_host = bcin;
+    bc = to_dev(bcin);
+    all_neumann = !any_dirichlet(bcin, dim);
+    a = a_;
+    has_sigma = sigma_dev != nullptr;
+    cfg = cfg_;
+    opts = opts_;
+    SGML_CUDA(cudaSetDevice(ctx->device));
+
+    // schedule (cycle.cpp:28-45) flattened to relax passes
+    int pass_idx = 0;
+    for (int v1 = n - 1; v1 >= 0; --v1) {
+        const int cnt = relax_count(n, cfg.n_r, v1);
+        for (int v = v1; v >= 0; --v) {
+            pass_idx += v;  // Restrict(v) costs v passes
+            for (int k = 0; k < cnt; ++k) { pass_level.push_back(v); pass_index.push_back(pass_idx++); }
+        }
+    }
+    const int tail = relax_count(n, cfg.n_r, 0 /* 2^n cap */);
+    for (int k = 0; k < tail; ++k) { pass_level.push_back(0); pass_index.push_back(pass_idx++); }
+    units_per_cycle = (uint64_t)pass_idx;
+    n_slots = (int)pass_level.size();
+
+    SGML_CUDA(cudaMalloc((void**)&d_cycle, (n_slots + 4) * sizeof(unsigned long long)));
+    SGML_CUDA(cudaMalloc((void**)&d_flag, 4 * sizeof(int)));
+    SGML_CUDA(cudaMallocHost((void**)&h_cycle, (n_slots + 4) * sizeof(unsigned long long)));
+    SGML_CUDA(cudaMallocHost((void**)&h_flag, 4 * sizeof(int)));
+
+    const uint64_t T = g.total;
+    r = alloc(T);
+    utot = alloc(T);
+    A = alloc(T);
+    B = alloc(T);
+
+    Nl.resize(n);
+    for (int v = 0; v < n; ++v) Nl[v] = (1 << (n - v)) + 1;
+
+    if (opts.engine == 0) {
+        P.assign(n, nullptr);
+        for (int m = 1; m < n; ++m) P[m] = alloc(pow_dim(Nl[m], dim));
+        U.assign(n, {nullptr, nullptr});
+        DU.assign(n, {});
+        for (int v = 1; v < n; ++v) {
+            const uint64_t Sv = pow_dim(Nl[v], dim);
+            U[v][0] = alloc(Sv);
+            U[v][1] = alloc(Sv);
+            const int cmax = relax_count(n, cfg.n_r, v);
+            for (int k = 0; k + 1 < cmax; ++k) DU[v].push_back(alloc(Sv));
+        }
+        if (has_sigma) {
+            S.assign(n, nullptr);
+            S[0] = alloc(T);
+            for (int m = 1; m < n; ++m) S[m] = alloc(pow_dim(Nl[m], dim));
+        }
+    } else {
+        ensure_literal();
+        if (has_sigma) {
+            Lsig.assign(n, nullptr);
+            for (int v = 0; v < n; ++v) Lsig[v] = alloc(T);
+        }
+    }
+    if (has_sigma) load_sigma(sigma_dev);
+    SGML_CUDA(cudaGetLastError());
+    SGML_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// cycle.cpp:117-133: sigma restricted per level with even (all-Neumann)
+// ghosts; every level must stay positive.  The compact engine keeps level v
+// only on its subset nodes (pyramid); positivity of the full
+// field is checked at level 0, every coarser value is a positive average.
+void sgml_solver::load_sigma(const double* sigma_dev) {
+    const int dim = g.dim, n = g.n;
+    const uint64_t T = g.total;
+    const cudaStream_t s = ctx->stream;
+    sgml_bc even{};
+    for (int f = 0; f < 6; ++f) even.kind[f] = 1;
+    const BcDev ev = to_dev(even);
+    SGML_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
+    if (opts.engine == 0) {
+        if (sigma_dev != S[0])
+            SGML_CUDA(cudaMemcpyAsync(S[0], sigma_dev, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        launch(SGML_CLASS_OTHER, [&] { launch_check_positive(S[0], T, d_flag, s); });
+        for (int m = 1; m < n; ++m) {
+            launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid_step(dim, S[m - 1], Nl[m - 1], S[m], Nl[m], ev, s); });
+            launch(SGML_CLASS_OTHER, [&] { launch_check_positive(S[m], pow_dim(Nl[m], dim), d_flag, s); });
+        }
+    } else {
+        for (int v = 0; v < n; ++v) {
+            // restriction_into(sigma, v, even): v literal passes ending in Lsig[v]
+            if (v == 0) {
+                if (sigma_dev != Lsig[0])
+                    SGML_CUDA(cudaMemcpyAsync(Lsig[0], sigma_dev, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            } else {
+                const double* src = Lsig[0];
+                double* dst = (v % 2 == 1) ? Lsig[v] : Lscr;
+                for (int m = 0; m < v; ++m) {
+                    launch(SGML_CLASS_LITERAL, [&] { launch_restrict_pass(dim, src, dst, g.N, 1 << m, ev, s); });
+                    src = dst;
+                    dst = (dst == Lsig[v]) ? Lscr : Lsig[v];
+                }
+            }
+            launch(SGML_CLASS_OTHER, [&] { launch_check_positive(Lsig[v], T, d_flag, s); });
+        }
+    }
+    SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SGML_CUDA(cudaStreamSynchronize(s));
+    SGML_CUDA(cudaGetLastError());
+    if (h_flag[0]) fail(SGML_EINVAL, "restrict_sigma_levels: coefficient must stay positive");
+}
+
+void sgml_solver::ensure_literal() {
+    if (Lg) return;
+    const uint64_t T = g.total;
+    Lg = alloc(T); Lscr = alloc(T); Lu = alloc(T); Lup = alloc(T); Ldu = alloc(T); Ldup = alloc(T);
+}
+
+// ---------------------------------------------------------------------------
+// one cycle
+// ---------------------------------------------------------------------------
+
+const double* sgml_solver::cycle(const double* source, bool homogeneous) {
+    return opts.engine == 0 ? cycle_compact(source, homogeneous) : cycle_literal(source, homogeneous);
+}
+
+const double* sgml_solver::cycle_compact(const double* source, bool homogeneous) {
+    const int dim = g.dim, n = g.n, N = g.N;
+    const cudaStream_t s = ctx->stream;
+    const uint64_t T = g.total;
+    unsigned long long* diag = d_cycle;
+    int* flag = d_flag;
+
+    // restriction pyramid of the cycle's source (once per cycle, F4)
+    for (int m = 0; m + 1 < n; ++m)
+        launch(SGML_CLASS_PYRAMID, [&] {
+            launch_pyramid_step(dim, m == 0 ? source : P[m], Nl[m], P[m + 1], Nl[m + 1], bc, s);
+        });
+    auto gsrc = [&](int v) { return v == 0 ? source : (const double*)P[v]; };
+    auto sig = [&](int v) { return has_sigma ? (const double*)S[v] : nullptr; };
+
+    int slot = 0;
+    bool first = true;          // no pass has run in this cycle yet
+    double* base = A;           // full-grid state after the last level-0 visit
+    double* other = B;
+    bool base_zero = true;      // state.u entered the cycle zeroed
+
+    auto relax_level = [&](int v, double* in, int c, double* p0, double* p1) -> double* {
+        const RelaxConst rc = relax_const(dim, v, g.h, a, cfg.safety, homogeneous);
+        double* cur = in;
+        for (int p = 1; p <= c; ++p) {
+            double* out = cur == p0 ? p1 : p0;
+            double* duo = (v > 0 && p < c) ? DU[v][p - 1] : nullptr;
+            launch(v == 0 ? SGML_CLASS_RELAX0 : SGML_CLASS_RELAX_COARSE, [&] {
+                launch_relax_compact(dim, has_sigma, out, duo, cur, gsrc(v), sig(v), Nl[v], rc, bc,
+                                     diag + slot, flag, s);
+            });
+            ++slot;
+            cur = out;
+            first = false;
+        }
+        return cur;
+    };
+
+    for (int v1 = n - 1; v1 >= 0; --v1) {
+        const int c = relax_count(n, cfg.n_r, v1);
+        Chain chain{};
+        chain.count = 0;
+        const double* ufinal = nullptr;  // last pass output of level v+1
+        for (int v = v1; v >= 1; --v) {
+            double* in = U[v][0];
+            const uint64_t Sv = pow_dim(Nl[v], dim);
+            if (first) {
+                SGML_CUDA(cudaMemsetAsync(in, 0, Sv * sizeof(double), s));
+            } else {
+                if (chain.count + (c - 1) > kMaxChain) {
+                    // fold the pending increments into a full-grid base
+                    launch(SGML_CLASS_MATERIALIZE, [&] {
+                        launch_materialize(dim, other, N, 0, base, N, base_zero, ufinal, Nl[v + 1],
+                                           v + 1, chain, bc, homogeneous, flag, s);
+                    });
+                    std::swap(base, other);
+                    base_zero = false;
+                    chain.count = 0;
+                    ufinal = nullptr;  // already folded into base
+                }
+                launch(SGML_CLASS_MATERIALIZE, [&] {
+                    launch_materialize(dim, in, Nl[v], v, base, N, base_zero, ufinal,
+                                       v + 1 < n ? Nl[v + 1] : 0, 1, chain, bc, homogeneous, flag, s);
+                });
+            }
+            ufinal = relax_level(v, in, c, U[v][0], U[v][1]);
+            for (int k = 0; k + 1 < c; ++k) {
+                chain.level[chain.count] = v;
+                chain.Nl[chain.count] = Nl[v];
+                chain.du[chain.count] = DU[v][k];
+                ++chain.count;
+            }
+        }
+        // level 0 visit of this tooth
+        double* in0;
+        if (first) {
+            SGML_CUDA(cudaMemsetAsync(base, 0, T * sizeof(double), s));
+            in0 = base;
+        } else if (v1 >= 1) {
+            launch(SGML_CLASS_MATERIALIZE, [&] {
+                launch_materialize(dim, other, N, 0, base, N, base_zero, ufinal, Nl.size() > 1 ? Nl[1] : 0,
+                                   1, chain, bc, homogeneous, flag, s);
+            });
+            in0 = other;
+        } else {
+            in0 = base;
+        }
+        base = relax_level(0, in0, c, A, B);
+        other = base == A ? B : A;
+        base_zero = false;
+    }
+    // tail Relax(0, min(n_r, 2^n))
+    base = relax_level(0, base, relax_count(n, cfg.n_r, 0), A, B);
+    return base;
+}
+
+const double* sgml_solver::cycle_literal(const double* source, bool homogeneous) {
+    const int dim = g.dim, n = g.n, N = g.N;
+    const cudaStream_t s = ctx->stream;
+    const uint64_t T = g.total;
+    ensure_literal();
+    // state.u / u_prev zeroed by solve (cycle.cpp:179-180); du reset at the
+    // first relax step
+    SGML_CUDA(cudaMemsetAsync(Lu, 0, T * sizeof(double), s));
+    SGML_CUDA(cudaMemsetAsync(Lup, 0, T * sizeof(double), s));
+    double *u = Lu, *up = Lup, *du = Ldu, *dup = Ldup;
+    int slot = 0, current = -1;
+    for (int v1 = n - 1; v1 >= -1; --v1) {
+        const bool tail = v1 < 0;
+        const int c = tail ? relax_count(n, cfg.n_r, 0) : relax_count(n, cfg.n_r, v1);
+        for (int v = tail ? 0 : v1; v >= 0; --v) {
+            if (!tail) {
+                // restriction_into(source, v, bc, g, scratch) (kernels.cpp:305-325)
+                if (v == 0) {
+                    SGML_CUDA(cudaMemcpyAsync(Lg, source, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
+                } else {
+                    const double* src = source;
+                    double* dst = (v % 2 == 1) ? Lg : Lscr;
+                    for (int m = 0; m < v; ++m) {
+                        launch(SGML_CLASS_LITERAL, [&] { launch_restrict_pass(dim, src, dst, N, 1 << m, bc, s); });
+                        src = dst;
+                        dst = (dst == Lg) ? Lscr : Lg;
+                    }
+                }
+            }
+            if (v != current) {  // SolveState::reset_level
+                SGML_CUDA(cudaMemsetAsync(du, 0, T * sizeof(double), s));
+                SGML_CUDA(cudaMemsetAsync(dup, 0, T * sizeof(double), s));
+                current = v;
+            }
+            const RelaxConst rc = relax_const(dim, v, g.h, a, cfg.safety, homogeneous);
+            for (int p = 0; p < c; ++p) {
+                std::swap(u, up);
+                std::swap(du, dup);
+                launch(SGML_CLASS_LITERAL, [&] {
+                    launch_relax_literal(dim, has_sigma, u, du, up, dup, Lg, has_sigma ? Lsig[v] : nullptr,
+                                         N, v, rc, bc, d_cycle + slot, d_flag, s);
+                });
+                ++slot;
+            }
+            if (tail) break;
+        }
+    }
+    Lu = u; Lup = up; Ldu = du; Ldup = dup;
+    return Lu;
+}
+
+void sgml_solver::zero_mean(double* field) {
+    const double mean = trapezoid_mean_host(ctx, g, field);
+    launch(SGML_CLASS_OTHER, [&] { launch_sub_scalar(field, g.total, mean, ctx->stream); });
+}
+
+// ---------------------------------------------------------------------------
+// solve (cycle.cpp:140-247)
+// ---------------------------------------------------------------------------
+
+void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
+    SGML_CUDA(cudaSetDevice(ctx->device));
+    const cudaStream_t s = ctx->stream;
+    const uint64_t T = g.total;
+    const int dim = g.dim;
+    launches = 0;
+    for (int k = 0; k < 8; ++k) { cls_ms[k] = 0.0; cls_n[k] = 0; }
+    spans.clear();
+    evused = 0;
+
+    if (!tev0) {
+        SGML_CUDA(cudaEventCreate(&tev0));
+        SGML_CUDA(cudaEventCreate(&tev1));
+    }
+    cudaEvent_t ev0 = tev0, ev1 = tev1;
+    SGML_CUDA(cudaEventRecord(ev0, s));
+
+    // input validation (cycle.cpp:150-152)
+    SGML_CUDA(cudaMemsetAsync(d_flag, 0, 4 * sizeof(int), s));
+    launch(SGML_CLASS_OTHER, [&] { launch_check_finite(f, T, d_flag, s); });
+    SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SGML_CUDA(cudaStreamSynchronize(s));
+    if (h_flag[0]) fail(SGML_EINVAL, "solve: source contains non-finite values");
+
+    rep->n_rows = 0;
+    rep->n_trace = 0;
+    rep->converged = rep->nan_detected = rep->stagnated = 0;
+    rep->normalization = 0.0;
+    rep->node_updates = 0;
+
+    SGML_CUDA(cudaMemcpyAsync(r, f, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    SGML_CUDA(cudaMemsetAsync(utot, 0, T * sizeof(double), s));
+    if (all_neumann) zero_mean(r);
+
+    // norm = max|r|
+    unsigned long long* d_rmax = d_cycle + n_slots;
+    SGML_CUDA(cudaMemsetAsync(d_rmax, 0, sizeof(unsigned long long), s));
+    launch(SGML_CLASS_OTHER, [&] { launch_max_abs(r, T, d_rmax, s); });
+    SGML_CUDA(cudaMemcpyAsync(h_cycle + n_slots, d_rmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    SGML_CUDA(cudaStreamSynchronize(s));
+    double norm;
+    std::memcpy(&norm, &h_cycle[n_slots], sizeof(double));
+    bool norm_pending = norm == 0.0;
+
+    const double inv_h2 = 1.0 / (g.h * g.h);
+    const double pref = dim == 2 ? 0.5 : 3.0 / 13.0;
+    const double* sig0 = has_sigma ? (opts.engine == 0 ? S[0] : Lsig[0]) : nullptr;
+    uint64_t work = 0;
+    double prev_res = std::numeric_limits<double>::infinity();
+    int non_decreasing = 0;
+    const bool badstep = !(cfg.safety > 0.0);
+
+    for (int cyc = 0; cyc < cfg.max_cycles; ++cyc) {
+        const bool homogeneous = cyc > 0;
+        if (all_neumann && cyc > 0) zero_mean(r);
+        if (badstep) {  // kernels.cpp:197,343: the first pass throws
+            rep->nan_detected = 1;
+            rep->converged = 0;
+            break;
+        }
+        SGML_CUDA(cudaMemsetAsync(d_cycle, 0, (n_slots + 1) * sizeof(unsigned long long), s));
+        SGML_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
+        const double* e = cycle(r, homogeneous);
+        // kernel_error check before the recurrence touches u_tot and r
+        SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+        if (h_flag[0]) {
+            // no row for this cycle (cycle.cpp:186-190)
+            rep->nan_detected = 1;
+            rep->converged = 0;
+            break;
+        }
+        // u_tot += e; r -= A(e) + a e; r = 0 on Dirichlet; max|r|
+        launch(SGML_CLASS_RESIDUAL, [&] {
+            launch_residual(dim, has_sigma, r, e, utot, sig0, g.N, inv_h2, pref, a, bc, d_rmax, s);
+        });
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaMemcpyAsync(h_cycle, d_cycle, (n_slots + 1) * sizeof(unsigned long long),
+                                  cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+        if (opts.timing) harvest_spans();
+
+        const double inv_norm = !norm_pending && norm > 0.0 ? 1.0 / norm : 1.0;
+        const int64_t trace_mark = rep->n_trace;
+        for (int p = 0; p < n_slots; ++p) {
+            double d;
+            std::memcpy(&d, &h_cycle[p], sizeof(double));
+            if (rep->n_trace < rep->trace_cap)
+                rep->trace[rep->n_trace] = sgml_diag_sample{cyc, pass_index[p], pass_level[p], 0, d * inv_norm};
+            rep->n_trace++;
+        }
+        work += units_per_cycle;
+        rep->node_updates += units_per_cycle * T;
+
+        double r_max;
+        std::memcpy(&r_max, &h_cycle[n_slots], sizeof(double));
+        if (norm_pending) {
+            norm = r_max;
+            norm_pending = false;
+            if (norm == 0.0) {
+                if (rep->n_rows < rep->rows_cap)
+                    rep->rows[rep->n_rows] = sgml_cycle_record{cyc, 0, work, 0.0, 0.0, 0.0};
+                rep->n_rows++;
+                rep->converged = 1;
+                break;
+            }
+            for (int64_t t = trace_mark; t < rep->n_trace && t < rep->trace_cap; ++t)
+                rep->trace[t].value /= norm;
+        }
+        const double res = r_max / norm;
+        double diag_min = std::numeric_limits<double>::infinity();
+        for (int64_t t = trace_mark; t < rep->n_trace && t < rep->trace_cap; ++t)
+            diag_min = std::min(diag_min, rep->trace[t].value);
+        sgml_cycle_record row{cyc, 0, work, res, diag_min, 0.0};
+        if (rep->hook) {
+            sgml_field view;
+            view.ctx = ctx;
+            view.grid = g;
+            view.d = utot;
+            double l1 = 0.0;
+            if (rep->hook(rep->hook_user, cyc, &view, &l1)) {
+                row.has_l1 = 1;
+                row.l1_error = l1;
+            }
+        }
+        if (rep->n_rows < rep->rows_cap) rep->rows[rep->n_rows] = row;
+        rep->n_rows++;
+
+        if (!std::isfinite(res)) { rep->nan_detected = 1; break; }
+        if (res <= cfg.tol) { rep->converged = 1; break; }
+        if (res >= prev_res) {
+            if (++non_decreasing >= 3) { rep->stagnated = 1; break; }
+        } else {
+            non_decreasing = 0;
+        }
+        prev_res = res;
+    }
+    rep->normalization = norm_pending ? 0.0 : norm;
+    if (all_neumann && a == 0.0) zero_mean(utot);  // pure_neumann_pin
+    if (u_out && u_out != utot)
+        SGML_CUDA(cudaMemcpyAsync(u_out, utot, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    SGML_CUDA(cudaEventRecord(ev1, s));
+    SGML_CUDA(cudaEventSynchronize(ev1));
+    float ms = 0.f;
+    SGML_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    if (opts.timing) harvest_spans();
+    rep->device_ms = ms;
+    rep->kernel_launches = launches;
+    for (int k = 0; k < 8; ++k) {
+        rep->class_ms[k] = cls_ms[k];
+        rep->class_launches[k] = cls_n[k];
+    }
+    evused = 0;
+    SGML_CUDA(cudaGetLastError());
+}

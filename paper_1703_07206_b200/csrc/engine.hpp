@@ -1,0 +1,149 @@
+// engine.hpp — host side of the B200 SGML engine (C++, behind the C-ABI).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/sgml_b200.h"
+#include "device.cuh"
+#include "internal.hpp"
+
+// ---- opaque C-ABI objects ----------------------------------------------
+struct sgml_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    unsigned long long* d_slots = nullptr;  // generic reduction slots
+    int* d_flags = nullptr;
+    unsigned long long* h_slots = nullptr;  // pinned mirrors
+    int* h_flags = nullptr;
+    double* h_stage = nullptr;              // pinned staging for host reductions
+    size_t h_stage_bytes = 0;
+    // sgml_solve's engine cache (one problem shape), see capi.cpp
+    struct sgml_solver* cached = nullptr;
+    std::string cached_key;
+    std::mutex mu;
+};
+
+struct sgml_field {
+    sgml_ctx* ctx = nullptr;
+    sgml_grid grid{};
+    double* d = nullptr;
+};
+
+namespace sgmlb {
+
+// error plumbing ----------------------------------------------------------
+struct Error {
+    int code;
+    std::string msg;
+};
+void set_error(const std::string& msg);
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define SGML_CUDA(call) ::sgmlb::cuda_check((call), #call)
+
+BcDev to_dev(const sgml_bc& bc);
+bool any_dirichlet(const sgml_bc& bc, int dim);
+sgml_grid make_grid_or_throw(int dim, int n);
+int relax_count(int n, int n_r, int v1);
+RelaxConst relax_const(int dim, int level, double h, double a, double safety, bool homogeneous);
+double* dalloc(size_t count);
+void dfree(double* p);
+
+// serial Kahan trapezoid mean over a host copy (kernels.cpp:367-386)
+double trapezoid_mean_host(sgml_ctx* ctx, const sgml_grid& g, const double* dfield);
+
+}  // namespace sgmlb
+
+// ---- the engine ---------------------------------------------------------
+struct sgml_solver {
+    sgml_ctx* ctx = nullptr;
+    sgml_grid g{};
+    sgml_bc bc_host{};
+    sgmlb::BcDev bc{};
+    bool all_neumann = false;
+    double a = 0.0;
+    bool has_sigma = false;
+    sgml_solver_cfg cfg{};
+    sgml_solver_opts opts{};
+    uint64_t units_per_cycle = 0;
+    int n_slots = 0;
+
+    // schedule flattened: for every relax pass, its (level, pass_index)
+    std::vector<int> pass_level, pass_index;
+
+    // full-grid buffers
+    double* r = nullptr;
+    double* utot = nullptr;
+    double* A = nullptr;
+    double* B = nullptr;
+    double* fin = nullptr;   // staging for host-buffer solves (sgml_solve)
+    // level-compact buffers (index = level)
+    std::vector<int> Nl;
+    std::vector<double*> P;                   // P[m], m >= 1 (P[0] is r)
+    std::vector<double*> S;                   // S[m] sigma pyramid, S[0] full sigma
+    std::vector<std::array<double*, 2>> U;    // U[v][0..1], v >= 1
+    std::vector<std::vector<double*>> DU;     // DU[v][k]
+    // literal-engine buffers (lazily allocated)
+    double *Lg = nullptr, *Lscr = nullptr, *Lu = nullptr, *Lup = nullptr, *Ldu = nullptr,
+           *Ldup = nullptr;
+    std::vector<double*> Lsig;                // full sigma levels
+    // per-cycle device scratch: [0..n_slots) diag, n_slots = rmax
+    unsigned long long* d_cycle = nullptr;
+    int* d_flag = nullptr;
+    unsigned long long* h_cycle = nullptr;
+    int* h_flag = nullptr;
+    uint64_t bytes = 0;
+    uint64_t launches = 0;
+    // CUDA graphs of the cycle launch sequence, keyed by homogeneous flag
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    // per-class device timing (opts.timing): event pairs harvested per cycle
+    struct Span {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<cudaEvent_t> evpool;
+    size_t evused = 0;
+    std::vector<Span> spans;
+    cudaEvent_t tev0 = nullptr, tev1 = nullptr;  // whole-solve timing
+    double cls_ms[8] = {0};
+    uint64_t cls_n[8] = {0};
+
+    ~sgml_solver();
+    void build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double a_, const double* sigma_dev,
+               const sgml_solver_cfg& cfg_, const sgml_solver_opts& opts_);
+    // (re)load the coefficient: sigma pyramid / literal sigma levels + positivity
+    void load_sigma(const double* sigma_dev);
+    // device buffer that receives an uploaded coefficient (level 0)
+    double* sigma_level0() { return opts.engine == 0 ? S[0] : Lsig[0]; }
+    // timed launch: records an event pair around fn when opts.timing
+    template <typename F>
+    void launch(int cls, F&& fn) {
+        ++launches;
+        if (!opts.timing) {
+            fn();
+            return;
+        }
+        Span sp{cls, next_event(), next_event()};
+        cudaEventRecord(sp.a, ctx->stream);
+        fn();
+        cudaEventRecord(sp.b, ctx->stream);
+        spans.push_back(sp);
+    }
+    cudaEvent_t next_event();
+    void harvest_spans();  // call after a stream synchronize
+    // cycle.cpp:140-247
+    void run(const double* f_dev, double* u_out_dev, sgml_report* rep);
+    // one cycle of the schedule on `source`, result (state.u) returned
+    const double* cycle(const double* source, bool homogeneous);
+    const double* cycle_compact(const double* source, bool homogeneous);
+    const double* cycle_literal(const double* source, bool homogeneous);
+    void ensure_literal();
+    void zero_mean(double* field);
+    double* alloc(size_t count);
+};
