@@ -310,9 +310,8 @@ int sgml_residual_update(sgml_field* r, const sgml_field* e, const sgml_field* s
         sgml_ctx* ctx = r->ctx;
         activate(ctx);
         const sgml_grid& g = r->grid;
-        launch_residual(g.dim, sigma != nullptr, r->d, e->d, nullptr, sigma ? sigma->d : nullptr, g.N,
-                        1.0 / (g.h * g.h), g.dim == 2 ? 0.5 : 3.0 / 13.0, a, to_dev(*bc), nullptr,
-                        ctx->stream);
+        launch_residual_tiled(g.dim, sigma != nullptr, r->d, e->d, nullptr, sigma ? sigma->d : nullptr, g.N,
+                              relax_const(g.dim, 0, g.h, a, 1.0, false), to_dev(*bc), nullptr, ctx->stream);
         SGML_CUDA(cudaGetLastError());
         SGML_CUDA(cudaStreamSynchronize(ctx->stream));
     });

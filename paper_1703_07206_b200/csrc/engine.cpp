@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
@@ -176,6 +177,7 @@ sgml_solver::~sgml_solver() {
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
     if (tev0) cudaEventDestroy(tev0);
     if (tev1) cudaEventDestroy(tev1);
+    if (d_chain) cudaFree(d_chain);
     if (d_cycle) cudaFree(d_cycle);
     if (d_flag) cudaFree(d_flag);
     if (h_cycle) cudaFreeHost(h_cycle);
@@ -261,6 +263,20 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
             const int cmax = relax_count(n, cfg.n_r, v);
             for (int k = 0; k + 1 < cmax; ++k) DU[v].push_back(alloc(Sv));
         }
+        // tooth v1's increments in application order: levels v1..1, passes 1..c-1
+        std::vector<ChainEntry> entries;
+        tooth_off.assign(n, 0);
+        for (int v1 = 0; v1 < n; ++v1) {
+            tooth_off[v1] = (int)entries.size();
+            const int c = relax_count(n, cfg.n_r, v1);
+            for (int v = v1; v >= 1; --v)
+                for (int k = 0; k + 1 < c; ++k) entries.push_back(ChainEntry{DU[v][k], v, Nl[v]});
+        }
+        if (!entries.empty()) {
+            SGML_CUDA(cudaMalloc((void**)&d_chain, entries.size() * sizeof(ChainEntry)));
+            SGML_CUDA(cudaMemcpy(d_chain, entries.data(), entries.size() * sizeof(ChainEntry),
+                                 cudaMemcpyHostToDevice));
+        }
         if (has_sigma) {
             S.assign(n, nullptr);
             S[0] = alloc(T);
@@ -295,7 +311,7 @@ void sgml_solver::load_sigma(const double* sigma_dev) {
             SGML_CUDA(cudaMemcpyAsync(S[0], sigma_dev, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
         launch(SGML_CLASS_OTHER, [&] { launch_check_positive(S[0], T, d_flag, s); });
         for (int m = 1; m < n; ++m) {
-            launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid_step(dim, S[m - 1], Nl[m - 1], S[m], Nl[m], ev, s); });
+            launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid2(dim, S[m - 1], Nl[m - 1], S[m], Nl[m], ev, s); });
             launch(SGML_CLASS_OTHER, [&] { launch_check_positive(S[m], pow_dim(Nl[m], dim), d_flag, s); });
         }
     } else {
@@ -346,7 +362,7 @@ const double* sgml_solver::cycle_compact(const double* source, bool homogeneous)
     // restriction pyramid of the cycle's source (once per cycle, F4)
     for (int m = 0; m + 1 < n; ++m)
         launch(SGML_CLASS_PYRAMID, [&] {
-            launch_pyramid_step(dim, m == 0 ? source : P[m], Nl[m], P[m + 1], Nl[m + 1], bc, s);
+            launch_pyramid2(dim, m == 0 ? source : P[m], Nl[m], P[m + 1], Nl[m + 1], bc, s);
         });
     auto gsrc = [&](int v) { return v == 0 ? source : (const double*)P[v]; };
     auto sig = [&](int v) { return has_sigma ? (const double*)S[v] : nullptr; };
@@ -364,8 +380,8 @@ const double* sgml_solver::cycle_compact(const double* source, bool homogeneous)
             double* out = cur == p0 ? p1 : p0;
             double* duo = (v > 0 && p < c) ? DU[v][p - 1] : nullptr;
             launch(v == 0 ? SGML_CLASS_RELAX0 : SGML_CLASS_RELAX_COARSE, [&] {
-                launch_relax_compact(dim, has_sigma, out, duo, cur, gsrc(v), sig(v), Nl[v], rc, bc,
-                                     diag + slot, flag, s);
+                launch_relax_tiled(dim, has_sigma, out, duo, cur, gsrc(v), sig(v), Nl[v], rc, bc,
+                                   diag + slot, flag, s);
             });
             ++slot;
             cur = out;
@@ -376,8 +392,9 @@ const double* sgml_solver::cycle_compact(const double* source, bool homogeneous)
 
     for (int v1 = n - 1; v1 >= 0; --v1) {
         const int c = relax_count(n, cfg.n_r, v1);
-        Chain chain{};
-        chain.count = 0;
+        // pending increments of this tooth: d_chain[tooth_off[v1] + start, + count)
+        int start = 0, count = 0;
+        auto chain_at = [&]() { return d_chain ? d_chain + tooth_off[v1] + start : nullptr; };
         const double* ufinal = nullptr;  // last pass output of level v+1
         for (int v = v1; v >= 1; --v) {
             double* in = U[v][0];
@@ -385,29 +402,27 @@ const double* sgml_solver::cycle_compact(const double* source, bool homogeneous)
             if (first) {
                 SGML_CUDA(cudaMemsetAsync(in, 0, Sv * sizeof(double), s));
             } else {
-                if (chain.count + (c - 1) > kMaxChain) {
+                if (count + (c - 1) > kMaxChain) {
                     // fold the pending increments into a full-grid base
+                    const ChainEntry* ch = chain_at();
                     launch(SGML_CLASS_MATERIALIZE, [&] {
-                        launch_materialize(dim, other, N, 0, base, N, base_zero, ufinal, Nl[v + 1],
-                                           v + 1, chain, bc, homogeneous, flag, s);
+                        launch_materialize4(dim, other, N, 0, base, N, base_zero, ufinal, Nl[v + 1],
+                                            v + 1, ch, count, bc, homogeneous, flag, s);
                     });
                     std::swap(base, other);
                     base_zero = false;
-                    chain.count = 0;
+                    start += count;
+                    count = 0;
                     ufinal = nullptr;  // already folded into base
                 }
+                const ChainEntry* ch = chain_at();
                 launch(SGML_CLASS_MATERIALIZE, [&] {
-                    launch_materialize(dim, in, Nl[v], v, base, N, base_zero, ufinal,
-                                       v + 1 < n ? Nl[v + 1] : 0, 1, chain, bc, homogeneous, flag, s);
+                    launch_materialize4(dim, in, Nl[v], v, base, N, base_zero, ufinal,
+                                        v + 1 < n ? Nl[v + 1] : 0, 1, ch, count, bc, homogeneous, flag, s);
                 });
             }
             ufinal = relax_level(v, in, c, U[v][0], U[v][1]);
-            for (int k = 0; k + 1 < c; ++k) {
-                chain.level[chain.count] = v;
-                chain.Nl[chain.count] = Nl[v];
-                chain.du[chain.count] = DU[v][k];
-                ++chain.count;
-            }
+            count += c - 1;
         }
         // level 0 visit of this tooth
         double* in0;
@@ -415,9 +430,10 @@ const double* sgml_solver::cycle_compact(const double* source, bool homogeneous)
             SGML_CUDA(cudaMemsetAsync(base, 0, T * sizeof(double), s));
             in0 = base;
         } else if (v1 >= 1) {
+            const ChainEntry* ch = chain_at();
             launch(SGML_CLASS_MATERIALIZE, [&] {
-                launch_materialize(dim, other, N, 0, base, N, base_zero, ufinal, Nl.size() > 1 ? Nl[1] : 0,
-                                   1, chain, bc, homogeneous, flag, s);
+                launch_materialize4(dim, other, N, 0, base, N, base_zero, ufinal, Nl.size() > 1 ? Nl[1] : 0,
+                                    1, ch, count, bc, homogeneous, flag, s);
             });
             in0 = other;
         } else {
@@ -566,7 +582,8 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
         }
         // u_tot += e; r -= A(e) + a e; r = 0 on Dirichlet; max|r|
         launch(SGML_CLASS_RESIDUAL, [&] {
-            launch_residual(dim, has_sigma, r, e, utot, sig0, g.N, inv_h2, pref, a, bc, d_rmax, s);
+            launch_residual_tiled(dim, has_sigma, r, e, utot, sig0, g.N,
+                                  relax_const(dim, 0, g.h, a, cfg.safety, false), bc, d_rmax, s);
         });
         SGML_CUDA(cudaGetLastError());
         SGML_CUDA(cudaMemcpyAsync(h_cycle, d_cycle, (n_slots + 1) * sizeof(unsigned long long),

@@ -89,6 +89,8 @@ struct sgml_solver {
     std::vector<double*> S;                   // S[m] sigma pyramid, S[0] full sigma
     std::vector<std::array<double*, 2>> U;    // U[v][0..1], v >= 1
     std::vector<std::vector<double*>> DU;     // DU[v][k]
+    sgmlb::ChainEntry* d_chain = nullptr;     // per-tooth pending-increment lists
+    std::vector<int> tooth_off;               // offset of tooth v1's list in d_chain
     // literal-engine buffers (lazily allocated)
     double *Lg = nullptr, *Lscr = nullptr, *Lu = nullptr, *Lup = nullptr, *Ldu = nullptr,
            *Ldup = nullptr;
