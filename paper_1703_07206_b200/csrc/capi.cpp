@@ -310,8 +310,8 @@ int sgml_residual_update(sgml_field* r, const sgml_field* e, const sgml_field* s
         sgml_ctx* ctx = r->ctx;
         activate(ctx);
         const sgml_grid& g = r->grid;
-        launch_residual_tiled(g.dim, sigma != nullptr, r->d, e->d, nullptr, sigma ? sigma->d : nullptr, g.N,
-                              relax_const(g.dim, 0, g.h, a, 1.0, false), to_dev(*bc), nullptr, ctx->stream);
+        launch_residual(g.dim, sigma != nullptr, r->d, e->d, nullptr, sigma ? sigma->d : nullptr, g.N,
+                        1.0 / (g.h * g.h), g.dim == 2 ? 0.5 : 3.0 / 13.0, a, to_dev(*bc), nullptr, ctx->stream);
         SGML_CUDA(cudaGetLastError());
         SGML_CUDA(cudaStreamSynchronize(ctx->stream));
     });
@@ -425,8 +425,7 @@ int sgml_single_cycle(sgml_ctx* ctx, sgml_field* state_u, const sgml_field* sour
         }
         SGML_CUDA(cudaMemsetAsync(sv.d_cycle, 0, (sv.n_slots + 1) * sizeof(unsigned long long), s));
         SGML_CUDA(cudaMemsetAsync(sv.d_flag, 0, sizeof(int), s));
-        const double* e = sv.cycle(source->d, homogeneous != 0);
-        SGML_CUDA(cudaMemcpyAsync(state_u->d, e, g.total * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        sv.cycle_dense(source->d, state_u->d, homogeneous != 0);
         SGML_CUDA(cudaMemcpyAsync(sv.h_cycle, sv.d_cycle, sv.n_slots * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaMemcpyAsync(sv.h_flag, sv.d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -522,14 +521,14 @@ int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f
             ctx->cached_key = key;
         } else if (sigma_host) {
             sgml_solver* sv = ctx->cached;
-            SGML_CUDA(cudaMemcpyAsync(sv->sigma_level0(), sigma_host, bytes, cudaMemcpyHostToDevice, s));
-            sv->load_sigma(sv->sigma_level0());
+            SGML_CUDA(cudaMemcpyAsync(sv->sigma_stage(), sigma_host, bytes, cudaMemcpyHostToDevice, s));
+            sv->load_sigma(sv->sigma_stage());
         }
         sgml_solver* sv = ctx->cached;
         SGML_CUDA(cudaMemcpyAsync(sv->fin, f_host, bytes, cudaMemcpyHostToDevice, s));
         sv->run(sv->fin, nullptr, rep);
         if (u_host_out)
-            SGML_CUDA(cudaMemcpyAsync(u_host_out, sv->utot, bytes, cudaMemcpyDeviceToHost, s));
+            SGML_CUDA(cudaMemcpyAsync(u_host_out, sv->result(), bytes, cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -265,3 +265,112 @@ __device__ __forceinline__ void block_or_commit(int bad, int* flag) {
 }
 
 }  // namespace sgmlb
+
+// ---------------------------------------------------------------------------
+// Ghost-extended, padded level arrays (compact engine storage)
+//
+// A level array with N data nodes per axis is stored with one ghost layer on
+// every side (Ne = N + 2 cells per axis) and an even row pitch Px >= Ne, so
+// that every row starts 16-byte aligned and TMA can stream tiles.  Data node
+// (i, j, k), i in [0, N), sits at cell (i+1, j+1, k+1).  Ghost cells hold
+// the even mirror of the data (u(-1) = u(1), u(N) = u(N-2), per axis); every
+// kernel that writes a node at data index 1 or N-2 also writes its mirror
+// cells.  The even mirror is the reference's ghost value across Neumann
+// faces (stencil.cpp:52-85) and for sigma (stencil.cpp:87-90); across a
+// Dirichlet face the reference's odd ghost is only ever read by nodes on
+// that face, which take their Dirichlet value instead, so those cells never
+// influence a result.
+// ---------------------------------------------------------------------------
+namespace sgmlb {
+
+struct ExtLay {
+    int N;            // data nodes per axis
+    int Ne;           // N + 2
+    int Px;           // row pitch in doubles (even)
+    int pad_;
+    long long plane;  // stride of the slowest axis: Px * Ne (3D) or Px (2D)
+};
+
+template <int DIM>
+__device__ __forceinline__ ptrdiff_t eix(const ExtLay& L, int i, int j, int k) {
+    return DIM == 3 ? (ptrdiff_t)(i + 1) + (ptrdiff_t)L.Px * ((j + 1) + (ptrdiff_t)L.Ne * (k + 1))
+                    : (ptrdiff_t)(i + 1) + (ptrdiff_t)L.Px * (j + 1);
+}
+
+// write the even-mirror ghost cells of data node (i, j, k) (rare path)
+template <int DIM>
+__device__ __noinline__ void store_mirrors(double* a, ExtLay L, int i, int j, int k, double v) {
+    const int N = L.N;
+    int ci[3], cj[3], ck[3];
+    int ni = 1, nj = 1, nk = 1;
+    ci[0] = i;
+    cj[0] = j;
+    ck[0] = k;
+    if (i == 1) ci[ni++] = -1;
+    if (i == N - 2) ci[ni++] = N;
+    if (j == 1) cj[nj++] = -1;
+    if (j == N - 2) cj[nj++] = N;
+    if (DIM == 3) {
+        if (k == 1) ck[nk++] = -1;
+        if (k == N - 2) ck[nk++] = N;
+    }
+    for (int ia = 0; ia < ni; ++ia)
+        for (int ib = 0; ib < nj; ++ib)
+            for (int ic = 0; ic < nk; ++ic)
+                if (ia | ib | ic) a[eix<DIM>(L, ci[ia], cj[ib], ck[ic])] = v;
+}
+
+template <int DIM>
+__device__ __forceinline__ void store_ext(double* a, const ExtLay& L, int i, int j, int k, double v) {
+    a[eix<DIM>(L, i, j, k)] = v;
+    const int N = L.N;
+    if (i == 1 || i == N - 2 || j == 1 || j == N - 2 || (DIM == 3 && (k == 1 || k == N - 2)))
+        store_mirrors<DIM>(a, L, i, j, k, v);
+}
+
+// ---- mbarrier / TMA (sm_90+; used on sm_100a) ------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* map, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* map, int c0, int c1,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+}  // namespace sgmlb

@@ -26,6 +26,8 @@
 //   sign of exact zeros (I(0) is not added).
 #include "engine.hpp"
 
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -154,20 +156,71 @@ double trapezoid_mean_host(sgml_ctx* ctx, const sgml_grid& g, const double* dfie
 using namespace sgmlb;
 
 // ---------------------------------------------------------------------------
+// TMA descriptors
+// ---------------------------------------------------------------------------
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        SGML_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) fail(SGML_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+CUtensorMap make_map(int dim, const double* p, const ExtLay& L, const unsigned* box) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {(cuuint64_t)L.Ne, (cuuint64_t)L.Ne, (cuuint64_t)L.Ne};
+    cuuint64_t strides[2] = {(cuuint64_t)L.Px * 8, (cuuint64_t)L.Px * L.Ne * 8};
+    cuuint32_t bx[3] = {box[0], box[1], box[2]};
+    cuuint32_t es[3] = {1, 1, 1};
+    const CUresult rc = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, dim, const_cast<double*>(p), dims,
+                                    strides, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) fail(SGML_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)rc) + ")");
+    return m;
+}
+
+}  // namespace
+
+void sgml_solver::add_maps(const double* p, const ExtLay& L, bool want_u, bool want_g) {
+    unsigned bu[3], bg[3];
+    tile_boxes(g.dim, bu, bg);
+    if (want_u) map_u.emplace_back(p, make_map(g.dim, p, L, bu));
+    if (want_g) map_g.emplace_back(p, make_map(g.dim, p, L, bg));
+}
+
+const CUtensorMap& sgml_solver::umap(const double* p) const {
+    for (const auto& e : map_u)
+        if (e.first == p) return e.second;
+    fail(SGML_ELOGIC, "internal: no TMA descriptor for buffer");
+}
+const CUtensorMap& sgml_solver::gmap(const double* p) const {
+    for (const auto& e : map_g)
+        if (e.first == p) return e.second;
+    fail(SGML_ELOGIC, "internal: no TMA descriptor for buffer");
+}
+
+// ---------------------------------------------------------------------------
 // construction
 // ---------------------------------------------------------------------------
 
 double* sgml_solver::alloc(size_t count) {
     double* p = dalloc(count);
     bytes += std::max<size_t>(count, 1) * sizeof(double);
+    SGML_CUDA(cudaMemsetAsync(p, 0, std::max<size_t>(count, 1) * sizeof(double), ctx->stream));
     return p;
 }
 
 sgml_solver::~sgml_solver() {
     if (ctx) cudaSetDevice(ctx->device);
-    for (auto& ge : graph)
-        if (ge) cudaGraphExecDestroy(ge);
-    dfree(r); dfree(utot); dfree(A); dfree(B); dfree(fin);
+    dfree(r); dfree(utot); dfree(A); dfree(B); dfree(fin); dfree(dense);
     for (size_t m = 1; m < P.size(); ++m) dfree(P[m]);
     for (double* s : S) dfree(s);
     for (size_t v = 1; v < U.size(); ++v) { dfree(U[v][0]); dfree(U[v][1]); }
@@ -185,6 +238,17 @@ sgml_solver::~sgml_solver() {
 }
 
 static uint64_t pow_dim(int N, int dim) { return dim == 2 ? (uint64_t)N * N : (uint64_t)N * N * N; }
+
+void sgml_solver::check_launch(int cls) {
+    static const char* names[] = {"relax0", "relax_coarse", "materialize", "pyramid", "residual",
+                                  "literal", "other", "?"};
+    const cudaError_t e1 = cudaGetLastError();
+    const cudaError_t e2 = cudaStreamSynchronize(ctx->stream);
+    const cudaError_t e = e1 != cudaSuccess ? e1 : e2;
+    if (e != cudaSuccess)
+        fail(SGML_ECUDA, std::string("CUDA error ") + cudaGetErrorString(e) + " in kernel class " +
+                             names[cls & 7] + " (launch #" + std::to_string(launches) + ")");
+}
 
 cudaEvent_t sgml_solver::next_event() {
     if (evused == evpool.size()) {
@@ -243,34 +307,37 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
     SGML_CUDA(cudaMallocHost((void**)&h_flag, 4 * sizeof(int)));
 
     const uint64_t T = g.total;
-    r = alloc(T);
-    utot = alloc(T);
-    A = alloc(T);
-    B = alloc(T);
-
     Nl.resize(n);
     for (int v = 0; v < n; ++v) Nl[v] = (1 << (n - v)) + 1;
 
-    if (opts.engine == 0) {
+    if (compact()) {
+        Lv.resize(n);
+        for (int v = 0; v < n; ++v) Lv[v] = make_ext(dim, Nl[v]);
+        const uint64_t E0 = ext_size(dim, Lv[0]);
+        r = alloc(E0);
+        utot = alloc(E0);
+        A = alloc(E0);
+        B = alloc(E0);
+        dense = alloc(T);
         P.assign(n, nullptr);
-        for (int m = 1; m < n; ++m) P[m] = alloc(pow_dim(Nl[m], dim));
+        for (int m = 1; m < n; ++m) P[m] = alloc(ext_size(dim, Lv[m]));
         U.assign(n, {nullptr, nullptr});
         DU.assign(n, {});
         for (int v = 1; v < n; ++v) {
-            const uint64_t Sv = pow_dim(Nl[v], dim);
-            U[v][0] = alloc(Sv);
-            U[v][1] = alloc(Sv);
+            const uint64_t Ev = ext_size(dim, Lv[v]);
+            U[v][0] = alloc(Ev);
+            U[v][1] = alloc(Ev);
             const int cmax = relax_count(n, cfg.n_r, v);
-            for (int k = 0; k + 1 < cmax; ++k) DU[v].push_back(alloc(Sv));
+            for (int k = 0; k + 1 < cmax; ++k) DU[v].push_back(alloc(Ev));
         }
         // tooth v1's increments in application order: levels v1..1, passes 1..c-1
         std::vector<ChainEntry> entries;
         tooth_off.assign(n, 0);
         for (int v1 = 0; v1 < n; ++v1) {
             tooth_off[v1] = (int)entries.size();
-            const int c = relax_count(n, cfg.n_r, v1);
+            const int cc = relax_count(n, cfg.n_r, v1);
             for (int v = v1; v >= 1; --v)
-                for (int k = 0; k + 1 < c; ++k) entries.push_back(ChainEntry{DU[v][k], v, Nl[v]});
+                for (int k = 0; k + 1 < cc; ++k) entries.push_back(ChainEntry{DU[v][k], Lv[v], v, 0});
         }
         if (!entries.empty()) {
             SGML_CUDA(cudaMalloc((void**)&d_chain, entries.size() * sizeof(ChainEntry)));
@@ -279,10 +346,24 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
         }
         if (has_sigma) {
             S.assign(n, nullptr);
-            S[0] = alloc(T);
-            for (int m = 1; m < n; ++m) S[m] = alloc(pow_dim(Nl[m], dim));
+            for (int m = 0; m < n; ++m) S[m] = alloc(ext_size(dim, Lv[m]));
         }
+        // TMA descriptors: window arrays (relax inputs, sigma) and tile arrays
+        // (sources, residual, u_tot)
+        add_maps(A, Lv[0], true, false);
+        add_maps(B, Lv[0], true, false);
+        add_maps(r, Lv[0], false, true);
+        add_maps(utot, Lv[0], false, true);
+        for (int v = 1; v < n; ++v) {
+            add_maps(U[v][0], Lv[v], true, false);
+            add_maps(U[v][1], Lv[v], true, false);
+            add_maps(P[v], Lv[v], false, true);
+        }
+        if (has_sigma)
+            for (int v = 0; v < n; ++v) add_maps(S[v], Lv[v], true, false);
     } else {
+        r = alloc(T);
+        utot = alloc(T);
         ensure_literal();
         if (has_sigma) {
             Lsig.assign(n, nullptr);
@@ -296,30 +377,27 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
 
 // cycle.cpp:117-133: sigma restricted per level with even (all-Neumann)
 // ghosts; every level must stay positive.  The compact engine keeps level v
-// only on its subset nodes (pyramid); positivity of the full
-// field is checked at level 0, every coarser value is a positive average.
-void sgml_solver::load_sigma(const double* sigma_dev) {
+// only on its subset nodes (pyramid); positivity is checked on
+// the full level-0 field, every coarser value being a positive average.
+void sgml_solver::load_sigma(const double* sigma_dense) {
     const int dim = g.dim, n = g.n;
     const uint64_t T = g.total;
     const cudaStream_t s = ctx->stream;
-    sgml_bc even{};
-    for (int f = 0; f < 6; ++f) even.kind[f] = 1;
-    const BcDev ev = to_dev(even);
     SGML_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
-    if (opts.engine == 0) {
-        if (sigma_dev != S[0])
-            SGML_CUDA(cudaMemcpyAsync(S[0], sigma_dev, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        launch(SGML_CLASS_OTHER, [&] { launch_check_positive(S[0], T, d_flag, s); });
-        for (int m = 1; m < n; ++m) {
-            launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid2(dim, S[m - 1], Nl[m - 1], S[m], Nl[m], ev, s); });
-            launch(SGML_CLASS_OTHER, [&] { launch_check_positive(S[m], pow_dim(Nl[m], dim), d_flag, s); });
-        }
+    if (compact()) {
+        launch(SGML_CLASS_OTHER, [&] { launch_check_positive(sigma_dense, T, d_flag, s); });
+        launch(SGML_CLASS_OTHER, [&] { launch_scatter_ext(dim, sigma_dense, S[0], Lv[0], s); });
+        for (int m = 1; m < n; ++m)
+            launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid_ext(dim, S[m - 1], Lv[m - 1], S[m], Lv[m], s); });
     } else {
+        sgml_bc even{};
+        for (int f = 0; f < 6; ++f) even.kind[f] = 1;
+        const BcDev ev = to_dev(even);
         for (int v = 0; v < n; ++v) {
             // restriction_into(sigma, v, even): v literal passes ending in Lsig[v]
             if (v == 0) {
-                if (sigma_dev != Lsig[0])
-                    SGML_CUDA(cudaMemcpyAsync(Lsig[0], sigma_dev, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
+                if (sigma_dense != Lsig[0])
+                    SGML_CUDA(cudaMemcpyAsync(Lsig[0], sigma_dense, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
             } else {
                 const double* src = Lsig[0];
                 double* dst = (v % 2 == 1) ? Lsig[v] : Lscr;
@@ -345,27 +423,98 @@ void sgml_solver::ensure_literal() {
 }
 
 // ---------------------------------------------------------------------------
+// layout-dependent helpers
+// ---------------------------------------------------------------------------
+
+void sgml_solver::load_source(const double* f) {
+    const cudaStream_t s = ctx->stream;
+    if (compact())
+        launch(SGML_CLASS_OTHER, [&] { launch_scatter_ext(g.dim, f, r, Lv[0], s); });
+    else
+        SGML_CUDA(cudaMemcpyAsync(r, f, g.total * sizeof(double), cudaMemcpyDeviceToDevice, s));
+}
+
+const double* sgml_solver::dense_view(const double* field) {
+    if (!compact()) return field;
+    launch(SGML_CLASS_OTHER, [&] { launch_gather_ext(g.dim, field, Lv[0], dense, ctx->stream); });
+    return dense;
+}
+
+// kernels.cpp:388-395 on r (serial Kahan mean on the host, then subtract;
+// the subtraction also covers r's mirror ghosts, which stay consistent)
+void sgml_solver::zero_mean_r() {
+    const double mean = trapezoid_mean_host(ctx, g, dense_view(r));
+    const uint64_t count = compact() ? ext_size(g.dim, Lv[0]) : g.total;
+    launch(SGML_CLASS_OTHER, [&] { launch_sub_scalar(r, count, mean, ctx->stream); });
+}
+
+double sgml_solver::max_abs_r(const double* f_dense) {
+    const cudaStream_t s = ctx->stream;
+    unsigned long long* d_rmax = d_cycle + n_slots;
+    const double* src = all_neumann ? dense_view(r) : (compact() ? f_dense : r);
+    SGML_CUDA(cudaMemsetAsync(d_rmax, 0, sizeof(unsigned long long), s));
+    launch(SGML_CLASS_OTHER, [&] { launch_max_abs(src, g.total, d_rmax, s); });
+    SGML_CUDA(cudaMemcpyAsync(h_cycle + n_slots, d_rmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    SGML_CUDA(cudaStreamSynchronize(s));
+    double norm;
+    std::memcpy(&norm, &h_cycle[n_slots], sizeof(double));
+    return norm;
+}
+
+// u_tot += e; r -= A(e) + a e; r = 0 on Dirichlet; max|r| into d_cycle[n_slots]
+void sgml_solver::residual(const double* e) {
+    const int dim = g.dim;
+    const cudaStream_t s = ctx->stream;
+    unsigned long long* d_rmax = d_cycle + n_slots;
+    const RelaxConst rc0 = relax_const(dim, 0, g.h, a, cfg.safety, false);
+    if (compact()) {
+        TmaSet tm;
+        tm.u = umap(e);
+        tm.g = gmap(r);
+        tm.s = has_sigma ? umap(S[0]) : tm.u;
+        tm.t = gmap(utot);
+        launch(SGML_CLASS_RESIDUAL, [&] { launch_residual_tma(dim, has_sigma, tm, r, utot, Lv[0], rc0, bc, d_rmax, s); });
+    } else {
+        const double inv_h2 = 1.0 / (g.h * g.h);
+        const double pref = dim == 2 ? 0.5 : 3.0 / 13.0;
+        launch(SGML_CLASS_RESIDUAL, [&] {
+            launch_residual(dim, has_sigma, r, e, utot, has_sigma ? Lsig[0] : nullptr, g.N, inv_h2, pref, a, bc,
+                            d_rmax, s);
+        });
+    }
+}
+
+// ---------------------------------------------------------------------------
 // one cycle
 // ---------------------------------------------------------------------------
 
-const double* sgml_solver::cycle(const double* source, bool homogeneous) {
-    return opts.engine == 0 ? cycle_compact(source, homogeneous) : cycle_literal(source, homogeneous);
+const double* sgml_solver::cycle(bool homogeneous) {
+    return compact() ? cycle_compact(homogeneous) : cycle_literal(homogeneous);
 }
 
-const double* sgml_solver::cycle_compact(const double* source, bool homogeneous) {
-    const int dim = g.dim, n = g.n, N = g.N;
+void sgml_solver::cycle_dense(const double* src_dense, double* out_dense, bool homogeneous) {
+    load_source(src_dense);
+    const double* e = cycle(homogeneous);
+    if (compact()) {
+        launch(SGML_CLASS_OTHER, [&] { launch_gather_ext(g.dim, e, Lv[0], out_dense, ctx->stream); });
+    } else {
+        SGML_CUDA(cudaMemcpyAsync(out_dense, e, g.total * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+}
+
+const double* sgml_solver::cycle_compact(bool homogeneous) {
+    const int dim = g.dim, n = g.n;
     const cudaStream_t s = ctx->stream;
-    const uint64_t T = g.total;
+    const uint64_t E0 = ext_size(dim, Lv[0]);
     unsigned long long* diag = d_cycle;
     int* flag = d_flag;
 
     // restriction pyramid of the cycle's source (once per cycle, F4)
     for (int m = 0; m + 1 < n; ++m)
         launch(SGML_CLASS_PYRAMID, [&] {
-            launch_pyramid2(dim, m == 0 ? source : P[m], Nl[m], P[m + 1], Nl[m + 1], bc, s);
+            launch_pyramid_ext(dim, m == 0 ? r : P[m], Lv[m], P[m + 1], Lv[m + 1], s);
         });
-    auto gsrc = [&](int v) { return v == 0 ? source : (const double*)P[v]; };
-    auto sig = [&](int v) { return has_sigma ? (const double*)S[v] : nullptr; };
+    auto gsrc = [&](int v) { return v == 0 ? (const double*)r : (const double*)P[v]; };
 
     int slot = 0;
     bool first = true;          // no pass has run in this cycle yet
@@ -379,9 +528,13 @@ const double* sgml_solver::cycle_compact(const double* source, bool homogeneous)
         for (int p = 1; p <= c; ++p) {
             double* out = cur == p0 ? p1 : p0;
             double* duo = (v > 0 && p < c) ? DU[v][p - 1] : nullptr;
+            TmaSet tm;
+            tm.u = umap(cur);
+            tm.g = gmap(gsrc(v));
+            tm.s = has_sigma ? umap(S[v]) : tm.u;
+            tm.t = tm.g;
             launch(v == 0 ? SGML_CLASS_RELAX0 : SGML_CLASS_RELAX_COARSE, [&] {
-                launch_relax_tiled(dim, has_sigma, out, duo, cur, gsrc(v), sig(v), Nl[v], rc, bc,
-                                   diag + slot, flag, s);
+                launch_relax_tma(dim, has_sigma, tm, out, duo, Lv[v], rc, bc, diag + slot, flag, s);
             });
             ++slot;
             cur = out;
@@ -398,15 +551,14 @@ const double* sgml_solver::cycle_compact(const double* source, bool homogeneous)
         const double* ufinal = nullptr;  // last pass output of level v+1
         for (int v = v1; v >= 1; --v) {
             double* in = U[v][0];
-            const uint64_t Sv = pow_dim(Nl[v], dim);
             if (first) {
-                SGML_CUDA(cudaMemsetAsync(in, 0, Sv * sizeof(double), s));
+                SGML_CUDA(cudaMemsetAsync(in, 0, ext_size(dim, Lv[v]) * sizeof(double), s));
             } else {
                 if (count + (c - 1) > kMaxChain) {
                     // fold the pending increments into a full-grid base
                     const ChainEntry* ch = chain_at();
                     launch(SGML_CLASS_MATERIALIZE, [&] {
-                        launch_materialize4(dim, other, N, 0, base, N, base_zero, ufinal, Nl[v + 1],
+                        launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], base_zero, ufinal, Lv[v + 1],
                                             v + 1, ch, count, bc, homogeneous, flag, s);
                     });
                     std::swap(base, other);
@@ -416,9 +568,10 @@ const double* sgml_solver::cycle_compact(const double* source, bool homogeneous)
                     ufinal = nullptr;  // already folded into base
                 }
                 const ChainEntry* ch = chain_at();
+                const ExtLay Lf = v + 1 < n ? Lv[v + 1] : Lv[v];
                 launch(SGML_CLASS_MATERIALIZE, [&] {
-                    launch_materialize4(dim, in, Nl[v], v, base, N, base_zero, ufinal,
-                                        v + 1 < n ? Nl[v + 1] : 0, 1, ch, count, bc, homogeneous, flag, s);
+                    launch_materialize4(dim, in, Lv[v], v, base, Lv[0], base_zero, ufinal, Lf, 1, ch, count, bc,
+                                        homogeneous, flag, s);
                 });
             }
             ufinal = relax_level(v, in, c, U[v][0], U[v][1]);
@@ -427,13 +580,14 @@ const double* sgml_solver::cycle_compact(const double* source, bool homogeneous)
         // level 0 visit of this tooth
         double* in0;
         if (first) {
-            SGML_CUDA(cudaMemsetAsync(base, 0, T * sizeof(double), s));
+            SGML_CUDA(cudaMemsetAsync(base, 0, E0 * sizeof(double), s));
             in0 = base;
         } else if (v1 >= 1) {
             const ChainEntry* ch = chain_at();
+            const ExtLay Lf = n > 1 ? Lv[1] : Lv[0];
             launch(SGML_CLASS_MATERIALIZE, [&] {
-                launch_materialize4(dim, other, N, 0, base, N, base_zero, ufinal, Nl.size() > 1 ? Nl[1] : 0,
-                                    1, ch, count, bc, homogeneous, flag, s);
+                launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], base_zero, ufinal, Lf, 1, ch, count, bc,
+                                    homogeneous, flag, s);
             });
             in0 = other;
         } else {
@@ -448,11 +602,11 @@ const double* sgml_solver::cycle_compact(const double* source, bool homogeneous)
     return base;
 }
 
-const double* sgml_solver::cycle_literal(const double* source, bool homogeneous) {
+const double* sgml_solver::cycle_literal(bool homogeneous) {
     const int dim = g.dim, n = g.n, N = g.N;
     const cudaStream_t s = ctx->stream;
     const uint64_t T = g.total;
-    ensure_literal();
+    const double* source = r;
     // state.u / u_prev zeroed by solve (cycle.cpp:179-180); du reset at the
     // first relax step
     SGML_CUDA(cudaMemsetAsync(Lu, 0, T * sizeof(double), s));
@@ -499,9 +653,18 @@ const double* sgml_solver::cycle_literal(const double* source, bool homogeneous)
     return Lu;
 }
 
-void sgml_solver::zero_mean(double* field) {
-    const double mean = trapezoid_mean_host(ctx, g, field);
-    launch(SGML_CLASS_OTHER, [&] { launch_sub_scalar(field, g.total, mean, ctx->stream); });
+// cycle.cpp:244-245 (pure_neumann_pin) and the dense result
+void sgml_solver::pin_and_emit(double* u_out) {
+    const cudaStream_t s = ctx->stream;
+    const uint64_t T = g.total;
+    double* res = compact() ? dense : utot;
+    if (compact()) launch(SGML_CLASS_OTHER, [&] { launch_gather_ext(g.dim, utot, Lv[0], dense, s); });
+    if (all_neumann && a == 0.0) {
+        const double mean = trapezoid_mean_host(ctx, g, res);
+        launch(SGML_CLASS_OTHER, [&] { launch_sub_scalar(res, T, mean, s); });
+    }
+    if (u_out && u_out != res)
+        SGML_CUDA(cudaMemcpyAsync(u_out, res, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
 // ---------------------------------------------------------------------------
@@ -512,18 +675,15 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
     SGML_CUDA(cudaSetDevice(ctx->device));
     const cudaStream_t s = ctx->stream;
     const uint64_t T = g.total;
-    const int dim = g.dim;
     launches = 0;
     for (int k = 0; k < 8; ++k) { cls_ms[k] = 0.0; cls_n[k] = 0; }
     spans.clear();
     evused = 0;
-
     if (!tev0) {
         SGML_CUDA(cudaEventCreate(&tev0));
         SGML_CUDA(cudaEventCreate(&tev1));
     }
-    cudaEvent_t ev0 = tev0, ev1 = tev1;
-    SGML_CUDA(cudaEventRecord(ev0, s));
+    SGML_CUDA(cudaEventRecord(tev0, s));
 
     // input validation (cycle.cpp:150-152)
     SGML_CUDA(cudaMemsetAsync(d_flag, 0, 4 * sizeof(int), s));
@@ -538,23 +698,12 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
     rep->normalization = 0.0;
     rep->node_updates = 0;
 
-    SGML_CUDA(cudaMemcpyAsync(r, f, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    SGML_CUDA(cudaMemsetAsync(utot, 0, T * sizeof(double), s));
-    if (all_neumann) zero_mean(r);
-
-    // norm = max|r|
-    unsigned long long* d_rmax = d_cycle + n_slots;
-    SGML_CUDA(cudaMemsetAsync(d_rmax, 0, sizeof(unsigned long long), s));
-    launch(SGML_CLASS_OTHER, [&] { launch_max_abs(r, T, d_rmax, s); });
-    SGML_CUDA(cudaMemcpyAsync(h_cycle + n_slots, d_rmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
-    SGML_CUDA(cudaStreamSynchronize(s));
-    double norm;
-    std::memcpy(&norm, &h_cycle[n_slots], sizeof(double));
+    load_source(f);
+    SGML_CUDA(cudaMemsetAsync(utot, 0, (compact() ? ext_size(g.dim, Lv[0]) : T) * sizeof(double), s));
+    if (all_neumann) zero_mean_r();
+    double norm = max_abs_r(f);  // D = max|f|; 0 falls back to the cycle-0 residual
     bool norm_pending = norm == 0.0;
 
-    const double inv_h2 = 1.0 / (g.h * g.h);
-    const double pref = dim == 2 ? 0.5 : 3.0 / 13.0;
-    const double* sig0 = has_sigma ? (opts.engine == 0 ? S[0] : Lsig[0]) : nullptr;
     uint64_t work = 0;
     double prev_res = std::numeric_limits<double>::infinity();
     int non_decreasing = 0;
@@ -562,7 +711,7 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
 
     for (int cyc = 0; cyc < cfg.max_cycles; ++cyc) {
         const bool homogeneous = cyc > 0;
-        if (all_neumann && cyc > 0) zero_mean(r);
+        if (all_neumann && cyc > 0) zero_mean_r();
         if (badstep) {  // kernels.cpp:197,343: the first pass throws
             rep->nan_detected = 1;
             rep->converged = 0;
@@ -570,7 +719,7 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
         }
         SGML_CUDA(cudaMemsetAsync(d_cycle, 0, (n_slots + 1) * sizeof(unsigned long long), s));
         SGML_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
-        const double* e = cycle(r, homogeneous);
+        const double* e = cycle(homogeneous);
         // kernel_error check before the recurrence touches u_tot and r
         SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaStreamSynchronize(s));
@@ -580,11 +729,7 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
             rep->converged = 0;
             break;
         }
-        // u_tot += e; r -= A(e) + a e; r = 0 on Dirichlet; max|r|
-        launch(SGML_CLASS_RESIDUAL, [&] {
-            launch_residual_tiled(dim, has_sigma, r, e, utot, sig0, g.N,
-                                  relax_const(dim, 0, g.h, a, cfg.safety, false), bc, d_rmax, s);
-        });
+        residual(e);
         SGML_CUDA(cudaGetLastError());
         SGML_CUDA(cudaMemcpyAsync(h_cycle, d_cycle, (n_slots + 1) * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s));
@@ -627,7 +772,8 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
             sgml_field view;
             view.ctx = ctx;
             view.grid = g;
-            view.d = utot;
+            view.d = const_cast<double*>(dense_view(utot));
+            SGML_CUDA(cudaStreamSynchronize(s));
             double l1 = 0.0;
             if (rep->hook(rep->hook_user, cyc, &view, &l1)) {
                 row.has_l1 = 1;
@@ -647,13 +793,11 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
         prev_res = res;
     }
     rep->normalization = norm_pending ? 0.0 : norm;
-    if (all_neumann && a == 0.0) zero_mean(utot);  // pure_neumann_pin
-    if (u_out && u_out != utot)
-        SGML_CUDA(cudaMemcpyAsync(u_out, utot, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    SGML_CUDA(cudaEventRecord(ev1, s));
-    SGML_CUDA(cudaEventSynchronize(ev1));
+    pin_and_emit(u_out);
+    SGML_CUDA(cudaEventRecord(tev1, s));
+    SGML_CUDA(cudaEventSynchronize(tev1));
     float ms = 0.f;
-    SGML_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    SGML_CUDA(cudaEventElapsedTime(&ms, tev0, tev1));
     if (opts.timing) harvest_spans();
     rep->device_ms = ms;
     rep->kernel_launches = launches;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <array>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -73,25 +74,34 @@ struct sgml_solver {
     sgml_solver_opts opts{};
     uint64_t units_per_cycle = 0;
     int n_slots = 0;
+    bool compact() const { return opts.engine == 0; }
 
     // schedule flattened: for every relax pass, its (level, pass_index)
     std::vector<int> pass_level, pass_index;
 
-    // full-grid buffers
+    // Full-grid buffers.  Compact engine: ghost-extended layout Lv[0]
+    // (utot: extended without ghosts); literal engine: dense x-fastest.
     double* r = nullptr;
     double* utot = nullptr;
     double* A = nullptr;
     double* B = nullptr;
-    double* fin = nullptr;   // staging for host-buffer solves (sgml_solve)
-    // level-compact buffers (index = level)
+    double* fin = nullptr;     // dense staging for host-buffer solves (sgml_solve)
+    double* dense = nullptr;   // dense scratch / result (compact engine)
+    // level arrays of the compact engine (index = level), extended layout
     std::vector<int> Nl;
+    std::vector<sgmlb::ExtLay> Lv;
     std::vector<double*> P;                   // P[m], m >= 1 (P[0] is r)
     std::vector<double*> S;                   // S[m] sigma pyramid, S[0] full sigma
     std::vector<std::array<double*, 2>> U;    // U[v][0..1], v >= 1
     std::vector<std::vector<double*>> DU;     // DU[v][k]
     sgmlb::ChainEntry* d_chain = nullptr;     // per-tooth pending-increment lists
     std::vector<int> tooth_off;               // offset of tooth v1's list in d_chain
-    // literal-engine buffers (lazily allocated)
+    // TMA descriptors per buffer: window box (tile + halo) and tile box
+    std::vector<std::pair<const double*, CUtensorMap>> map_u, map_g;
+    const CUtensorMap& umap(const double* p) const;
+    const CUtensorMap& gmap(const double* p) const;
+    void add_maps(const double* p, const sgmlb::ExtLay& L, bool want_u, bool want_g);
+    // literal-engine buffers
     double *Lg = nullptr, *Lscr = nullptr, *Lu = nullptr, *Lup = nullptr, *Ldu = nullptr,
            *Ldup = nullptr;
     std::vector<double*> Lsig;                // full sigma levels
@@ -102,8 +112,6 @@ struct sgml_solver {
     int* h_flag = nullptr;
     uint64_t bytes = 0;
     uint64_t launches = 0;
-    // CUDA graphs of the cycle launch sequence, keyed by homogeneous flag
-    cudaGraphExec_t graph[2] = {nullptr, nullptr};
     // per-class device timing (opts.timing): event pairs harvested per cycle
     struct Span {
         int cls;
@@ -119,14 +127,23 @@ struct sgml_solver {
     ~sgml_solver();
     void build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double a_, const double* sigma_dev,
                const sgml_solver_cfg& cfg_, const sgml_solver_opts& opts_);
-    // (re)load the coefficient: sigma pyramid / literal sigma levels + positivity
-    void load_sigma(const double* sigma_dev);
-    // device buffer that receives an uploaded coefficient (level 0)
-    double* sigma_level0() { return opts.engine == 0 ? S[0] : Lsig[0]; }
+    // (re)load the coefficient from a DENSE device field: sigma pyramid /
+    // literal sigma levels, positivity check (cycle.cpp:117-133)
+    void load_sigma(const double* sigma_dense);
+    // dense device buffer an uploaded coefficient can be staged in
+    double* sigma_stage() { return compact() ? dense : Lsig[0]; }
     // timed launch: records an event pair around fn when opts.timing
+    int debug_sync = -1;  // SGML_DEBUG_SYNC=1: synchronize + check after every launch
+    void check_launch(int cls);
     template <typename F>
     void launch(int cls, F&& fn) {
         ++launches;
+        if (debug_sync < 0) debug_sync = std::getenv("SGML_DEBUG_SYNC") ? 1 : 0;
+        if (debug_sync) {
+            fn();
+            check_launch(cls);
+            return;
+        }
         if (!opts.timing) {
             fn();
             return;
@@ -139,13 +156,23 @@ struct sgml_solver {
     }
     cudaEvent_t next_event();
     void harvest_spans();  // call after a stream synchronize
-    // cycle.cpp:140-247
+    // cycle.cpp:140-247 on a DENSE device source; the dense result goes to
+    // u_out_dev (or the internal dense buffer, see result())
     void run(const double* f_dev, double* u_out_dev, sgml_report* rep);
-    // one cycle of the schedule on `source`, result (state.u) returned
-    const double* cycle(const double* source, bool homogeneous);
-    const double* cycle_compact(const double* source, bool homogeneous);
-    const double* cycle_literal(const double* source, bool homogeneous);
+    const double* result() const { return compact() ? dense : utot; }
+    // one cycle on the engine's own source buffer r; returns state.u in the
+    // engine layout
+    const double* cycle(bool homogeneous);
+    const double* cycle_compact(bool homogeneous);
+    const double* cycle_literal(bool homogeneous);
+    // one cycle from a dense source into a dense state.u (sgml_single_cycle)
+    void cycle_dense(const double* src_dense, double* out_dense, bool homogeneous);
+    void load_source(const double* f_dense);            // r <- f
+    void zero_mean_r();                                  // zero_mean_projection(r)
+    double max_abs_r(const double* f_dense);             // max |r| (data nodes)
+    void residual(const double* e);                      // fused recurrence step
+    const double* dense_view(const double* engine_field);  // dense device view
+    void pin_and_emit(double* u_out_dev);                // pure_neumann_pin + result
     void ensure_literal();
-    void zero_mean(double* field);
     double* alloc(size_t count);
 };

@@ -67,15 +67,6 @@ __global__ void __launch_bounds__(BX* BY) k_restrict_pass(const double* __restri
     out[lin3(N, i, j, k)] = restrict_point<DIM>(in, N, lam, i, j, k, bc);
 }
 
-template <int DIM>
-__global__ void __launch_bounds__(BX* BY) k_pyramid_step(const double* __restrict__ in, int Nin,
-                                                         double* __restrict__ out, int Nout,
-                                                         BcDev bc) {
-    const int I = blockIdx.x * BX + threadIdx.x, J = blockIdx.y * BY + threadIdx.y, K = blockIdx.z;
-    if (I >= Nout || J >= Nout) return;
-    out[lin3(Nout, I, J, K)] = restrict_point<DIM>(in, Nin, 1, 2 * I, 2 * J, 2 * K, bc);
-}
-
 // kernels.cpp:140-174 on a full-grid du_prev (corners at i0, i0 + lam);
 // zero-weight corners are skipped, so the reference's out-of-row reads on
 // non-Dirichlet high faces never happen here.
@@ -145,59 +136,6 @@ __global__ void __launch_bounds__(BX* BY)
         du[pos] = duv;
     }
     block_max_commit(diag, diag_slot);
-    block_or_commit(bad, flag);
-}
-
-template <int DIM, bool SIG>
-__global__ void __launch_bounds__(BX* BY)
-    k_relax_compact(double* __restrict__ uo, double* __restrict__ duo, const double* __restrict__ ui,
-                    const double* __restrict__ g, const double* __restrict__ sig, int Nc,
-                    RelaxConst rc, BcDev bc, unsigned long long* diag_slot, int* flag) {
-    const int i = blockIdx.x * BX + threadIdx.x, j = blockIdx.y * BY + threadIdx.y, k = blockIdx.z;
-    double diag = 0.0;
-    int bad = 0;
-    if (i < Nc && j < Nc) {
-        const size_t pos = lin3(Nc, i, j, k);
-        const bool on_face = i == 0 || i == Nc - 1 || j == 0 || j == Nc - 1 ||
-                             (DIM == 3 && (k == 0 || k == Nc - 1));
-        double value;
-        if (on_face && on_dirichlet<DIM>(bc, Nc, i, j, k)) {
-            value = rc.homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nc, i, j, k);
-        } else {
-            value = relax_at<DIM, SIG>(ui, sig, g, Nc, 1, i, j, k, pos, rc, bc, diag);
-        }
-        bad = !isfinite(value);
-        uo[pos] = value;
-        if (duo) duo[pos] = value - ui[pos];
-    }
-    block_max_commit(diag, diag_slot);
-    block_or_commit(bad, flag);
-}
-
-template <int DIM>
-__global__ void __launch_bounds__(BX* BY)
-    k_materialize(double* __restrict__ out, int Nw, int w, const double* __restrict__ base, int N,
-                  int base_zero, const double* __restrict__ ufine, int Nf, int frel, Chain chain,
-                  BcDev bc, int homogeneous, int* flag) {
-    const int I = blockIdx.x * BX + threadIdx.x, J = blockIdx.y * BY + threadIdx.y, K = blockIdx.z;
-    int bad = 0;
-    if (I < Nw && J < Nw) {
-        const bool on_face = I == 0 || I == Nw - 1 || J == 0 || J == Nw - 1 ||
-                             (DIM == 3 && (K == 0 || K == Nw - 1));
-        double value;
-        if (on_face && on_dirichlet<DIM>(bc, Nw, I, J, K)) {
-            value = homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, I, J, K);
-        } else if (ufine && ((I | J | K) & ((1 << frel) - 1)) == 0) {
-            value = ufine[lin3(Nf, I >> frel, J >> frel, K >> frel)];
-        } else {
-            const int x = I << w, y = J << w, z = K << w;
-            value = base_zero ? 0.0 : base[lin3(N, x, y, z)];
-            for (int c = 0; c < chain.count; ++c)
-                value = value + interp_compact<DIM>(chain.du[c], chain.Nl[c], chain.level[c], x, y, z);
-        }
-        bad = !isfinite(value);
-        out[lin3(Nw, I, J, K)] = value;
-    }
     block_or_commit(bad, flag);
 }
 
@@ -314,12 +252,6 @@ void launch_restrict_pass(int dim, const double* in, double* out, int N, int lam
     else k_restrict_pass<3><<<grid_for(3, N), dim3(BX, BY), 0, s>>>(in, out, N, lam, bc);
 }
 
-void launch_pyramid_step(int dim, const double* in, int Nin, double* out, int Nout,
-                         const BcDev& bc, cudaStream_t s) {
-    if (dim == 2) k_pyramid_step<2><<<grid_for(2, Nout), dim3(BX, BY), 0, s>>>(in, Nin, out, Nout, bc);
-    else k_pyramid_step<3><<<grid_for(3, Nout), dim3(BX, BY), 0, s>>>(in, Nin, out, Nout, bc);
-}
-
 void launch_relax_literal(int dim, bool sig, double* u, double* du, const double* up,
                           const double* dup, const double* g, const double* sigma, int N, int level,
                           const RelaxConst& rc, const BcDev& bc, unsigned long long* slot, int* flag,
@@ -332,29 +264,6 @@ void launch_relax_literal(int dim, bool sig, double* u, double* du, const double
         if (sig) k_relax_literal<3, true><<<gr, bl, 0, s>>>(u, du, up, dup, g, sigma, N, level, rc, bc, slot, flag);
         else k_relax_literal<3, false><<<gr, bl, 0, s>>>(u, du, up, dup, g, sigma, N, level, rc, bc, slot, flag);
     }
-}
-
-void launch_relax_compact(int dim, bool sig, double* uo, double* duo, const double* ui,
-                          const double* g, const double* sigma, int Nc, const RelaxConst& rc,
-                          const BcDev& bc, unsigned long long* slot, int* flag, cudaStream_t s) {
-    const dim3 gr = grid_for(dim, Nc), bl(BX, BY);
-    if (dim == 2) {
-        if (sig) k_relax_compact<2, true><<<gr, bl, 0, s>>>(uo, duo, ui, g, sigma, Nc, rc, bc, slot, flag);
-        else k_relax_compact<2, false><<<gr, bl, 0, s>>>(uo, duo, ui, g, sigma, Nc, rc, bc, slot, flag);
-    } else {
-        if (sig) k_relax_compact<3, true><<<gr, bl, 0, s>>>(uo, duo, ui, g, sigma, Nc, rc, bc, slot, flag);
-        else k_relax_compact<3, false><<<gr, bl, 0, s>>>(uo, duo, ui, g, sigma, Nc, rc, bc, slot, flag);
-    }
-}
-
-void launch_materialize(int dim, double* out, int Nw, int w, const double* base, int N,
-                        bool base_zero, const double* ufine, int Nf, int frel, const Chain& chain,
-                        const BcDev& bc, bool homogeneous, int* flag, cudaStream_t s) {
-    const dim3 gr = grid_for(dim, Nw), bl(BX, BY);
-    if (dim == 2)
-        k_materialize<2><<<gr, bl, 0, s>>>(out, Nw, w, base, N, base_zero, ufine, Nf, frel, chain, bc, homogeneous, flag);
-    else
-        k_materialize<3><<<gr, bl, 0, s>>>(out, Nw, w, base, N, base_zero, ufine, Nf, frel, chain, bc, homogeneous, flag);
 }
 
 void launch_residual(int dim, bool sig, double* r, const double* e, double* utot,

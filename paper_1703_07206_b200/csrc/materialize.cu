@@ -1,10 +1,13 @@
-// materialize.cu — lazy application of the pending interpolation increments.
+// materialize.cu — level-array kernels of the compact engine other than the
+// relaxation pass: lazy interpolation (materialize), the restriction
+// pyramid, and dense <-> ghost-extended conversions.  All level arrays use
+// the ghost-extended padded layout of device.cuh (ExtLay).
 //
-// In the reference every pass at level v >= 1 sweeps the whole grid and
-// adds u_prev + I(du_prev) at each non-subset node (kernels.cpp:140-174,
-// 225-226).  The compact engine (engine.cpp) keeps those variations on the
-// level-v subset (DU arrays) and applies them only when the next level's
-// input is needed, in the reference's order:
+// Lazy interpolation.  In the reference every pass at level v >= 1 sweeps
+// the whole grid and adds u_prev + I(du_prev) at each non-subset node
+// (kernels.cpp:140-174, 225-226).  The compact engine keeps those
+// variations on the level-v subset (DU arrays) and applies them only when
+// the next level's input is needed, in the reference's order:
 //
 //   value = Dirichlet face value                 (on a Dirichlet face)
 //         = U_lf[x]                              (x on the finest relaxed level lf)
@@ -12,7 +15,6 @@
 //
 // with I_l(du)(x) = sum over corners r, q, p of ((wz*wy)*wx) * du[corner]
 // (all weights exact dyadics; zero-weight corners skipped: sign of zero only).
-//
 // A thread owns MV = 4 consecutive x nodes.  For every level coarser than
 // the first the four nodes share one cell, so the 8 corner loads serve four
 // nodes; y and z are uniform across a warp, so the zero-weight corner rows
@@ -31,8 +33,8 @@ constexpr int MBX = 32, MBY = 4;
 
 template <int DIM>
 __global__ void __launch_bounds__(MBX* MBY)
-    k_materialize4(double* __restrict__ out, int Nw, int w, const double* __restrict__ base, int N,
-                   int base_zero, const double* __restrict__ ufine, int Nf, int frel,
+    k_materialize4(double* __restrict__ out, ExtLay Lw, int w, const double* __restrict__ base,
+                   ExtLay L0, int base_zero, const double* __restrict__ ufine, ExtLay Lf, int frel,
                    const ChainEntry* __restrict__ chain, int nchain, BcDev bc, int homogeneous,
                    int* flag) {
     __shared__ ChainEntry sch[kMaxChain];
@@ -40,6 +42,7 @@ __global__ void __launch_bounds__(MBX* MBY)
     for (int c = tid; c < nchain; c += MBX * MBY) sch[c] = chain[c];
     __syncthreads();
 
+    const int Nw = Lw.N;
     const int X4 = (blockIdx.x * MBX + threadIdx.x) * MV;
     const int J = blockIdx.y * MBY + threadIdx.y;
     const int K = blockIdx.z;
@@ -50,11 +53,11 @@ __global__ void __launch_bounds__(MBX* MBY)
         double val[MV];
 #pragma unroll
         for (int k = 0; k < MV; ++k)
-            val[k] = (!base_zero && k < nv) ? __ldg(base + lin3(N, (X4 + k) << w, y, z)) : 0.0;
+            val[k] = (!base_zero && k < nv) ? __ldg(base + eix<DIM>(L0, (X4 + k) << w, y, z)) : 0.0;
 
         for (int c = 0; c < nchain; ++c) {
             const ChainEntry ce = sch[c];
-            const int l = ce.level, Nl = ce.Nl;
+            const int l = ce.level, Nl = ce.L.N;
             const int msk = (1 << l) - 1;
             const double inv = 1.0 / (double)(1 << l);  // exact power of two
             const int iy = y & msk, iz = z & msk;
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(MBX* MBY)
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
                     if (r < nr && q < nq) {
-                        const double* row = ce.du + lin3(Nl, X0, (y >> l) + q, DIM == 3 ? (z >> l) + r : 0);
+                        const double* row = ce.du + eix<DIM>(ce.L, X0, (y >> l) + q, DIM == 3 ? (z >> l) + r : 0);
 #pragma unroll
                         for (int p = 0; p < 3; ++p) cc[r][q][p] = X0 + p < Nl ? __ldg(row + p) : 0.0;
                     } else {
@@ -113,51 +116,34 @@ __global__ void __launch_bounds__(MBX* MBY)
             if ((jface || I == 0 || I == Nw - 1) && on_dirichlet<DIM>(bc, Nw, I, J, K)) {
                 value = homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, I, J, K);
             } else if (ufine && ((I | J | K) & fmask) == 0) {
-                value = __ldg(ufine + lin3(Nf, I >> frel, J >> frel, K >> frel));
+                value = __ldg(ufine + eix<DIM>(Lf, I >> frel, J >> frel, K >> frel));
             }
             bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
-            out[lin3(Nw, I, J, K)] = value;
+            store_ext<DIM>(out, Lw, I, J, K, value);
         }
     }
     block_or_commit(bad, flag);
 }
 
-}  // namespace
-
-void launch_materialize4(int dim, double* out, int Nw, int w, const double* base, int N,
-                         bool base_zero, const double* ufine, int Nf, int frel,
-                         const ChainEntry* chain, int nchain, const BcDev& bc, bool homogeneous,
-                         int* flag, cudaStream_t s) {
-    const int threads_x = (Nw + MV - 1) / MV;
-    const dim3 grid((threads_x + MBX - 1) / MBX, (Nw + MBY - 1) / MBY, dim == 3 ? Nw : 1);
-    if (dim == 2)
-        k_materialize4<2><<<grid, dim3(MBX, MBY), 0, s>>>(out, Nw, w, base, N, base_zero, ufine, Nf, frel,
-                                                          chain, nchain, bc, homogeneous, flag);
-    else
-        k_materialize4<3><<<grid, dim3(MBX, MBY), 0, s>>>(out, Nw, w, base, N, base_zero, ufine, Nf, frel,
-                                                          chain, nchain, bc, homogeneous, flag);
-}
-
-}  // namespace sgmlb
-
 // ---------------------------------------------------------------------------
-// Restriction pyramid step: level-(m+1) compact <- the
-// reference's averaging pass at stride 2^m (kernels.cpp:39-80,
-// stencil.cpp:98-119) evaluated only at level-(m+1) nodes, which in the
-// level-m compact index space are the even nodes with neighbours at +-1.
-// Interior outputs take the branch-free path; the one-node boundary layer
-// goes out of line through the reference's ghost recursion.
+// Restriction pyramid step: level-(m+1) <- the reference's
+// averaging pass at stride 2^m (kernels.cpp:39-80, stencil.cpp:98-119)
+// evaluated only at level-(m+1) nodes, which in the level-m index space are
+// the even nodes with neighbours at +-1.  The input's ghost cells hold the
+// even mirror, which is the reference's ghost value wherever the result is
+// consumed (see device.cuh); outputs are written with their mirror ghosts.
 // ---------------------------------------------------------------------------
-
-namespace sgmlb {
-
-namespace {
 
 __device__ __forceinline__ double axw2(int o) { return o == 0 ? 0.5 : 0.25; }
 
 template <int DIM>
-__device__ __noinline__ double pyramid_cold(const double* __restrict__ in, int Nin, int i, int j, int k,
-                                            BcDev bc) {
+__global__ void __launch_bounds__(128) k_pyramid_ext(const double* __restrict__ in, ExtLay Lin,
+                                                     double* __restrict__ out, ExtLay Lout) {
+    const int Nout = Lout.N;
+    const int I = blockIdx.x * 32 + threadIdx.x, J = blockIdx.y * 4 + threadIdx.y, K = blockIdx.z;
+    if (I >= Nout || J >= Nout) return;
+    const double* c = in + eix<DIM>(Lin, 2 * I, 2 * J, DIM == 3 ? 2 * K : 0);
+    const ptrdiff_t sy = Lin.Px, sz = (ptrdiff_t)Lin.Px * Lin.Ne;
     double acc = 0.0;
 #pragma unroll
     for (int r = (DIM == 3 ? -1 : 0); r <= (DIM == 3 ? 1 : 0); ++r)
@@ -166,45 +152,77 @@ __device__ __noinline__ double pyramid_cold(const double* __restrict__ in, int N
 #pragma unroll
             for (int p = -1; p <= 1; ++p) {
                 const double w = DIM == 3 ? (axw2(p) * axw2(q)) * axw2(r) : axw2(p) * axw2(q);
-                acc = acc + w * ghost(in, Nin, bc, i + p, j + q, k + r);
+                acc = acc + w * __ldg(c + r * sz + q * sy + p);
             }
-    return acc;
+    store_ext<DIM>(out, Lout, I, J, K, acc);
 }
 
+// dense x-fastest field -> ghost-extended array (data + mirror ghosts)
 template <int DIM>
-__global__ void __launch_bounds__(128) k_pyramid2(const double* __restrict__ in, int Nin,
-                                                  double* __restrict__ out, int Nout, BcDev bc) {
-    const int I = blockIdx.x * 32 + threadIdx.x, J = blockIdx.y * 4 + threadIdx.y, K = blockIdx.z;
-    if (I >= Nout || J >= Nout) return;
-    const int i = 2 * I, j = 2 * J, k = DIM == 3 ? 2 * K : 0;
-    const bool inner = I >= 1 && I <= Nout - 2 && J >= 1 && J <= Nout - 2 &&
-                       (DIM == 2 || (K >= 1 && K <= Nout - 2));
-    double acc = 0.0;
-    if (inner) {
-        const double* c = in + lin3(Nin, i, j, k);
-        const ptrdiff_t sy = Nin, sz = (ptrdiff_t)Nin * Nin;
-#pragma unroll
-        for (int r = (DIM == 3 ? -1 : 0); r <= (DIM == 3 ? 1 : 0); ++r)
-#pragma unroll
-            for (int q = -1; q <= 1; ++q)
-#pragma unroll
-                for (int p = -1; p <= 1; ++p) {
-                    const double w = DIM == 3 ? (axw2(p) * axw2(q)) * axw2(r) : axw2(p) * axw2(q);
-                    acc = acc + w * __ldg(c + r * sz + q * sy + p);
-                }
-    } else {
-        acc = pyramid_cold<DIM>(in, Nin, i, j, k, bc);
-    }
-    out[lin3(Nout, I, J, K)] = acc;
+__global__ void __launch_bounds__(128) k_scatter_ext(const double* __restrict__ dense, double* ext,
+                                                     ExtLay L) {
+    const int N = L.N;
+    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 4 + threadIdx.y, k = blockIdx.z;
+    if (i >= N || j >= N) return;
+    store_ext<DIM>(ext, L, i, j, k, dense[lin3(N, i, j, k)]);
 }
+
+// ghost-extended array -> dense x-fastest field
+template <int DIM>
+__global__ void __launch_bounds__(128) k_gather_ext(const double* __restrict__ ext, ExtLay L,
+                                                    double* __restrict__ dense) {
+    const int N = L.N;
+    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 4 + threadIdx.y, k = blockIdx.z;
+    if (i >= N || j >= N) return;
+    dense[lin3(N, i, j, k)] = ext[eix<DIM>(L, i, j, k)];
+}
+
+inline dim3 ext_grid(int dim, int N) { return dim3((N + 31) / 32, (N + 3) / 4, dim == 3 ? N : 1); }
 
 }  // namespace
 
-void launch_pyramid2(int dim, const double* in, int Nin, double* out, int Nout, const BcDev& bc,
-                     cudaStream_t s) {
-    const dim3 grid((Nout + 31) / 32, (Nout + 3) / 4, dim == 3 ? Nout : 1);
-    if (dim == 2) k_pyramid2<2><<<grid, dim3(32, 4), 0, s>>>(in, Nin, out, Nout, bc);
-    else k_pyramid2<3><<<grid, dim3(32, 4), 0, s>>>(in, Nin, out, Nout, bc);
+ExtLay make_ext(int dim, int N) {
+    ExtLay L{};
+    L.N = N;
+    L.Ne = N + 2;
+    L.Px = (L.Ne + 1) / 2 * 2;  // even pitch: 16-byte aligned rows for TMA
+    L.plane = dim == 3 ? (long long)L.Px * L.Ne : (long long)L.Px;
+    return L;
+}
+
+uint64_t ext_size(int dim, const ExtLay& L) {
+    return dim == 3 ? (uint64_t)L.Px * L.Ne * L.Ne : (uint64_t)L.Px * L.Ne;
+}
+
+void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
+                         const ExtLay& L0, bool base_zero, const double* ufine, const ExtLay& Lf,
+                         int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
+                         bool homogeneous, int* flag, cudaStream_t s) {
+    const int Nw = Lw.N;
+    const int threads_x = (Nw + MV - 1) / MV;
+    const dim3 grid((threads_x + MBX - 1) / MBX, (Nw + MBY - 1) / MBY, dim == 3 ? Nw : 1);
+    if (dim == 2)
+        k_materialize4<2><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, base_zero, ufine, Lf, frel,
+                                                          chain, nchain, bc, homogeneous, flag);
+    else
+        k_materialize4<3><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, base_zero, ufine, Lf, frel,
+                                                          chain, nchain, bc, homogeneous, flag);
+}
+
+void launch_pyramid_ext(int dim, const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout,
+                        cudaStream_t s) {
+    if (dim == 2) k_pyramid_ext<2><<<ext_grid(2, Lout.N), dim3(32, 4), 0, s>>>(in, Lin, out, Lout);
+    else k_pyramid_ext<3><<<ext_grid(3, Lout.N), dim3(32, 4), 0, s>>>(in, Lin, out, Lout);
+}
+
+void launch_scatter_ext(int dim, const double* dense, double* ext, const ExtLay& L, cudaStream_t s) {
+    if (dim == 2) k_scatter_ext<2><<<ext_grid(2, L.N), dim3(32, 4), 0, s>>>(dense, ext, L);
+    else k_scatter_ext<3><<<ext_grid(3, L.N), dim3(32, 4), 0, s>>>(dense, ext, L);
+}
+
+void launch_gather_ext(int dim, const double* ext, const ExtLay& L, double* dense, cudaStream_t s) {
+    if (dim == 2) k_gather_ext<2><<<ext_grid(2, L.N), dim3(32, 4), 0, s>>>(ext, L, dense);
+    else k_gather_ext<3><<<ext_grid(3, L.N), dim3(32, 4), 0, s>>>(ext, L, dense);
 }
 
 }  // namespace sgmlb
