@@ -5,19 +5,21 @@
 // residual recurrence at level 0 (kernels.cpp:243-297 + cycle.cpp:194-198).
 //
 // Storage: ghost-extended padded arrays (device.cuh, ExtLay), so the tile
-// halo never needs boundary code.  A CTA owns an X x Y column bundle (3D:
-// 32 x 8 nodes, 2D: 128 x 1) and marches along the slowest axis over `zb`
-// planes, two planes per step.  Thread 0 streams planes of u (tile + halo),
-// g (tile + x halo) and sigma into an NST-deep shared-memory ring with TMA
-// (cp.async.bulk.tensor), one full/empty mbarrier pair per slot: consumers
-// wait on `full`, each warp releases a slot on `empty` once it has read it,
-// and the producer refills a slot only after all warps released it (no
-// __syncthreads in the march; warps drift freely within the ring).
-// Every thread keeps a 3 x 3 x 3 register window (planes m-1 .. m+1) and
-// computes nodes m and m+1: the plane m-1 registers are refilled with m+2
-// as soon as node m's r = -1 terms and node m+1's r = -1 terms are summed,
-// giving two independent accumulation chains per thread in the reference's
-// strict 26-term order.
+// halo never needs boundary code.  A CTA owns an X x ROWS column bundle (3D:
+// 32 x 16 nodes, 2D: 128 x 1) and marches along the slowest axis over `zb`
+// planes, one plane per step.  Thread 0 streams planes of u (tile + halo),
+// g (tile rows + x halo: TMA boxes must start 16-byte aligned) and sigma
+// into an NST-deep shared-memory ring with TMA (cp.async.bulk.tensor), one
+// full/empty mbarrier pair per slot: consumers wait on `full`, each warp
+// releases a slot on `empty` once it has read it, and the producer refills a
+// slot only after all warps released it (no __syncthreads in the march).
+//
+// In 3D every thread computes RT = 2 adjacent rows (y, y+1) of the plane: it
+// keeps a (RT+2) x 3 register window of each of planes m-1, m, m+1 (12
+// values per plane, so 6 shared loads per node) and the two nodes'
+// accumulation chains interleave term by term in the reference's strict
+// 26-term order.  The window roles rotate with period 3, so the march is
+// unrolled three steps and no register moves are issued.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -33,19 +35,18 @@ enum { MODE_RELAX = 0, MODE_RESID = 1 };
 
 template <int DIM>
 struct Tile {
-    static constexpr int X = DIM == 3 ? 32 : 128;
-    static constexpr int Y = DIM == 3 ? 8 : 1;
+    static constexpr int X = DIM == 3 ? 32 : 128;      // nodes per row (= threads in x)
+    static constexpr int TY = DIM == 3 ? 8 : 1;        // thread rows
+    static constexpr int RT = DIM == 3 ? 2 : 1;        // node rows per thread
+    static constexpr int ROWS = TY * RT;               // node rows per CTA
     static constexpr int HX = X + 2;
-    static constexpr int HY = DIM == 3 ? Y + 2 : 1;
-    static constexpr int PLANE = HX * HY;
-    static constexpr int INNER = X * Y;
-    // g / u_tot box: the tile rows plus the x halo, so that the box starts on
-    // an even (16-byte aligned) cell as TMA requires in the innermost dim
-    static constexpr int GBOX = HX * Y;
-    static constexpr int THREADS = X * Y;
+    static constexpr int HY = DIM == 3 ? ROWS + 2 : 1;
+    static constexpr int PLANE = HX * HY;              // u / sigma box (tile + halo)
+    static constexpr int GBOX = HX * ROWS;             // g / u_tot box (tile rows + x halo)
+    static constexpr int THREADS = X * TY;
     static constexpr int NWARPS = THREADS / 32;
-    static constexpr int Q = DIM == 3 ? 3 : 1;               // in-plane y extent of the stencil
-    static constexpr int NST = 8;                            // ring depth (planes), power of two
+    static constexpr int WR = DIM == 3 ? RT + 2 : 1;   // window rows per plane
+    static constexpr int NST = 8;                      // ring depth (planes), power of two
     static constexpr int PLANE_AL = (PLANE + 15) / 16 * 16;  // slots 128-byte aligned
     static constexpr int GBOX_AL = (GBOX + 15) / 16 * 16;
 };
@@ -60,8 +61,10 @@ struct __align__(128) TRing {
     unsigned long long empty[Tile<DIM>::NST];
 };
 
+template <int DIM>
+using Win = double[Tile<DIM>::WR][3];
 template <int DIM, bool SIG>
-using SWin = double[SIG ? Tile<DIM>::Q : 1][SIG ? 3 : 1];
+using SWin = double[SIG ? Tile<DIM>::WR : 1][SIG ? 3 : 1];
 
 // MODE_RELAX:  uo <- relaxed u (with mirror ghosts), duo <- u - u_prev (optional),
 //              tm_g = source g, diag_slot <- max |A(u)+a u - g| over relax nodes.
@@ -75,7 +78,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                 double* uo, double* duo, ExtLay L, int zb, RelaxConst rc, BcDev bc,
                 unsigned long long* diag_slot, int* flag) {
     using TL = Tile<DIM>;
-    constexpr int Q = TL::Q, NST = TL::NST;
+    constexpr int NST = TL::NST, RT = TL::RT, WR = TL::WR;
     constexpr bool RESID = MODE == MODE_RESID;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TRing<DIM, SIG, MODE>& R = *reinterpret_cast<TRing<DIM, SIG, MODE>*>(smem_raw);
@@ -84,19 +87,23 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     const int tid = tx + TL::X * ty;
     const int lane = tid & 31;
     const int N = L.N;
-    const int x0 = blockIdx.x * TL::X, y0 = DIM == 3 ? blockIdx.y * TL::Y : 0;
+    const int x0 = blockIdx.x * TL::X, y0 = DIM == 3 ? blockIdx.y * TL::ROWS : 0;
     const int m0 = blockIdx.z * zb;
     const int mend = min(m0 + zb, N);  // exclusive
-    const int xi = x0 + tx, yi = y0 + ty;
-    const bool col_ok = xi < N && (DIM == 2 || yi < N);
+    const int xi = x0 + tx;
+    const int yb = y0 + ty * RT;       // first node row of this thread (3D)
     const bool with_t = RESID && duo != nullptr;
+    bool ok[RT];
+#pragma unroll
+    for (int a = 0; a < RT; ++a) ok[a] = xi < N && (DIM == 2 || yb + a < N);
 
-    // Dirichlet status of this column (lowest face id wins, grid.cpp:53-62):
-    // x/y faces outrank the z faces, so only z is decided per plane.
-    const bool dir_ij = DIM == 3 ? ((xi == 0 && !bc.neu[0]) || (xi == N - 1 && !bc.neu[1]) ||
-                                    (yi == 0 && !bc.neu[2]) || (yi == N - 1 && !bc.neu[3]))
-                                 : ((xi == 0 && !bc.neu[0]) || (xi == N - 1 && !bc.neu[1]));
     constexpr int fm = DIM == 3 ? 4 : 2;  // marching-axis faces (z in 3D, y in 2D)
+    // can any node of this CTA lie on a Dirichlet face?  (block-uniform)
+    const bool edge_tile = x0 == 0 || x0 + TL::X >= N - 1 ||
+                           (DIM == 3 && (y0 == 0 || y0 + TL::ROWS >= N - 1));
+    const bool maybe_dir =
+        (edge_tile && (!bc.neu[0] || !bc.neu[1] || (DIM == 3 && (!bc.neu[2] || !bc.neu[3])))) ||
+        (m0 == 0 && !bc.neu[fm]) || (mend == N && !bc.neu[fm + 1]);
 
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
@@ -142,43 +149,50 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
         if (lane == 0) mbar_arrive(&R.empty[slot_of(m)]);
     };
 
-    const int rbase = tx + TL::HX * ty;  // window origin in the plane
-    auto read_plane = [&](int m, double (&P)[Q][3], SWin<DIM, SIG>& Ps) {
+    const int wbase = tx + TL::HX * (DIM == 3 ? ty * RT : 0);  // window origin in the u box
+    auto read_plane = [&](int m, Win<DIM>& P, SWin<DIM, SIG>& Ps) {
         const int slot = slot_of(m);
 #pragma unroll
-        for (int q = 0; q < Q; ++q)
+        for (int w = 0; w < WR; ++w)
 #pragma unroll
             for (int p = 0; p < 3; ++p) {
-                P[q][p] = R.u[slot][rbase + p + TL::HX * q];
-                if constexpr (SIG) Ps[q][p] = R.s[slot][rbase + p + TL::HX * q];
+                P[w][p] = R.u[slot][wbase + p + TL::HX * w];
+                if constexpr (SIG) Ps[w][p] = R.s[slot][wbase + p + TL::HX * w];
             }
     };
 
     double dmax = 0.0;
     int bad = 0;
 
-    // acc += the terms of one plane (stencil offset r) for one node
-    auto plane_terms = [&](double& acc, double& smax, const double (&P)[Q][3],
-                           const SWin<DIM, SIG>& Ps, double uc, double sc, int dr) {
+    // the RT nodes' terms of one stencil plane (offset dr), interleaved term
+    // by term so the independent accumulation chains overlap
+    auto plane_terms = [&](double (&acc)[RT], double (&smax)[RT], const Win<DIM>& P,
+                           const SWin<DIM, SIG>& Ps, const double (&uc)[RT], const double (&sc)[RT],
+                           int dr) {
 #pragma unroll
-        for (int q = 0; q < Q; ++q)
+        for (int q = (DIM == 3 ? -1 : 0); q <= (DIM == 3 ? 1 : 0); ++q)
 #pragma unroll
-            for (int p = 0; p < 3; ++p) {
-                const int dq = DIM == 3 ? q - 1 : 0, dp = p - 1;
-                if (dr == 0 && dq == 0 && dp == 0) continue;
-                double sbar = 1.0;
-                if constexpr (SIG) {
-                    sbar = 0.5 * (Ps[q][p] + sc);
-                    smax = smax < sbar ? sbar : smax;
+            for (int p = -1; p <= 1; ++p) {
+                if (dr == 0 && q == 0 && p == 0) continue;
+                const int l2 = dr * dr + q * q + p * p;
+#pragma unroll
+                for (int a = 0; a < RT; ++a) {
+                    const int w = DIM == 3 ? a + q + 1 : 0;
+                    double sbar = 1.0;
+                    if constexpr (SIG) {
+                        sbar = 0.5 * (Ps[w][p + 1] + sc[a]);
+                        smax[a] = smax[a] < sbar ? sbar : smax[a];
+                    }
+                    acc[a] = stencil_term<SIG>(acc[a], sbar, P[w][p + 1], uc[a], l2);
                 }
-                acc = stencil_term<SIG>(acc, sbar, P[q][p], uc, dr * dr + dq * dq + dp * dp);
             }
     };
 
     // finish one node: op, diag / residual, Euler step, Dirichlet override, store
-    auto finish = [&](int m, double acc, double smax, double uc, double gc, double tc) {
-        const int i = xi, j = DIM == 3 ? yi : m, k = DIM == 3 ? m : 0;
-        const bool dir = dir_ij || (m == 0 && !bc.neu[fm]) || (m == N - 1 && !bc.neu[fm + 1]);
+    auto finish = [&](int m, int a, double acc, double smax, double uc, double gc, double tc) {
+        const int i = xi, j = DIM == 3 ? yb + a : m, k = DIM == 3 ? m : 0;
+        bool dir = false;
+        if (maybe_dir) dir = on_dirichlet<DIM>(bc, N, i, j, k);
         const double op = (acc * rc.pref) * rc.inv_s2;
         if constexpr (RESID) {
             double rn = gc - (HAS_A ? op + rc.a * uc : op);
@@ -214,7 +228,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
         if (duo) duo[eix<DIM>(L, i, j, k)] = value - uc;
     };
 
-    double X[Q][3], Y[Q][3], Z[Q][3];  // window planes, rotating roles
+    Win<DIM> X, Y, Z;  // window planes, rotating roles
     SWin<DIM, SIG> Xs, Ys, Zs;
 
     if (m0 < N) {
@@ -227,58 +241,42 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
         read_plane(m0, Y, Ys);
         release(m0 - 1);
 
-#pragma unroll 1
-        for (int m = m0; m < mend; m += 2) {
-            const bool two = m + 1 < mend;
-            wait_plane(m + 1);
-            read_plane(m + 1, Z, Zs);
-            double g0 = 0.0, g1 = 0.0, t0 = 0.0, t1 = 0.0;
-            if (col_ok) {
-                const int gi = tx + 1 + TL::HX * ty;  // this node in the g / u_tot box
-                g0 = R.g[slot_of(m)][gi];
-                if (two) g1 = R.g[slot_of(m + 1)][gi];
-                if (with_t) {
-                    t0 = R.t[slot_of(m)][gi];
-                    if (two) t1 = R.t[slot_of(m + 1)][gi];
-                }
-            }
-            const double uc0 = Y[Q / 2][1], uc1 = Z[Q / 2][1];
-            double sc0 = 1.0, sc1 = 1.0;
-            if constexpr (SIG) {
-                sc0 = Ys[Q / 2][1];
-                sc1 = Zs[Q / 2][1];
-            }
-            double acc0 = 0.0, acc1 = 0.0, smax0 = 0.0, smax1 = 0.0;
-            plane_terms(acc0, smax0, X, Xs, uc0, sc0, -1);
-            plane_terms(acc1, smax1, Y, Ys, uc1, sc1, -1);
-            if (two) {  // plane m-1 is dead: refill with m+2
-                wait_plane(m + 2);
-                read_plane(m + 2, X, Xs);
-            }
-            plane_terms(acc0, smax0, Y, Ys, uc0, sc0, 0);
-            plane_terms(acc1, smax1, Z, Zs, uc1, sc1, 0);
-            plane_terms(acc0, smax0, Z, Zs, uc0, sc0, 1);
-            plane_terms(acc1, smax1, X, Xs, uc1, sc1, 1);
-            if (col_ok) {
-                finish(m, acc0, smax0, uc0, g0, t0);
-                if (two) finish(m + 1, acc1, smax1, uc1, g1, t1);
-            }
-            release(m);
-            release(m + 1);
+        // one plane: P0 = m-1, P1 = m (held), P2 <- m+1
+        auto step = [&](int m, Win<DIM>& P0, Win<DIM>& P1, Win<DIM>& P2, SWin<DIM, SIG>& S0,
+                        SWin<DIM, SIG>& S1, SWin<DIM, SIG>& S2) {
             if (tid == 0)
-                for (; next <= mend && next <= m + NST - 1; ++next) issue(next);
-            // window roles rotate (X, Y, Z) -> (Z, X, -): next P0 = m+1, P1 = m+2
+                for (; next <= mend && next <= m + NST - 2; ++next) issue(next);
+            wait_plane(m + 1);
+            read_plane(m + 1, P2, S2);
+            const int sm = slot_of(m);
+            double uc[RT], sc[RT], acc[RT], smax[RT], gc[RT], tc[RT];
 #pragma unroll
-            for (int q = 0; q < Q; ++q)
+            for (int a = 0; a < RT; ++a) {
+                const int gi = tx + 1 + TL::HX * (DIM == 3 ? ty * RT + a : 0);  // node in the g box
+                gc[a] = R.g[sm][gi];
+                tc[a] = with_t ? R.t[sm][gi] : 0.0;
+                uc[a] = P1[DIM == 3 ? a + 1 : 0][1];
+                sc[a] = 1.0;
+                if constexpr (SIG) sc[a] = S1[DIM == 3 ? a + 1 : 0][1];
+                acc[a] = 0.0;
+                smax[a] = 0.0;
+            }
+            plane_terms(acc, smax, P0, S0, uc, sc, -1);
+            plane_terms(acc, smax, P1, S1, uc, sc, 0);
+            plane_terms(acc, smax, P2, S2, uc, sc, 1);
 #pragma unroll
-                for (int p = 0; p < 3; ++p) {
-                    Y[q][p] = X[q][p];
-                    X[q][p] = Z[q][p];
-                    if constexpr (SIG) {
-                        Ys[q][p] = Xs[q][p];
-                        Xs[q][p] = Zs[q][p];
-                    }
-                }
+            for (int a = 0; a < RT; ++a)
+                if (ok[a]) finish(m, a, acc[a], smax[a], uc[a], gc[a], tc[a]);
+            release(m);
+        };
+        // roles rotate (P0, P1, P2) -> (P1, P2, P0) each plane: period 3
+#pragma unroll 1
+        for (int m = m0; m < mend; m += 3) {
+            step(m, X, Y, Z, Xs, Ys, Zs);
+            if (m + 1 >= mend) break;
+            step(m + 1, Y, Z, X, Ys, Zs, Xs);
+            if (m + 2 >= mend) break;
+            step(m + 2, Z, X, Y, Zs, Xs, Ys);
         }
     }
     if (RESID) {
@@ -325,8 +323,8 @@ void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, c
     const int zb = relax_tiled_zb(dim, Nc);
     if (dim == 3) {
         using TL = Tile<3>;
-        const dim3 grid((Nc + TL::X - 1) / TL::X, (Nc + TL::Y - 1) / TL::Y, (Nc + zb - 1) / zb);
-        launch_dim<3, MODE>(grid, dim3(TL::X, TL::Y), sig, s, tm, uo, duo, L, zb, rc, bc, slot, flag);
+        const dim3 grid((Nc + TL::X - 1) / TL::X, (Nc + TL::ROWS - 1) / TL::ROWS, (Nc + zb - 1) / zb);
+        launch_dim<3, MODE>(grid, dim3(TL::X, TL::TY), sig, s, tm, uo, duo, L, zb, rc, bc, slot, flag);
     } else {
         using TL = Tile<2>;
         const dim3 grid((Nc + TL::X - 1) / TL::X, 1, (Nc + zb - 1) / zb);
@@ -337,14 +335,14 @@ void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, c
 }  // namespace
 
 int relax_tiled_zb(int dim, int N) {
-    if (dim == 2) return N >= 1024 ? 64 : 32;
-    return N >= 256 ? 32 : 16;
+    if (dim == 2) return N >= 1024 ? 128 : 32;
+    return N >= 512 ? 64 : (N >= 128 ? 32 : 16);
 }
 
 void tile_boxes(int dim, unsigned* box_u, unsigned* box_g) {
     if (dim == 3) {
-        box_u[0] = Tile<3>::HX; box_u[1] = Tile<3>::HY; box_u[2] = 1;
-        box_g[0] = Tile<3>::HX; box_g[1] = Tile<3>::Y;  box_g[2] = 1;
+        box_u[0] = Tile<3>::HX; box_u[1] = Tile<3>::HY;   box_u[2] = 1;
+        box_g[0] = Tile<3>::HX; box_g[1] = Tile<3>::ROWS; box_g[2] = 1;
     } else {
         box_u[0] = Tile<2>::HX; box_u[1] = 1; box_u[2] = 1;
         box_g[0] = Tile<2>::HX; box_g[1] = 1; box_g[2] = 1;
