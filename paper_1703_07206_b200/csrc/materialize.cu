@@ -14,11 +14,13 @@
 //         = ((base + I_l0(du0)) + I_l1(du1)) + ...   (everything else)
 //
 // with I_l(du)(x) = sum over corners r, q, p of ((wz*wy)*wx) * du[corner]
-// (all weights exact dyadics; zero-weight corners skipped: sign of zero only).
-// A thread owns MV = 4 consecutive x nodes.  For every level coarser than
-// the first the four nodes share one cell, so the 8 corner loads serve four
-// nodes; y and z are uniform across a warp, so the zero-weight corner rows
-// are skipped without divergence.  Chain descriptors sit in shared memory.
+// (all weights exact dyadics; zero-weight corner rows in y / z are skipped,
+// which changes at most the sign of an exact zero).
+// A thread owns MV = 4 consecutive x nodes and accumulates them corner by
+// corner (four interleaved chains).  For every level coarser than the first
+// the four nodes share one cell, so the 8 corner loads serve four nodes; y
+// and z are uniform across a warp, so the zero-weight corner rows are skipped
+// without divergence.  Chain descriptors sit in shared memory.
 #include <cuda_runtime.h>
 
 #include "device.cuh"
@@ -59,52 +61,56 @@ __global__ void __launch_bounds__(MBX* MBY)
             const ChainEntry ce = sch[c];
             const int l = ce.level, Nl = ce.L.N;
             const int msk = (1 << l) - 1;
-            const double inv = 1.0 / (double)(1 << l);  // exact power of two
+            const double inv = __longlong_as_double((long long)(1023 - l) << 52);  // 2^-l, exact
             const int iy = y & msk, iz = z & msk;
             const double fy = (double)iy * inv, fz = (double)iz * inv;
             const double wy[2] = {1.0 - fy, fy};
             const double wz[2] = {1.0 - fz, fz};
             const int nq = iy ? 2 : 1, nr = (DIM == 3 && iz) ? 2 : 1;  // warp-uniform
-            const int x0 = X4 << w;
-            const int X0 = x0 >> l;
-            // corner columns X0, X0+1, X0+2 (the third only when the run
-            // straddles two cells, i.e. l == w + 1)
-            double cc[2][2][3];
-#pragma unroll
-            for (int r = 0; r < 2; ++r)
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    if (r < nr && q < nq) {
-                        const double* row = ce.du + eix<DIM>(ce.L, X0, (y >> l) + q, DIM == 3 ? (z >> l) + r : 0);
-#pragma unroll
-                        for (int p = 0; p < 3; ++p) cc[r][q][p] = X0 + p < Nl ? __ldg(row + p) : 0.0;
-                    } else {
-#pragma unroll
-                        for (int p = 0; p < 3; ++p) cc[r][q][p] = 0.0;
-                    }
-                }
+            const int X0 = (X4 << w) >> l;
+            // the run of MV nodes straddles two cells only on level w + 1
+            const bool straddle = l == w + 1;
+            double fx[MV], wx0[MV];
+            int jk[MV];
 #pragma unroll
             for (int k = 0; k < MV; ++k) {
                 const int x = (X4 + k) << w;
-                const int ix = x & msk;
-                const int j = (x >> l) - X0;  // 0 or 1
-                const double fx = (double)ix * inv;
-                const double wx0 = 1.0 - fx, wx1 = fx;
-                double acc = 0.0;
+                fx[k] = (double)(x & msk) * inv;
+                wx0[k] = 1.0 - fx[k];
+                jk[k] = straddle ? (x >> l) - X0 : 0;
+            }
+            double acc[MV];
+            // `st` is a literal at both call sites: the straddle selects vanish
+            // from the common (same-cell) path
+            auto accumulate = [&](bool st) {
 #pragma unroll
                 for (int r = 0; r < 2; ++r)
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         if (r < nr && q < nq) {
+                            const double* row =
+                                ce.du + eix<DIM>(ce.L, X0, (y >> l) + q, DIM == 3 ? (z >> l) + r : 0);
+                            const double c0 = __ldg(row);
+                            const double c1 = X0 + 1 < Nl ? __ldg(row + 1) : 0.0;
+                            const double c2 = (st && X0 + 2 < Nl) ? __ldg(row + 2) : 0.0;
                             const double wzy = DIM == 3 ? wz[r] * wy[q] : wy[q];
-                            const double ca = j ? cc[r][q][1] : cc[r][q][0];
-                            const double cb = j ? cc[r][q][2] : cc[r][q][1];
-                            acc = acc + ((wzy * wx0) * ca);
-                            if (ix) acc = acc + ((wzy * wx1) * cb);
+                            // reference order per node: corner p = 0 then p = 1 of this
+                            // (r, q); a zero-weight p = 1 term adds +-0 (as the reference)
+#pragma unroll
+                            for (int k = 0; k < MV; ++k) {
+                                const double ca = (st && jk[k]) ? c1 : c0;
+                                const double cb = (st && jk[k]) ? c2 : c1;
+                                const double t0 = (wzy * wx0[k]) * ca;
+                                acc[k] = (r == 0 && q == 0) ? t0 : acc[k] + t0;
+                                acc[k] = acc[k] + ((wzy * fx[k]) * cb);
+                            }
                         }
                     }
-                val[k] = val[k] + acc;
-            }
+            };
+            if (straddle) accumulate(true);
+            else accumulate(false);
+#pragma unroll
+            for (int k = 0; k < MV; ++k) val[k] = val[k] + acc[k];
         }
         const bool jface = J == 0 || J == Nw - 1 || (DIM == 3 && (K == 0 || K == Nw - 1));
         const int fmask = (1 << frel) - 1;

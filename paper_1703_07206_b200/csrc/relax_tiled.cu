@@ -105,6 +105,26 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
         (edge_tile && (!bc.neu[0] || !bc.neu[1] || (DIM == 3 && (!bc.neu[2] || !bc.neu[3])))) ||
         (m0 == 0 && !bc.neu[fm]) || (mend == N && !bc.neu[fm + 1]);
 
+    // per-row constants: output offset at plane 0, Dirichlet status of the
+    // column (x/y faces outrank the marching-axis faces, grid.cpp:53-62) and
+    // whether the node has mirror ghost cells in x/y
+    ptrdiff_t obase[RT];
+    bool dir_row[RT], mir_row[RT];
+    double val_row[RT];
+#pragma unroll
+    for (int a = 0; a < RT; ++a) {
+        const int j = DIM == 3 ? yb + a : 0;
+        obase[a] = eix<DIM>(L, xi, j, -1);  // + (m + 1) * plane
+        if (DIM == 2) obase[a] = (ptrdiff_t)(xi + 1);
+        dir_row[a] = (xi == 0 && !bc.neu[0]) || (xi == N - 1 && !bc.neu[1]) ||
+                     (DIM == 3 && ((j == 0 && !bc.neu[2]) || (j == N - 1 && !bc.neu[3])));
+        val_row[a] = rc.homogeneous ? 0.0 : dirichlet_value<DIM>(bc, N, xi, j, 0);
+        mir_row[a] = xi == 1 || xi == N - 2 || (DIM == 3 && (j == 1 || j == N - 2));
+    }
+    const bool dir_lo = !bc.neu[fm], dir_hi = !bc.neu[fm + 1];
+    const double val_lo = rc.homogeneous ? 0.0 : bc.val[fm];
+    const double val_hi = rc.homogeneous ? 0.0 : bc.val[fm + 1];
+
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&R.full[s], 1);
@@ -190,42 +210,47 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
 
     // finish one node: op, diag / residual, Euler step, Dirichlet override, store
     auto finish = [&](int m, int a, double acc, double smax, double uc, double gc, double tc) {
-        const int i = xi, j = DIM == 3 ? yb + a : m, k = DIM == 3 ? m : 0;
+        const ptrdiff_t pos = obase[a] + (ptrdiff_t)(m + 1) * L.plane;
         bool dir = false;
-        if (maybe_dir) dir = on_dirichlet<DIM>(bc, N, i, j, k);
+        double dval = 0.0;
+        if (maybe_dir) {
+            dir = dir_row[a] || (m == 0 && dir_lo) || (m == N - 1 && dir_hi);
+            dval = dir_row[a] ? val_row[a] : (m == 0 && dir_lo ? val_lo : val_hi);
+        }
         const double op = (acc * rc.pref) * rc.inv_s2;
-        if constexpr (RESID) {
-            double rn = gc - (HAS_A ? op + rc.a * uc : op);
-            if (dir) rn = 0.0;
-            const double ar = fabs(rn);
-            dmax = dmax < ar ? ar : dmax;
-            store_ext<DIM>(uo, L, i, j, k, rn);
-            if (with_t) duo[eix<DIM>(L, i, j, k)] = tc + uc;
-            return;
-        }
-        const double omg = op - gc;
-        const double diag = HAS_A ? fabs((op + rc.a * uc) - gc) : fabs(omg);
         double value;
-        if constexpr (SIG) {
-            const double dtau = (rc.safety * rc.kdim) / (rc.inv_s2 * smax);
-            if (!(dtau > 0.0)) {
-                value = __longlong_as_double(0x7ff8000000000000LL);
+        if constexpr (RESID) {
+            value = gc - (HAS_A ? op + rc.a * uc : op);
+            if (dir) value = 0.0;
+            const double ar = fabs(value);
+            dmax = dmax < ar ? ar : dmax;
+            if (with_t) duo[pos] = tc + uc;
+        } else {
+            const double omg = op - gc;
+            const double diag = HAS_A ? fabs((op + rc.a * uc) - gc) : fabs(omg);
+            if constexpr (SIG) {
+                const double dtau = (rc.safety * rc.kdim) / (rc.inv_s2 * smax);
+                if (!(dtau > 0.0)) {
+                    value = __longlong_as_double(0x7ff8000000000000LL);
+                } else {
+                    const double num = uc + dtau * omg;
+                    value = HAS_A ? num / (1.0 - dtau * rc.a) : num;
+                }
             } else {
-                const double num = uc + dtau * omg;
-                value = HAS_A ? num / (1.0 - dtau * rc.a) : num;
+                const double num = uc + rc.dtau1 * omg;
+                value = HAS_A ? num / rc.denom1 : num;
             }
-        } else {
-            const double num = uc + rc.dtau1 * omg;
-            value = HAS_A ? num / rc.denom1 : num;
+            if (dir) {
+                value = dval;
+            } else {
+                dmax = dmax < diag ? diag : dmax;
+            }
+            bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
+            if (duo) duo[pos] = value - uc;
         }
-        if (dir) {
-            value = rc.homogeneous ? 0.0 : dirichlet_value<DIM>(bc, N, i, j, k);
-        } else {
-            dmax = dmax < diag ? diag : dmax;
-        }
-        bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
-        store_ext<DIM>(uo, L, i, j, k, value);
-        if (duo) duo[eix<DIM>(L, i, j, k)] = value - uc;
+        uo[pos] = value;
+        if (mir_row[a] || m == 1 || m == N - 2)
+            store_mirrors<DIM>(uo, L, xi, DIM == 3 ? yb + a : m, DIM == 3 ? m : 0, value);
     };
 
     Win<DIM> X, Y, Z;  // window planes, rotating roles
