@@ -1,0 +1,357 @@
+// sgml_cpp.cpp — the reference's C++ solver API (include/sgml/*.hpp) on top of
+// the C-ABI (include/sgml_b200.h).  A reference caller recompiles against
+// these headers, links libsgml_b200.so instead of proj/core, and every
+// solve-path call runs on the B200.
+//
+// Error behaviour mirrors the reference: std::invalid_argument for bad
+// inputs, sgml::kernel_error for non-finite values / non-positive steps,
+// std::logic_error / std::out_of_range for misuse, std::runtime_error for
+// device failures.
+#include <cmath>
+#include <cstdlib>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sgml/cycle.hpp"
+#include "../../include/sgml/grid.hpp"
+#include "../../include/sgml/kernels.hpp"
+#include "../../include/sgml_b200.h"
+
+namespace sgml {
+
+namespace {
+
+void check(int status) {
+    if (status == SGML_OK) return;
+    const std::string msg = sgml_last_error();
+    switch (status) {
+        case SGML_EINVAL: throw std::invalid_argument(msg);
+        case SGML_EBADSTEP:
+        case SGML_ENONFINITE: throw kernel_error(msg);
+        case SGML_ELOGIC: throw std::logic_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+// One context per process on SGML_DEVICE (default 0), created on first use.
+sgml_ctx* context() {
+    static std::once_flag once;
+    static sgml_ctx* ctx = nullptr;
+    std::call_once(once, [] {
+        const char* d = std::getenv("SGML_DEVICE");
+        check(sgml_ctx_create(d ? std::atoi(d) : 0, &ctx));
+    });
+    return ctx;
+}
+
+sgml_bc to_c(const BoundarySpec& bc) {
+    sgml_bc b{};
+    for (int f = 0; f < 6; ++f) {
+        b.kind[f] = bc.faces[f].kind == BcKind::neumann ? 1 : 0;
+        b.value[f] = bc.faces[f].value;
+    }
+    return b;
+}
+
+// device copy of a host field for the duration of one call
+struct Dev {
+    sgml_field* f = nullptr;
+    explicit Dev(const Grid& g) { check(sgml_field_create(context(), g.dim, g.n, &f)); }
+    Dev(const Field& h) : Dev(h.grid()) { check(sgml_field_upload(f, h.data())); }
+    ~Dev() { sgml_field_destroy(f); }
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+    void to(Field& h) const { check(sgml_field_download(f, h.data())); }
+};
+
+}  // namespace
+
+// ---- grid.hpp --------------------------------------------------------------
+
+Grid make_grid(int dim, int n) {
+    sgml_grid g{};
+    check(sgml_make_grid(dim, n, &g));
+    return Grid{g.dim, g.n, g.N, g.h, static_cast<std::size_t>(g.total)};
+}
+
+BoundarySpec BoundarySpec::all_dirichlet(double value) {
+    BoundarySpec b;
+    for (auto& f : b.faces) f = FaceBc{BcKind::dirichlet, value};
+    return b;
+}
+
+BoundarySpec BoundarySpec::all_neumann() {
+    BoundarySpec b;
+    for (auto& f : b.faces) f = FaceBc{BcKind::neumann, 0.0};
+    return b;
+}
+
+bool BoundarySpec::any_dirichlet(int dim) const {
+    for (int f = 0; f < 2 * dim; ++f)
+        if (faces[f].kind == BcKind::dirichlet) return true;
+    return false;
+}
+
+bool BoundarySpec::on_dirichlet(const NodeIndex& idx, int dim, int N) const {
+    const int c[3] = {idx.i, idx.j, idx.k};
+    for (int a = 0; a < dim; ++a)
+        if ((c[a] == 0 && face(a, 0).kind == BcKind::dirichlet) ||
+            (c[a] == N - 1 && face(a, 1).kind == BcKind::dirichlet))
+            return true;
+    return false;
+}
+
+double BoundarySpec::dirichlet_value(const NodeIndex& idx, int dim, int N) const {
+    const int c[3] = {idx.i, idx.j, idx.k};
+    for (int a = 0; a < dim; ++a) {
+        if (c[a] == 0 && face(a, 0).kind == BcKind::dirichlet) return face(a, 0).value;
+        if (c[a] == N - 1 && face(a, 1).kind == BcKind::dirichlet) return face(a, 1).value;
+    }
+    throw std::logic_error("dirichlet_value: node is not on a Dirichlet face");
+}
+
+// ---- kernels.hpp -----------------------------------------------------------
+
+void restriction_into(const Field& f, int v, const BoundarySpec& bc, Field& out, Field& scratch,
+                      std::uint64_t* work) {
+    if (&out == &scratch) throw std::invalid_argument("restriction_into: out and scratch must differ");
+    Dev df(f), dout(f.grid()), dscr(f.grid());
+    const sgml_bc b = to_c(bc);
+    check(sgml_restriction_into(df.f, v, &b, dout.f, dscr.f, work));
+    if (out.grid() != f.grid() || out.size() != f.size()) out = Field(f.grid());
+    dout.to(out);
+}
+
+Field restriction(const Field& f, int v, const BoundarySpec& bc, std::uint64_t* work) {
+    Field out(f.grid()), scratch(f.grid());
+    restriction_into(f, v, bc, out, scratch, work);
+    return out;
+}
+
+double relaxation_interpolation(SolveState& state, const Field& g, const Field* sigma_level, double a,
+                                double safety, const BoundarySpec& bc, bool homogeneous, std::uint64_t* work) {
+    const Grid& gr = state.u_prev.grid();
+    Dev u(gr), du(gr), up(state.u_prev), dup(state.du_prev), dg(g);
+    std::unique_ptr<Dev> ds;
+    if (sigma_level) ds = std::make_unique<Dev>(*sigma_level);
+    const sgml_bc b = to_c(bc);
+    double diag = 0.0;
+    const int st = sgml_relaxation_interpolation(u.f, up.f, du.f, dup.f, state.level, dg.f, ds ? ds->f : nullptr,
+                                                 a, safety, &b, homogeneous ? 1 : 0, &diag, work);
+    if (st == SGML_OK || st == SGML_ENONFINITE || st == SGML_EBADSTEP) {  // outputs written either way
+        u.to(state.u);
+        du.to(state.du);
+    }
+    check(st);
+    return diag;
+}
+
+void residual_update(Field& r, const Field& e, const OperatorCoefficients& coeff, const BoundarySpec& bc) {
+    Dev dr(r), de(e);
+    std::unique_ptr<Dev> ds;
+    if (coeff.sigma) ds = std::make_unique<Dev>(*coeff.sigma);
+    const sgml_bc b = to_c(bc);
+    check(sgml_residual_update(dr.f, de.f, ds ? ds->f : nullptr, coeff.a, &b));
+    dr.to(r);
+}
+
+Field residual(const Field& u, const Field& f, const OperatorCoefficients& coeff, const BoundarySpec& bc) {
+    Field r = f;
+    residual_update(r, u, coeff, bc);
+    return r;
+}
+
+double trapezoid_mean(const Field& f) {
+    Dev d(f);
+    double m = 0.0;
+    check(sgml_trapezoid_mean(d.f, &m));
+    return m;
+}
+
+void zero_mean_projection(Field& f) {
+    Dev d(f);
+    check(sgml_zero_mean_projection(d.f));
+    d.to(f);
+}
+
+void apply_boundary(Field& u, const BoundarySpec& bc, bool homogeneous) {
+    Dev d(u);
+    const sgml_bc b = to_c(bc);
+    check(sgml_apply_boundary(d.f, &b, homogeneous ? 1 : 0));
+    d.to(u);
+}
+
+double max_abs(const Field& f) {
+    Dev d(f);
+    double m = 0.0;
+    check(sgml_max_abs(d.f, &m));
+    return m;
+}
+
+// ---- cycle.hpp -------------------------------------------------------------
+
+CycleSchedule build_schedule(int n, int n_r) {
+    int count = 0;
+    check(sgml_build_schedule(n, n_r, nullptr, nullptr, nullptr, 0, &count));
+    std::vector<int> k(count), l(count), c(count);
+    check(sgml_build_schedule(n, n_r, k.data(), l.data(), c.data(), count, &count));
+    CycleSchedule s;
+    s.n = n;
+    s.n_r = n_r;
+    for (int i = 0; i < count; ++i)
+        s.steps.push_back(ScheduleStep{k[i] == 0 ? ScheduleStep::Kind::restrict_source : ScheduleStep::Kind::relax,
+                                       l[i], c[i]});
+    return s;
+}
+
+std::uint64_t closed_form_work_units(int n, int n_r) { return sgml_closed_form_work_units(n, n_r); }
+
+std::uint64_t schedule_work_units(const CycleSchedule& schedule) {
+    std::uint64_t total = 0;
+    for (const ScheduleStep& st : schedule.steps)
+        total += st.kind == ScheduleStep::Kind::restrict_source ? static_cast<std::uint64_t>(st.level)
+                                                                 : static_cast<std::uint64_t>(st.count);
+    return total;
+}
+
+namespace {
+
+std::size_t relax_passes(int n, int n_r) {
+    std::size_t p = 0;
+    for (const ScheduleStep& st : build_schedule(n, n_r).steps)
+        if (st.kind == ScheduleStep::Kind::relax) p += static_cast<std::size_t>(st.count);
+    return p;
+}
+
+struct HookData {
+    const ExactSolution* exact;
+    Grid grid;
+};
+
+int l1_hook(void* user, int, const sgml_field* u_total, double* l1) {
+    const HookData* hd = static_cast<const HookData*>(user);
+    Field u(hd->grid);
+    if (sgml_field_download(u_total, u.data()) != SGML_OK) return 0;
+    *l1 = l1_error(u, *hd->exact);
+    return 1;
+}
+
+}  // namespace
+
+void single_cycle(SolveState& state, const Field& source, const std::vector<Field>& sigma_levels, double a,
+                  const BoundarySpec& bc, bool homogeneous, const CycleSchedule& schedule, double safety,
+                  int cycle_index, double normalization, SolveReport& report, std::uint64_t& work_units) {
+    const Grid& g = source.grid();
+    Dev su(g), src(source);
+    std::vector<std::unique_ptr<Dev>> lv;
+    std::vector<sgml_field*> lvp;
+    for (const Field& f : sigma_levels) {
+        lv.push_back(std::make_unique<Dev>(f));
+        lvp.push_back(lv.back()->f);
+    }
+    const sgml_bc b = to_c(bc);
+    std::vector<sgml_diag_sample> trace(relax_passes(g.n, schedule.n_r));
+    sgml_report rep{};
+    rep.trace = trace.data();
+    rep.trace_cap = static_cast<int64_t>(trace.size());
+    const int st = sgml_single_cycle(context(), su.f, src.f, lvp.empty() ? nullptr : lvp.data(), a, &b,
+                                     homogeneous ? 1 : 0, schedule.n_r, safety, cycle_index, normalization,
+                                     nullptr, &rep, &work_units);
+    for (int64_t t = 0; t < std::min<int64_t>(rep.n_trace, rep.trace_cap); ++t)
+        report.trace.push_back(DiagSample{trace[t].cycle, trace[t].pass, trace[t].level, trace[t].value});
+    check(st);
+    su.to(state.u);
+}
+
+SolveResult solve(const ProblemSpec& problem, const SolverConfig& config) {
+    const Grid& g = problem.grid;
+    if (problem.f.grid() != g) throw std::invalid_argument("solve: source grid mismatch");
+    if (problem.sigma.size() && problem.sigma.grid() != g)
+        throw std::invalid_argument("solve: sigma grid mismatch");
+    if (!(config.tol > 0.0)) throw std::invalid_argument("solve: tol must be positive");
+    if (config.n_r < 1) throw std::invalid_argument("solve: n_r must be >= 1");
+
+    SolveResult result{Field(g), {}};
+    const int max_rows = std::max(1, config.max_cycles);
+    std::vector<sgml_cycle_record> rows(static_cast<std::size_t>(max_rows));
+    std::vector<sgml_diag_sample> trace(static_cast<std::size_t>(max_rows) * relax_passes(g.n, config.n_r));
+    sgml_report rep{};
+    rep.rows = rows.data();
+    rep.rows_cap = max_rows;
+    rep.trace = trace.data();
+    rep.trace_cap = static_cast<int64_t>(trace.size());
+    HookData hd{&problem.exact, g};
+    if (problem.exact) {
+        rep.hook = &l1_hook;
+        rep.hook_user = &hd;
+    }
+    const sgml_bc b = to_c(problem.bc);
+    const sgml_solver_cfg cfg{config.n_r, config.max_cycles, config.tol, config.safety};
+    check(sgml_solve(context(), g.dim, g.n, &b, problem.f.data(),
+                     problem.sigma.size() ? problem.sigma.data() : nullptr, problem.a, &cfg, nullptr,
+                     result.u.data(), &rep));
+    SolveReport& out = result.report;
+    for (int64_t i = 0; i < std::min<int64_t>(rep.n_rows, rep.rows_cap); ++i) {
+        CycleRecord r{rows[i].cycle, rows[i].work_units, rows[i].residual, rows[i].diag_min, std::nullopt};
+        if (rows[i].has_l1) r.l1_error = rows[i].l1_error;
+        out.rows.push_back(r);
+    }
+    for (int64_t t = 0; t < std::min<int64_t>(rep.n_trace, rep.trace_cap); ++t)
+        out.trace.push_back(DiagSample{trace[t].cycle, trace[t].pass, trace[t].level, trace[t].value});
+    out.converged = rep.converged != 0;
+    out.nan_detected = rep.nan_detected != 0;
+    out.stagnated = rep.stagnated != 0;
+    out.normalization = rep.normalization;
+    out.node_updates = rep.node_updates;
+    return result;
+}
+
+void pure_neumann_pin(Field& u) { zero_mean_projection(u); }
+
+std::vector<Field> restrict_sigma_levels(const Field& sigma, int n) {
+    std::vector<Field> levels;
+    if (!sigma.size()) return levels;
+    Dev ds(sigma);
+    std::vector<std::unique_ptr<Dev>> lv;
+    std::vector<sgml_field*> lvp;
+    for (int v = 0; v < n; ++v) {
+        lv.push_back(std::make_unique<Dev>(sigma.grid()));
+        lvp.push_back(lv.back()->f);
+    }
+    check(sgml_restrict_sigma_levels(ds.f, lvp.data()));
+    for (int v = 0; v < n; ++v) {
+        levels.emplace_back(sigma.grid());
+        lv[static_cast<std::size_t>(v)]->to(levels.back());
+    }
+    return levels;
+}
+
+// problems.cpp:195-215: serial compensated sums of w|u - exact| and w|exact|
+// with trapezoid weights (1/2 per face axis).
+double l1_error(const Field& v_h, const ExactSolution& exact) {
+    if (!exact) throw std::invalid_argument("l1_error: no exact solution");
+    const Grid& g = v_h.grid();
+    double num = 0.0, cnum = 0.0, den = 0.0, cden = 0.0;
+    for (std::size_t p = 0; p < v_h.size(); ++p) {
+        const NodeIndex x = v_h.node_of(p);
+        double w = (x.i == 0 || x.i == g.N - 1) ? 0.5 : 1.0;
+        w *= (x.j == 0 || x.j == g.N - 1) ? 0.5 : 1.0;
+        if (g.dim == 3) w *= (x.k == 0 || x.k == g.N - 1) ? 0.5 : 1.0;
+        const double ue = exact(x.i * g.h, x.j * g.h, x.k * g.h);
+        double y = w * std::abs(v_h[p] - ue) - cnum;
+        double t = num + y;
+        cnum = (t - num) - y;
+        num = t;
+        y = w * std::abs(ue) - cden;
+        t = den + y;
+        cden = (t - den) - y;
+        den = t;
+    }
+    if (den == 0.0) throw std::invalid_argument("l1_error: exact solution is identically zero");
+    return num / den;
+}
+
+}  // namespace sgml
