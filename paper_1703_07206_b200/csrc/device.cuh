@@ -102,6 +102,15 @@ __device__ __forceinline__ double mirror(const double* __restrict__ u, int N, in
 // acc + ((sbar*(un-uc)) * inv_l2) with the exact shortcuts for sbar == 1 and
 // inv_l2 == 1 (l2 = 1: face neighbours).
 template <bool SIG>
+__device__ __forceinline__ double stencil_t(double sbar, double un, double uc, int l2) {
+    double t = un - uc;
+    if (SIG) t = sbar * t;
+    if (l2 == 2) t = t * 0.5;
+    else if (l2 == 3) t = t * kInv3;
+    return t;
+}
+
+template <bool SIG>
 __device__ __forceinline__ double stencil_term(double acc, double sbar, double un, double uc, int l2) {
     double t = un - uc;
     if (SIG) t = sbar * t;
@@ -354,6 +363,40 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
+        : "memory");
+}
+// shared-window (u32) address variants for hot loops: no generic->shared
+// conversion per use
+__device__ __forceinline__ void mbar_expect_tx_u32(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_u32(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_u32(unsigned dst, const void* map, int c0, int c1, int c2,
+                                                unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];\n" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_u32(unsigned dst, const void* map, int c0, int c1, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const void* map, int c0, int c1, int c2,

@@ -313,6 +313,19 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
     if (compact()) {
         Lv.resize(n);
         for (int v = 0; v < n; ++v) Lv[v] = make_ext(dim, Nl[v]);
+        // nodes off the Dirichlet faces, per level; face values
+        rng.assign(n, NodeRange{});
+        for (int v = 0; v < n; ++v)
+            for (int ax = 0; ax < 3; ++ax) {
+                const bool live = ax < dim;
+                rng[v].lo[ax] = live && bc_host.kind[2 * ax] == 0 ? 1 : 0;
+                rng[v].hi[ax] = !live ? 0 : (bc_host.kind[2 * ax + 1] == 0 ? Nl[v] - 2 : Nl[v] - 1);
+            }
+        for (int f = 0; f < 2 * dim; ++f)
+            if (bc_host.kind[f] == 0) {
+                bval_zero = bval_zero && bc_host.value[f] == 0.0;
+                bval_finite = bval_finite && std::isfinite(bc_host.value[f]);
+            }
         const uint64_t E0 = ext_size(dim, Lv[0]);
         r = alloc(E0);
         utot = alloc(E0);
@@ -370,9 +383,33 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
             for (int v = 0; v < n; ++v) Lsig[v] = alloc(T);
         }
     }
+    if (compact()) {
+        // alloc() zeroes: every level buffer starts with zero faces
+        fstate[r] = FS_ZERO;
+        fstate[utot] = FS_ZERO;
+        fstate[A] = FS_ZERO;
+        fstate[B] = FS_ZERO;
+        for (int v = 1; v < n; ++v) {
+            fstate[U[v][0]] = FS_ZERO;
+            fstate[U[v][1]] = FS_ZERO;
+            for (double* d : DU[v]) fstate[d] = FS_ZERO;
+        }
+    }
     if (has_sigma) load_sigma(sigma_dev);
     SGML_CUDA(cudaGetLastError());
     SGML_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+int sgml_solver::faces_of(const double* p) const {
+    const auto it = fstate.find(p);
+    return it == fstate.end() ? FS_OTHER : it->second;
+}
+
+void sgml_solver::set_faces(double* p, int level, int st) {
+    if (all_neumann || faces_of(p) == st) return;
+    if (st == FS_OTHER) fail(SGML_ELOGIC, "set_faces: no target content");
+    launch(SGML_CLASS_OTHER, [&] { launch_dirichlet_faces(g.dim, p, Lv[level], bc, st == FS_ZERO, ctx->stream); });
+    fstate[p] = st;
 }
 
 // cycle.cpp:117-133: sigma restricted per level with even (all-Neumann)
@@ -428,8 +465,10 @@ void sgml_solver::ensure_literal() {
 
 void sgml_solver::load_source(const double* f) {
     const cudaStream_t s = ctx->stream;
-    if (compact())
+    if (compact()) {
         launch(SGML_CLASS_OTHER, [&] { launch_scatter_ext(g.dim, f, r, Lv[0], s); });
+        fstate[r] = FS_OTHER;
+    }
     else
         SGML_CUDA(cudaMemcpyAsync(r, f, g.total * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
@@ -468,12 +507,22 @@ void sgml_solver::residual(const double* e) {
     unsigned long long* d_rmax = d_cycle + n_slots;
     const RelaxConst rc0 = relax_const(dim, 0, g.h, a, cfg.safety, false);
     if (compact()) {
+        // faces: r = 0 on Dirichlet nodes (kernels.cpp:351-358), u_tot += e
+        // there (e holds 0 or the face value)
+        set_faces(r, 0, FS_ZERO);
+        const int es = faces_of(e);
+        if (es == FS_BVAL) {
+            if (faces_of(utot) != FS_ZERO) fail(SGML_ELOGIC, "residual: u_tot faces out of step");
+            set_faces(utot, 0, FS_BVAL);
+        } else if (es != FS_ZERO) {
+            fail(SGML_ELOGIC, "residual: e faces unknown");
+        }
         TmaSet tm;
         tm.u = umap(e);
         tm.g = gmap(r);
         tm.s = has_sigma ? umap(S[0]) : tm.u;
         tm.t = gmap(utot);
-        launch(SGML_CLASS_RESIDUAL, [&] { launch_residual_tma(dim, has_sigma, tm, r, utot, Lv[0], rc0, bc, d_rmax, s); });
+        launch(SGML_CLASS_RESIDUAL, [&] { launch_residual_tma(dim, has_sigma, tm, r, utot, Lv[0], rng[0], rc0, d_rmax, s); });
     } else {
         const double inv_h2 = 1.0 / (g.h * g.h);
         const double pref = dim == 2 ? 0.5 : 3.0 / 13.0;
@@ -509,6 +558,9 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
     unsigned long long* diag = d_cycle;
     int* flag = d_flag;
 
+    // a non-finite Dirichlet value makes the first pass throw
+    // (kernels.cpp:228, 343-346); the kernels never write face nodes
+    if (!homogeneous && !bval_finite) SGML_CUDA(cudaMemsetAsync(flag, 1, 1, s));
     // restriction pyramid of the cycle's source (once per cycle, F4)
     for (int m = 0; m + 1 < n; ++m)
         launch(SGML_CLASS_PYRAMID, [&] {
@@ -528,13 +580,22 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
         for (int p = 1; p <= c; ++p) {
             double* out = cur == p0 ? p1 : p0;
             double* duo = (v > 0 && p < c) ? DU[v][p - 1] : nullptr;
+            // Dirichlet faces: out holds the face value of this cycle, du =
+            // face value - input face value (0, or the value on a zeroed input)
+            const int want = face_want(homogeneous), ins = faces_of(cur);
+            set_faces(out, v, want);
+            if (duo) {
+                if (ins == want) set_faces(duo, v, FS_ZERO);
+                else if (ins == FS_ZERO && want == FS_BVAL) set_faces(duo, v, FS_BVAL);
+                else fail(SGML_ELOGIC, "relax: input faces out of step");
+            }
             TmaSet tm;
             tm.u = umap(cur);
             tm.g = gmap(gsrc(v));
             tm.s = has_sigma ? umap(S[v]) : tm.u;
             tm.t = tm.g;
             launch(v == 0 ? SGML_CLASS_RELAX0 : SGML_CLASS_RELAX_COARSE, [&] {
-                launch_relax_tma(dim, has_sigma, tm, out, duo, Lv[v], rc, bc, diag + slot, flag, s);
+                launch_relax_tma(dim, has_sigma, tm, out, duo, Lv[v], rng[v], rc, diag + slot, flag, s);
             });
             ++slot;
             cur = out;
@@ -553,6 +614,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
             double* in = U[v][0];
             if (first) {
                 SGML_CUDA(cudaMemsetAsync(in, 0, ext_size(dim, Lv[v]) * sizeof(double), s));
+                fstate[in] = FS_ZERO;
             } else {
                 if (count + (c - 1) > kMaxChain) {
                     // fold the pending increments into a full-grid base
@@ -561,6 +623,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                         launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], base_zero, ufinal, Lv[v + 1],
                                             v + 1, ch, count, bc, homogeneous, flag, s);
                     });
+                    fstate[other] = face_want(homogeneous);
                     std::swap(base, other);
                     base_zero = false;
                     start += count;
@@ -573,6 +636,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                     launch_materialize4(dim, in, Lv[v], v, base, Lv[0], base_zero, ufinal, Lf, 1, ch, count, bc,
                                         homogeneous, flag, s);
                 });
+                fstate[in] = face_want(homogeneous);
             }
             ufinal = relax_level(v, in, c, U[v][0], U[v][1]);
             count += c - 1;
@@ -581,6 +645,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
         double* in0;
         if (first) {
             SGML_CUDA(cudaMemsetAsync(base, 0, E0 * sizeof(double), s));
+            fstate[base] = FS_ZERO;
             in0 = base;
         } else if (v1 >= 1) {
             const ChainEntry* ch = chain_at();
@@ -589,6 +654,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                 launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], base_zero, ufinal, Lf, 1, ch, count, bc,
                                     homogeneous, flag, s);
             });
+            fstate[other] = face_want(homogeneous);
             in0 = other;
         } else {
             in0 = base;

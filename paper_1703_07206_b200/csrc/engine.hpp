@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -175,4 +176,17 @@ struct sgml_solver {
     void pin_and_emit(double* u_out_dev);                // pure_neumann_pin + result
     void ensure_literal();
     double* alloc(size_t count);
+
+    // Dirichlet-face bookkeeping of the compact engine.  Relaxation and
+    // residual kernels cover only the nodes off the Dirichlet faces
+    // (rng[v]); the face nodes of every buffer keep a known content, tracked
+    // here, and are rewritten only when a consumer needs another one.
+    enum { FS_ZERO = 0, FS_BVAL = 1, FS_OTHER = 2 };
+    std::vector<sgmlb::NodeRange> rng;
+    bool bval_zero = true;     // every Dirichlet face value is 0
+    bool bval_finite = true;
+    std::unordered_map<const double*, int> fstate;
+    int face_want(bool homogeneous) const { return (homogeneous || bval_zero) ? FS_ZERO : FS_BVAL; }
+    int faces_of(const double* p) const;
+    void set_faces(double* p, int level, int st);
 };

@@ -64,18 +64,27 @@ struct TmaSet {
 void tile_boxes(int dim, unsigned* box_u, unsigned* box_g);
 int relax_tiled_zb(int dim, int N);
 
+// Box of data nodes a relaxation / residual launch covers: every node not on
+// a Dirichlet face (those keep their face value, resident in the buffers).
+struct NodeRange {
+    int lo[3], hi[3];
+};
 // One relaxation pass over a level array (every node a subset node):
 // uo (with mirror ghosts), duo = uo - ui (nullable, DU arrays), diag max
 // into diag_slot, non-finite flag.
 void launch_relax_tma(int dim, bool sig, const TmaSet& tm, double* uo, double* duo,
-                      const ExtLay& L, const RelaxConst& rc, const BcDev& bc,
+                      const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
                       unsigned long long* diag_slot, int* flag, cudaStream_t s);
-// Residual recurrence at level 0: r -= A(e) + a e, r = 0 on Dirichlet nodes
-// (tm.u = e, tm.g = r, r written with mirror ghosts), u_tot += e (tm.t /
-// utot, nullable), max|r| (slot nullable).  rc = relax_const(level 0).
+// Residual recurrence at level 0 over the range: r -= A(e) + a e (tm.u = e,
+// tm.g = r, r written with mirror ghosts), u_tot += e (tm.t / utot,
+// nullable), max|r| into rmax_slot.  rc = relax_const(level 0).
 void launch_residual_tma(int dim, bool sig, const TmaSet& tm, double* r, double* utot,
-                         const ExtLay& L, const RelaxConst& rc, const BcDev& bc,
+                         const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
                          unsigned long long* rmax_slot, cudaStream_t s);
+// Dirichlet-face nodes of an extended level array <- 0 (zero) or their face
+// value (the reference's lowest-face-id rule).
+void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc, bool zero,
+                            cudaStream_t s);
 // Materialise the level-w input of the next relax step from the tooth's
 // state: Dirichlet value, the finest relaxed level lf = w + frel (ufine) at
 // its subset nodes, or base + the pending increments chain[0..nchain).

@@ -16,11 +16,17 @@
 // with I_l(du)(x) = sum over corners r, q, p of ((wz*wy)*wx) * du[corner]
 // (all weights exact dyadics; zero-weight corner rows in y / z are skipped,
 // which changes at most the sign of an exact zero).
-// A thread owns MV = 4 consecutive x nodes and accumulates them corner by
-// corner (four interleaved chains).  For every level coarser than the first
-// the four nodes share one cell, so the 8 corner loads serve four nodes; y
-// and z are uniform across a warp, so the zero-weight corner rows are skipped
-// without divergence.  Chain descriptors sit in shared memory.
+// A thread owns MV = 4 consecutive x nodes in two "spread copies" along the
+// slowest axis (z in 3D, y in 2D): planes S and S + H with H = (Nw - 1) / 2.
+// Every chain level l has cells of 2^(l-w) target nodes, which divides H, so
+// the two copies see identical interpolation weights: each weight product
+// is formed once and used for 2 x 4 nodes.  For every level coarser than
+// the first, the four x nodes of a copy share one cell, so its 8 corner
+// loads serve four nodes; y and z are uniform across a warp, so zero-weight
+// corner rows are skipped without divergence.  The plane S = H holds the
+// last plane 2H alone (its second copy is computed redundantly and dropped).
+// Threads whose nodes all lie on Dirichlet faces skip the chain.  Chain
+// descriptors sit in shared memory.
 #include <cuda_runtime.h>
 
 #include "device.cuh"
@@ -44,20 +50,37 @@ __global__ void __launch_bounds__(MBX* MBY)
     for (int c = tid; c < nchain; c += MBX * MBY) sch[c] = chain[c];
     __syncthreads();
 
-    const int Nw = Lw.N;
+    const int Nw = Lw.N, H = (Nw - 1) >> 1;
     const int X4 = (blockIdx.x * MBX + threadIdx.x) * MV;
-    const int J = blockIdx.y * MBY + threadIdx.y;
-    const int K = blockIdx.z;
+    // 3D: row J, spread plane index S (block-uniform);  2D: spread row S
+    const int J = DIM == 3 ? blockIdx.y * MBY + threadIdx.y : 0;
+    const int S = DIM == 3 ? blockIdx.z : blockIdx.y * MBY + threadIdx.y;
     int bad = 0;
-    if (X4 < Nw && J < Nw) {
-        const int y = J << w, z = DIM == 3 ? K << w : 0;
+    if (X4 < Nw && J < Nw && S <= H) {
+        const int ncopy = S < H ? 2 : 1;
+        const int s0 = S < H ? S : 2 * H;
         const int nv = min(MV, Nw - X4);
-        double val[MV];
-#pragma unroll
-        for (int k = 0; k < MV; ++k)
-            val[k] = (!base_zero && k < nv) ? __ldg(base + eix<DIM>(L0, (X4 + k) << w, y, z)) : 0.0;
+        // node (k, copy cp): x = X4 + k, spread coordinate s0 + cp * H
+        auto node_j = [&](int cp) { return DIM == 3 ? J : s0 + cp * H; };
+        auto node_k = [&](int cp) { return DIM == 3 ? s0 + cp * H : 0; };
+        // every node of this thread on a Dirichlet face: nothing to interpolate
+        const bool xdir = nv == 1 && X4 == Nw - 1 && !bc.neu[1];
+        const bool rowdir = DIM == 3 ? ((J == 0 && !bc.neu[2]) || (J == Nw - 1 && !bc.neu[3]))
+                                     : (ncopy == 1 && !bc.neu[3]);
+        const bool pdir = DIM == 3 && ncopy == 1 && !bc.neu[5];
+        const int nch = (xdir || rowdir || pdir) ? 0 : nchain;
 
-        for (int c = 0; c < nchain; ++c) {
+        const int y = (DIM == 3 ? J : s0) << w, z = DIM == 3 ? s0 << w : 0;
+        double val[2][MV];
+#pragma unroll
+        for (int cp = 0; cp < 2; ++cp)
+#pragma unroll
+            for (int k = 0; k < MV; ++k)
+                val[cp][k] = (!base_zero && k < nv && cp < ncopy)
+                                 ? __ldg(base + eix<DIM>(L0, (X4 + k) << w, node_j(cp) << w, node_k(cp) << w))
+                                 : 0.0;
+
+        for (int c = 0; c < nch; ++c) {
             const ChainEntry ce = sch[c];
             const int l = ce.level, Nl = ce.L.N;
             const int msk = (1 << l) - 1;
@@ -68,6 +91,9 @@ __global__ void __launch_bounds__(MBX* MBY)
             const double wz[2] = {1.0 - fz, fz};
             const int nq = iy ? 2 : 1, nr = (DIM == 3 && iz) ? 2 : 1;  // warp-uniform
             const int X0 = (X4 << w) >> l;
+            // distance of the second copy's corners; 0 when it is a dummy
+            const ptrdiff_t dsp =
+                ncopy == 2 ? (ptrdiff_t)((Nl - 1) >> 1) * (DIM == 3 ? ce.L.plane : (long long)ce.L.Px) : 0;
             // the run of MV nodes straddles two cells only on level w + 1
             const bool straddle = l == w + 1;
             double fx[MV], wx0[MV];
@@ -79,7 +105,7 @@ __global__ void __launch_bounds__(MBX* MBY)
                 wx0[k] = 1.0 - fx[k];
                 jk[k] = straddle ? (x >> l) - X0 : 0;
             }
-            double acc[MV];
+            double acc[2][MV];
             // `st` is a literal at both call sites: the straddle selects vanish
             // from the common (same-cell) path
             auto accumulate = [&](bool st) {
@@ -90,19 +116,28 @@ __global__ void __launch_bounds__(MBX* MBY)
                         if (r < nr && q < nq) {
                             const double* row =
                                 ce.du + eix<DIM>(ce.L, X0, (y >> l) + q, DIM == 3 ? (z >> l) + r : 0);
-                            const double c0 = __ldg(row);
-                            const double c1 = X0 + 1 < Nl ? __ldg(row + 1) : 0.0;
-                            const double c2 = (st && X0 + 2 < Nl) ? __ldg(row + 2) : 0.0;
+                            double c0[2], c1[2], c2[2];
+#pragma unroll
+                            for (int cp = 0; cp < 2; ++cp) {
+                                const double* rw = row + cp * dsp;
+                                c0[cp] = __ldg(rw);
+                                c1[cp] = X0 + 1 < Nl ? __ldg(rw + 1) : 0.0;
+                                c2[cp] = (st && X0 + 2 < Nl) ? __ldg(rw + 2) : 0.0;
+                            }
                             const double wzy = DIM == 3 ? wz[r] * wy[q] : wy[q];
                             // reference order per node: corner p = 0 then p = 1 of this
                             // (r, q); a zero-weight p = 1 term adds +-0 (as the reference)
 #pragma unroll
                             for (int k = 0; k < MV; ++k) {
-                                const double ca = (st && jk[k]) ? c1 : c0;
-                                const double cb = (st && jk[k]) ? c2 : c1;
-                                const double t0 = (wzy * wx0[k]) * ca;
-                                acc[k] = (r == 0 && q == 0) ? t0 : acc[k] + t0;
-                                acc[k] = acc[k] + ((wzy * fx[k]) * cb);
+                                const double w0 = wzy * wx0[k], w1 = wzy * fx[k];
+#pragma unroll
+                                for (int cp = 0; cp < 2; ++cp) {
+                                    const double ca = (st && jk[k]) ? c1[cp] : c0[cp];
+                                    const double cb = (st && jk[k]) ? c2[cp] : c1[cp];
+                                    const double t0 = w0 * ca;
+                                    acc[cp][k] = (r == 0 && q == 0) ? t0 : acc[cp][k] + t0;
+                                    acc[cp][k] = acc[cp][k] + w1 * cb;
+                                }
                             }
                         }
                     }
@@ -110,22 +145,29 @@ __global__ void __launch_bounds__(MBX* MBY)
             if (straddle) accumulate(true);
             else accumulate(false);
 #pragma unroll
-            for (int k = 0; k < MV; ++k) val[k] = val[k] + acc[k];
+            for (int cp = 0; cp < 2; ++cp)
+#pragma unroll
+                for (int k = 0; k < MV; ++k) val[cp][k] = val[cp][k] + acc[cp][k];
         }
-        const bool jface = J == 0 || J == Nw - 1 || (DIM == 3 && (K == 0 || K == Nw - 1));
         const int fmask = (1 << frel) - 1;
 #pragma unroll
-        for (int k = 0; k < MV; ++k) {
-            if (k >= nv) break;
-            const int I = X4 + k;
-            double value = val[k];
-            if ((jface || I == 0 || I == Nw - 1) && on_dirichlet<DIM>(bc, Nw, I, J, K)) {
-                value = homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, I, J, K);
-            } else if (ufine && ((I | J | K) & fmask) == 0) {
-                value = __ldg(ufine + eix<DIM>(Lf, I >> frel, J >> frel, K >> frel));
+        for (int cp = 0; cp < 2; ++cp) {
+            if (cp >= ncopy) break;
+            const int Jn = node_j(cp), Kn = node_k(cp);
+            const bool jface = Jn == 0 || Jn == Nw - 1 || (DIM == 3 && (Kn == 0 || Kn == Nw - 1));
+#pragma unroll
+            for (int k = 0; k < MV; ++k) {
+                if (k >= nv) break;
+                const int I = X4 + k;
+                double value = val[cp][k];
+                if ((jface || I == 0 || I == Nw - 1) && on_dirichlet<DIM>(bc, Nw, I, Jn, Kn)) {
+                    value = homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, I, Jn, Kn);
+                } else if (ufine && ((I | Jn | Kn) & fmask) == 0) {
+                    value = __ldg(ufine + eix<DIM>(Lf, I >> frel, Jn >> frel, Kn >> frel));
+                }
+                bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
+                store_ext<DIM>(out, Lw, I, Jn, Kn, value);
             }
-            bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
-            store_ext<DIM>(out, Lw, I, J, K, value);
         }
     }
     block_or_commit(bad, flag);
@@ -183,6 +225,23 @@ __global__ void __launch_bounds__(128) k_gather_ext(const double* __restrict__ e
     dense[lin3(N, i, j, k)] = ext[eix<DIM>(L, i, j, k)];
 }
 
+// Dirichlet-face nodes (with their mirror ghosts) <- 0 or the face value.
+// One thread per (face, a, b); nodes on edges are written by several faces
+// with the same value (the lowest-face-id rule of dirichlet_value).
+template <int DIM>
+__global__ void __launch_bounds__(128) k_dirichlet_faces(double* a, ExtLay L, BcDev bc, int zero) {
+    const int N = L.N;
+    const int p = blockIdx.x * 32 + threadIdx.x, q = blockIdx.y * 4 + threadIdx.y, f = blockIdx.z;
+    if (p >= N || (DIM == 3 && q >= N) || (DIM == 2 && q > 0) || bc.neu[f]) return;
+    const int side = (f & 1) ? N - 1 : 0;
+    int i, j, k = 0;
+    if (f < 2) { i = side; j = p; k = q; }
+    else if (f < 4) { i = p; j = side; k = q; }
+    else { i = p; j = q; k = side; }
+    if (DIM == 2 && f < 2) { j = p; k = 0; }
+    store_ext<DIM>(a, L, i, j, k, zero ? 0.0 : dirichlet_value<DIM>(bc, N, i, j, k));
+}
+
 inline dim3 ext_grid(int dim, int N) { return dim3((N + 31) / 32, (N + 3) / 4, dim == 3 ? N : 1); }
 
 }  // namespace
@@ -205,8 +264,9 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
                          int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
                          bool homogeneous, int* flag, cudaStream_t s) {
     const int Nw = Lw.N;
-    const int threads_x = (Nw + MV - 1) / MV;
-    const dim3 grid((threads_x + MBX - 1) / MBX, (Nw + MBY - 1) / MBY, dim == 3 ? Nw : 1);
+    const int threads_x = (Nw + MV - 1) / MV, H = (Nw - 1) / 2;
+    const dim3 grid((threads_x + MBX - 1) / MBX, dim == 3 ? (Nw + MBY - 1) / MBY : (H + MBY) / MBY,
+                    dim == 3 ? H + 1 : 1);
     if (dim == 2)
         k_materialize4<2><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, base_zero, ufine, Lf, frel,
                                                           chain, nchain, bc, homogeneous, flag);
@@ -229,6 +289,15 @@ void launch_scatter_ext(int dim, const double* dense, double* ext, const ExtLay&
 void launch_gather_ext(int dim, const double* ext, const ExtLay& L, double* dense, cudaStream_t s) {
     if (dim == 2) k_gather_ext<2><<<ext_grid(2, L.N), dim3(32, 4), 0, s>>>(ext, L, dense);
     else k_gather_ext<3><<<ext_grid(3, L.N), dim3(32, 4), 0, s>>>(ext, L, dense);
+}
+
+void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc, bool zero,
+                            cudaStream_t s) {
+    const int N = L.N;
+    if (dim == 2)
+        k_dirichlet_faces<2><<<dim3((N + 31) / 32, 1, 4), dim3(32, 4), 0, s>>>(a, L, bc, zero ? 1 : 0);
+    else
+        k_dirichlet_faces<3><<<dim3((N + 31) / 32, (N + 3) / 4, 6), dim3(32, 4), 0, s>>>(a, L, bc, zero ? 1 : 0);
 }
 
 }  // namespace sgmlb

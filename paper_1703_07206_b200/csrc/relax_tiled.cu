@@ -1,18 +1,26 @@
 // relax_tiled.cu — the hot kernel: one relaxation pass over a level array of
 // the compact engine (every node a subset node, neighbours at +-1 index),
-// i.e. the reference's relax branch (kernels.cpp:94-137) and Dirichlet
-// branch (kernels.cpp:213-218) at any level v; and, in MODE_RESID, the fused
-// residual recurrence at level 0 (kernels.cpp:243-297 + cycle.cpp:194-198).
+// i.e. the reference's relax branch (kernels.cpp:94-137) at any level v; and,
+// in MODE_RESID, the fused residual recurrence at level 0 (kernels.cpp:243-297
+// + cycle.cpp:194-198).
+//
+// Range.  The kernel covers the box of nodes that are NOT on a Dirichlet face
+// (Neumann faces are included).  Dirichlet nodes take their face value in
+// every pass (kernels.cpp:213-218); the engine keeps that value resident in
+// the output buffers (engine.cpp, face states), so the kernel has no
+// boundary code at all, and the tile grid loses the thin boundary tiles.
 //
 // Storage: ghost-extended padded arrays (device.cuh, ExtLay), so the tile
-// halo never needs boundary code.  A CTA owns an X x ROWS column bundle (3D:
-// 32 x 16 nodes, 2D: 128 x 1) and marches along the slowest axis over `zb`
-// planes, one plane per step.  Thread 0 streams planes of u (tile + halo),
-// g (tile rows + x halo: TMA boxes must start 16-byte aligned) and sigma
-// into an NST-deep shared-memory ring with TMA (cp.async.bulk.tensor), one
-// full/empty mbarrier pair per slot: consumers wait on `full`, each warp
-// releases a slot on `empty` once it has read it, and the producer refills a
-// slot only after all warps released it (no __syncthreads in the march).
+// halo never needs boundary code either.  A CTA owns an X x ROWS column
+// bundle (3D: 32 x 16 nodes, 2D: 128 x 1) and marches along the slowest axis
+// over `zb` planes, one plane per step.  Planes of u (tile + halo), g (tile
+// rows + x halo) and sigma are streamed with TMA (cp.async.bulk.tensor) into
+// an NST-deep shared-memory ring, one full/empty mbarrier pair per slot.  TMA
+// boxes must start 16-byte aligned in x, so boxes start at the even cell at
+// or below the halo and the window carries an offset xoff in {0, 1}.  The
+// producer role rotates over the warps (warp (m - m0) % NWARPS issues plane
+// m + NST - 2 in step m), so every warp runs the same instruction stream;
+// consumers wait on `full`, each warp releases a slot on `empty`.
 //
 // In 3D every thread computes RT = 2 adjacent rows (y, y+1) of the plane: it
 // keeps a (RT+2) x 3 register window of each of planes m-1, m, m+1 (12
@@ -39,10 +47,11 @@ struct Tile {
     static constexpr int TY = DIM == 3 ? 8 : 1;        // thread rows
     static constexpr int RT = DIM == 3 ? 2 : 1;        // node rows per thread
     static constexpr int ROWS = TY * RT;               // node rows per CTA
-    static constexpr int HX = X + 2;
+    static constexpr int HXU = X + 4;                  // u / sigma box width (halo + alignment)
+    static constexpr int HXG = X + 2;                  // g / u_tot box width (alignment)
     static constexpr int HY = DIM == 3 ? ROWS + 2 : 1;
-    static constexpr int PLANE = HX * HY;              // u / sigma box (tile + halo)
-    static constexpr int GBOX = HX * ROWS;             // g / u_tot box (tile rows + x halo)
+    static constexpr int PLANE = HXU * HY;             // u / sigma box (tile + halo)
+    static constexpr int GBOX = HXG * ROWS;            // g / u_tot box (tile rows)
     static constexpr int THREADS = X * TY;
     static constexpr int NWARPS = THREADS / 32;
     static constexpr int WR = DIM == 3 ? RT + 2 : 1;   // window rows per plane
@@ -66,16 +75,17 @@ using Win = double[Tile<DIM>::WR][3];
 template <int DIM, bool SIG>
 using SWin = double[SIG ? Tile<DIM>::WR : 1][SIG ? 3 : 1];
 
-// MODE_RELAX:  uo <- relaxed u (with mirror ghosts), duo <- u - u_prev (optional),
-//              tm_g = source g, diag_slot <- max |A(u)+a u - g| over relax nodes.
-// MODE_RESID:  tm_u = e, tm_g = r, uo = r (updated in place: r -= A(e) + a e,
-//              0 on Dirichlet nodes), tm_t / duo = u_tot (+= e, optional),
-//              diag_slot <- max|r| (kernels.cpp:407-415).
-template <int DIM, bool SIG, bool HAS_A, int MODE>
+// MODE_RELAX:  uo <- relaxed u (with mirror ghosts), duo <- u - u_prev (DUO),
+//              tm_g = source g, diag_slot <- max |A(u)+a u - g| over the range.
+// MODE_RESID:  tm_u = e, tm_g = r, uo = r (updated in place: r -= A(e) + a e),
+//              tm_t / duo = u_tot (+= e, DUO), diag_slot <- max|r|
+//              (kernels.cpp:407-415; r is 0 on Dirichlet faces).
+// Range: data nodes [lo.x, hi.x] x [lo.y, hi.y] x [lo.z, hi.z] (2D: x, y).
+template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO>
 __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) : 4)
     k_relax_tma(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_g,
                 const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_t,
-                double* uo, double* duo, ExtLay L, int zb, RelaxConst rc, BcDev bc,
+                double* uo, double* duo, ExtLay L, int3 lo, int3 hi, int zb, RelaxConst rc,
                 unsigned long long* diag_slot, int* flag) {
     using TL = Tile<DIM>;
     constexpr int NST = TL::NST, RT = TL::RT, WR = TL::WR;
@@ -85,45 +95,31 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
 
     const int tx = threadIdx.x, ty = DIM == 3 ? threadIdx.y : 0;
     const int tid = tx + TL::X * ty;
-    const int lane = tid & 31;
+    const int lane = tid & 31, warp = tid >> 5;
     const int N = L.N;
-    const int x0 = blockIdx.x * TL::X, y0 = DIM == 3 ? blockIdx.y * TL::ROWS : 0;
-    const int m0 = blockIdx.z * zb;
-    const int mend = min(m0 + zb, N);  // exclusive
+    const int x0 = lo.x + blockIdx.x * TL::X;
+    const int y0 = DIM == 3 ? lo.y + blockIdx.y * TL::ROWS : 0;
+    const int zlo = DIM == 3 ? lo.z : lo.y, zhi = DIM == 3 ? hi.z : hi.y;  // marching axis
+    const int m0 = zlo + blockIdx.z * zb;
+    const int mend = min(m0 + zb, zhi + 1);  // exclusive
+    const int xb = x0 & ~1;                   // box start cell (ext index of data x0 - 1 is x0)
+    const int xoff = x0 - xb;
     const int xi = x0 + tx;
-    const int yb = y0 + ty * RT;       // first node row of this thread (3D)
-    const bool with_t = RESID && duo != nullptr;
+    const int yb = y0 + ty * RT;  // first node row of this thread (3D)
     bool ok[RT];
 #pragma unroll
-    for (int a = 0; a < RT; ++a) ok[a] = xi < N && (DIM == 2 || yb + a < N);
+    for (int a = 0; a < RT; ++a) ok[a] = xi <= hi.x && (DIM == 2 || yb + a <= hi.y);
 
-    constexpr int fm = DIM == 3 ? 4 : 2;  // marching-axis faces (z in 3D, y in 2D)
-    // can any node of this CTA lie on a Dirichlet face?  (block-uniform)
-    const bool edge_tile = x0 == 0 || x0 + TL::X >= N - 1 ||
-                           (DIM == 3 && (y0 == 0 || y0 + TL::ROWS >= N - 1));
-    const bool maybe_dir =
-        (edge_tile && (!bc.neu[0] || !bc.neu[1] || (DIM == 3 && (!bc.neu[2] || !bc.neu[3])))) ||
-        (m0 == 0 && !bc.neu[fm]) || (mend == N && !bc.neu[fm + 1]);
-
-    // per-row constants: output offset at plane 0, Dirichlet status of the
-    // column (x/y faces outrank the marching-axis faces, grid.cpp:53-62) and
-    // whether the node has mirror ghost cells in x/y
-    ptrdiff_t obase[RT];
-    bool dir_row[RT], mir_row[RT];
-    double val_row[RT];
+    // per-row output offsets at plane m = -1 (advanced by one plane per step)
+    // and whether the row's nodes have mirror ghost cells in x / y
+    ptrdiff_t opos = DIM == 3 ? eix<DIM>(L, xi, yb, -1) : (ptrdiff_t)(xi + 1);
+    const ptrdiff_t ostep = DIM == 3 ? (ptrdiff_t)L.plane : (ptrdiff_t)L.Px;
+    bool mir_row[RT];
 #pragma unroll
     for (int a = 0; a < RT; ++a) {
-        const int j = DIM == 3 ? yb + a : 0;
-        obase[a] = eix<DIM>(L, xi, j, -1);  // + (m + 1) * plane
-        if (DIM == 2) obase[a] = (ptrdiff_t)(xi + 1);
-        dir_row[a] = (xi == 0 && !bc.neu[0]) || (xi == N - 1 && !bc.neu[1]) ||
-                     (DIM == 3 && ((j == 0 && !bc.neu[2]) || (j == N - 1 && !bc.neu[3])));
-        val_row[a] = rc.homogeneous ? 0.0 : dirichlet_value<DIM>(bc, N, xi, j, 0);
+        const int j = yb + a;
         mir_row[a] = xi == 1 || xi == N - 2 || (DIM == 3 && (j == 1 || j == N - 2));
     }
-    const bool dir_lo = !bc.neu[fm], dir_hi = !bc.neu[fm + 1];
-    const double val_lo = rc.homogeneous ? 0.0 : bc.val[fm];
-    const double val_hi = rc.homogeneous ? 0.0 : bc.val[fm + 1];
 
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
@@ -134,58 +130,64 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     }
     __syncthreads();
 
+    const unsigned a_full = smem_u32(&R.full[0]), a_empty = smem_u32(&R.empty[0]);
+    const unsigned a_u = smem_u32(&R.u[0][0]), a_g = smem_u32(&R.g[0][0]);
+    const unsigned a_s = smem_u32(&R.s[0][0]), a_t = smem_u32(&R.t[0][0]);
     constexpr unsigned BU = TL::PLANE * 8, BG = TL::GBOX * 8;
-    // producer (thread 0): plane m -> slot; waits for the slot's previous use
+    // producer (one lane): plane m -> slot; waits for the slot's previous use
     auto issue = [&](int m) {
-        const int p = m - (m0 - 1);
-        const int s = p & (NST - 1), k = p / NST;
-        if (k > 0) mbar_wait(&R.empty[s], (k - 1) & 1);
+        const unsigned p = (unsigned)(m - m0 + 1);
+        const unsigned s = p & (NST - 1), k = p / NST;
+        if (k > 0) mbar_wait_u32(a_empty + 8 * s, (k - 1) & 1);
         const bool comp = m >= m0 && m < mend;
-        const unsigned bytes = BU + (SIG ? BU : 0u) + (comp ? BG + (with_t ? BG : 0u) : 0u);
-        mbar_expect_tx(&R.full[s], bytes);
+        const unsigned bytes = BU + (SIG ? BU : 0u) + (comp ? BG + (DUO && RESID ? BG : 0u) : 0u);
+        const unsigned bar = a_full + 8 * s;
+        mbar_expect_tx_u32(bar, bytes);
         if (DIM == 3) {
-            tma_load_3d(R.u[s], &tm_u, x0, y0, m + 1, &R.full[s]);
-            if (SIG) tma_load_3d(R.s[s], &tm_s, x0, y0, m + 1, &R.full[s]);
+            tma_load_3d_u32(a_u + s * (TL::PLANE_AL * 8), &tm_u, xb, y0, m + 1, bar);
+            if (SIG) tma_load_3d_u32(a_s + s * (TL::PLANE_AL * 8), &tm_s, xb, y0, m + 1, bar);
             if (comp) {
-                tma_load_3d(R.g[s], &tm_g, x0, y0 + 1, m + 1, &R.full[s]);
-                if (with_t) tma_load_3d(R.t[s], &tm_t, x0, y0 + 1, m + 1, &R.full[s]);
+                tma_load_3d_u32(a_g + s * (TL::GBOX_AL * 8), &tm_g, xb, y0 + 1, m + 1, bar);
+                if (DUO && RESID) tma_load_3d_u32(a_t + s * (TL::GBOX_AL * 8), &tm_t, xb, y0 + 1, m + 1, bar);
             }
         } else {
-            tma_load_2d(R.u[s], &tm_u, x0, m + 1, &R.full[s]);
-            if (SIG) tma_load_2d(R.s[s], &tm_s, x0, m + 1, &R.full[s]);
+            tma_load_2d_u32(a_u + s * (TL::PLANE_AL * 8), &tm_u, xb, m + 1, bar);
+            if (SIG) tma_load_2d_u32(a_s + s * (TL::PLANE_AL * 8), &tm_s, xb, m + 1, bar);
             if (comp) {
-                tma_load_2d(R.g[s], &tm_g, x0, m + 1, &R.full[s]);
-                if (with_t) tma_load_2d(R.t[s], &tm_t, x0, m + 1, &R.full[s]);
+                tma_load_2d_u32(a_g + s * (TL::GBOX_AL * 8), &tm_g, xb, m + 1, bar);
+                if (DUO && RESID) tma_load_2d_u32(a_t + s * (TL::GBOX_AL * 8), &tm_t, xb, m + 1, bar);
             }
         }
     };
-    auto slot_of = [&](int m) { return (m - (m0 - 1)) & (NST - 1); };
+    auto slot_of = [&](int m) { return (unsigned)(m - m0 + 1) & (NST - 1); };
     auto wait_plane = [&](int m) {
-        const int p = m - (m0 - 1);
-        mbar_wait(&R.full[p & (NST - 1)], (p / NST) & 1);
+        const unsigned p = (unsigned)(m - m0 + 1);
+        mbar_wait_u32(a_full + 8 * (p & (NST - 1)), (p / NST) & 1);
     };
     auto release = [&](int m) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&R.empty[slot_of(m)]);
+        if (lane == 0) mbar_arrive_u32(a_empty + 8 * slot_of(m));
     };
 
-    const int wbase = tx + TL::HX * (DIM == 3 ? ty * RT : 0);  // window origin in the u box
+    const int wbase = tx + xoff + TL::HXU * (DIM == 3 ? ty * RT : 0);  // window origin in the u box
+    const int gbase = tx + 1 + xoff + TL::HXG * (DIM == 3 ? ty * RT : 0);
     auto read_plane = [&](int m, Win<DIM>& P, SWin<DIM, SIG>& Ps) {
-        const int slot = slot_of(m);
+        const unsigned slot = slot_of(m);
 #pragma unroll
         for (int w = 0; w < WR; ++w)
 #pragma unroll
             for (int p = 0; p < 3; ++p) {
-                P[w][p] = R.u[slot][wbase + p + TL::HX * w];
-                if constexpr (SIG) Ps[w][p] = R.s[slot][wbase + p + TL::HX * w];
+                P[w][p] = R.u[slot][wbase + p + TL::HXU * w];
+                if constexpr (SIG) Ps[w][p] = R.s[slot][wbase + p + TL::HXU * w];
             }
     };
 
     double dmax = 0.0;
-    int bad = 0;
+    unsigned badhi = 0;  // max exponent field of the produced values
 
     // the RT nodes' terms of one stencil plane (offset dr), interleaved term
-    // by term so the independent accumulation chains overlap
+    // by term so the independent accumulation chains overlap; the first
+    // term starts the chain (0 + t differs from t only in the sign of zero)
     auto plane_terms = [&](double (&acc)[RT], double (&smax)[RT], const Win<DIM>& P,
                            const SWin<DIM, SIG>& Ps, const double (&uc)[RT], const double (&sc)[RT],
                            int dr) {
@@ -195,36 +197,31 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             for (int p = -1; p <= 1; ++p) {
                 if (dr == 0 && q == 0 && p == 0) continue;
                 const int l2 = dr * dr + q * q + p * p;
+                const bool first = dr == -1 && q == (DIM == 3 ? -1 : 0) && p == -1;
 #pragma unroll
                 for (int a = 0; a < RT; ++a) {
                     const int w = DIM == 3 ? a + q + 1 : 0;
                     double sbar = 1.0;
                     if constexpr (SIG) {
                         sbar = 0.5 * (Ps[w][p + 1] + sc[a]);
-                        smax[a] = smax[a] < sbar ? sbar : smax[a];
+                        smax[a] = first ? sbar : (smax[a] < sbar ? sbar : smax[a]);
                     }
-                    acc[a] = stencil_term<SIG>(acc[a], sbar, P[w][p + 1], uc[a], l2);
+                    const double t = stencil_t<SIG>(sbar, P[w][p + 1], uc[a], l2);
+                    acc[a] = first ? t : acc[a] + t;
                 }
             }
     };
 
-    // finish one node: op, diag / residual, Euler step, Dirichlet override, store
-    auto finish = [&](int m, int a, double acc, double smax, double uc, double gc, double tc) {
-        const ptrdiff_t pos = obase[a] + (ptrdiff_t)(m + 1) * L.plane;
-        bool dir = false;
-        double dval = 0.0;
-        if (maybe_dir) {
-            dir = dir_row[a] || (m == 0 && dir_lo) || (m == N - 1 && dir_hi);
-            dval = dir_row[a] ? val_row[a] : (m == 0 && dir_lo ? val_lo : val_hi);
-        }
+    // finish one node: op, diag / residual, Euler step, store
+    auto finish = [&](int m, int a, bool mir_m, double acc, double smax, double uc, double gc, double tc) {
+        const ptrdiff_t pos = opos + (DIM == 3 ? a * (ptrdiff_t)L.Px : 0);
         const double op = (acc * rc.pref) * rc.inv_s2;
         double value;
         if constexpr (RESID) {
             value = gc - (HAS_A ? op + rc.a * uc : op);
-            if (dir) value = 0.0;
             const double ar = fabs(value);
             dmax = dmax < ar ? ar : dmax;
-            if (with_t) duo[pos] = tc + uc;
+            if (DUO) duo[pos] = tc + uc;
         } else {
             const double omg = op - gc;
             const double diag = HAS_A ? fabs((op + rc.a * uc) - gc) : fabs(omg);
@@ -240,46 +237,44 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                 const double num = uc + rc.dtau1 * omg;
                 value = HAS_A ? num / rc.denom1 : num;
             }
-            if (dir) {
-                value = dval;
-            } else {
-                dmax = dmax < diag ? diag : dmax;
-            }
-            bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
-            if (duo) duo[pos] = value - uc;
+            dmax = dmax < diag ? diag : dmax;
+            badhi = max(badhi, (unsigned)__double2hiint(value) & 0x7ff00000u);
+            if (DUO) duo[pos] = value - uc;
         }
         uo[pos] = value;
-        if (mir_row[a] || m == 1 || m == N - 2)
+        if (mir_row[a] || mir_m)
             store_mirrors<DIM>(uo, L, xi, DIM == 3 ? yb + a : m, DIM == 3 ? m : 0, value);
     };
 
     Win<DIM> X, Y, Z;  // window planes, rotating roles
     SWin<DIM, SIG> Xs, Ys, Zs;
 
-    if (m0 < N) {
-        int next = m0 - 1;  // next plane the producer issues
+    if (m0 < mend) {
         if (tid == 0)
-            for (; next <= mend && next <= m0 + NST - 2; ++next) issue(next);
+            for (int q = m0 - 1; q <= mend && q <= m0 + NST - 2; ++q) issue(q);
         wait_plane(m0 - 1);
         read_plane(m0 - 1, X, Xs);
         wait_plane(m0);
         read_plane(m0, Y, Ys);
         release(m0 - 1);
+        opos += (ptrdiff_t)m0 * ostep;
 
         // one plane: P0 = m-1, P1 = m (held), P2 <- m+1
         auto step = [&](int m, Win<DIM>& P0, Win<DIM>& P1, Win<DIM>& P2, SWin<DIM, SIG>& S0,
                         SWin<DIM, SIG>& S1, SWin<DIM, SIG>& S2) {
-            if (tid == 0)
-                for (; next <= mend && next <= m + NST - 2; ++next) issue(next);
+            opos += ostep;
+            // rotating producer: plane m + NST - 2 (the prologue issued up to m0 + NST - 2)
+            if (warp == ((m - m0) & (TL::NWARPS - 1)) && lane == 0 && m > m0 && m + NST - 2 <= mend)
+                issue(m + NST - 2);
             wait_plane(m + 1);
             read_plane(m + 1, P2, S2);
-            const int sm = slot_of(m);
+            const unsigned sm = slot_of(m);
             double uc[RT], sc[RT], acc[RT], smax[RT], gc[RT], tc[RT];
 #pragma unroll
             for (int a = 0; a < RT; ++a) {
-                const int gi = tx + 1 + TL::HX * (DIM == 3 ? ty * RT + a : 0);  // node in the g box
+                const int gi = gbase + TL::HXG * a;  // node in the g box
                 gc[a] = R.g[sm][gi];
-                tc[a] = with_t ? R.t[sm][gi] : 0.0;
+                tc[a] = (DUO && RESID) ? R.t[sm][gi] : 0.0;
                 uc[a] = P1[DIM == 3 ? a + 1 : 0][1];
                 sc[a] = 1.0;
                 if constexpr (SIG) sc[a] = S1[DIM == 3 ? a + 1 : 0][1];
@@ -289,9 +284,10 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             plane_terms(acc, smax, P0, S0, uc, sc, -1);
             plane_terms(acc, smax, P1, S1, uc, sc, 0);
             plane_terms(acc, smax, P2, S2, uc, sc, 1);
+            const bool mir_m = m == 1 || m == N - 2;
 #pragma unroll
             for (int a = 0; a < RT; ++a)
-                if (ok[a]) finish(m, a, acc[a], smax[a], uc[a], gc[a], tc[a]);
+                if (ok[a]) finish(m, a, mir_m, acc[a], smax[a], uc[a], gc[a], tc[a]);
             release(m);
         };
         // roles rotate (P0, P1, P2) -> (P1, P2, P0) each plane: period 3
@@ -304,56 +300,63 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             step(m + 2, Z, X, Y, Zs, Xs, Ys);
         }
     }
-    if (RESID) {
-        if (diag_slot) block_max_commit(dmax, diag_slot);
-    } else {
-        block_max_commit(dmax, diag_slot);
-        block_or_commit(bad, flag);
-    }
+    block_max_commit(dmax, diag_slot);
+    if (!RESID) block_or_commit(badhi == 0x7ff00000u, flag);
 }
 
-template <int DIM, bool SIG, bool HAS_A, int MODE>
+template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO>
 void launch_t(dim3 grid, dim3 block, cudaStream_t s, const TmaSet& tm, double* uo, double* duo,
-              const ExtLay& L, int zb, const RelaxConst& rc, const BcDev& bc,
+              const ExtLay& L, int3 lo, int3 hi, int zb, const RelaxConst& rc,
               unsigned long long* slot, int* flag) {
     const int bytes = (int)sizeof(TRing<DIM, SIG, MODE>);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_relax_tma<DIM, SIG, HAS_A, MODE>,
+        cudaFuncSetAttribute(k_relax_tma<DIM, SIG, HAS_A, MODE, DUO>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         configured = true;
     }
-    k_relax_tma<DIM, SIG, HAS_A, MODE><<<grid, block, bytes, s>>>(tm.u, tm.g, tm.s, tm.t, uo, duo, L, zb,
-                                                                  rc, bc, slot, flag);
+    k_relax_tma<DIM, SIG, HAS_A, MODE, DUO><<<grid, block, bytes, s>>>(tm.u, tm.g, tm.s, tm.t, uo, duo, L, lo,
+                                                                       hi, zb, rc, slot, flag);
 }
 
-template <int DIM, int MODE>
-void launch_dim(dim3 grid, dim3 block, bool sig, cudaStream_t s, const TmaSet& tm, double* uo,
-                double* duo, const ExtLay& L, int zb, const RelaxConst& rc, const BcDev& bc,
+template <int DIM, int MODE, bool DUO>
+void launch_duo(dim3 grid, dim3 block, bool sig, cudaStream_t s, const TmaSet& tm, double* uo,
+                double* duo, const ExtLay& L, int3 lo, int3 hi, int zb, const RelaxConst& rc,
                 unsigned long long* slot, int* flag) {
     if (sig) {
-        if (rc.has_a) launch_t<DIM, true, true, MODE>(grid, block, s, tm, uo, duo, L, zb, rc, bc, slot, flag);
-        else launch_t<DIM, true, false, MODE>(grid, block, s, tm, uo, duo, L, zb, rc, bc, slot, flag);
+        if (rc.has_a) launch_t<DIM, true, true, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
+        else launch_t<DIM, true, false, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
     } else {
-        if (rc.has_a) launch_t<DIM, false, true, MODE>(grid, block, s, tm, uo, duo, L, zb, rc, bc, slot, flag);
-        else launch_t<DIM, false, false, MODE>(grid, block, s, tm, uo, duo, L, zb, rc, bc, slot, flag);
+        if (rc.has_a) launch_t<DIM, false, true, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
+        else launch_t<DIM, false, false, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
     }
 }
 
 template <int MODE>
 void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, const ExtLay& L,
-                 const RelaxConst& rc, const BcDev& bc, unsigned long long* slot, int* flag,
+                 const NodeRange& rg, const RelaxConst& rc, unsigned long long* slot, int* flag,
                  cudaStream_t s) {
-    const int Nc = L.N;
-    const int zb = relax_tiled_zb(dim, Nc);
+    const int3 lo = make_int3(rg.lo[0], rg.lo[1], rg.lo[2]);
+    const int3 hi = make_int3(rg.hi[0], rg.hi[1], rg.hi[2]);
+    const int nx = rg.hi[0] - rg.lo[0] + 1, ny = rg.hi[1] - rg.lo[1] + 1, nz = rg.hi[2] - rg.lo[2] + 1;
+    if (nx <= 0 || ny <= 0 || (dim == 3 && nz <= 0)) return;  // nothing off the Dirichlet faces
+    const int zb = relax_tiled_zb(dim, L.N);
+    dim3 grid, block;
     if (dim == 3) {
         using TL = Tile<3>;
-        const dim3 grid((Nc + TL::X - 1) / TL::X, (Nc + TL::ROWS - 1) / TL::ROWS, (Nc + zb - 1) / zb);
-        launch_dim<3, MODE>(grid, dim3(TL::X, TL::TY), sig, s, tm, uo, duo, L, zb, rc, bc, slot, flag);
+        grid = dim3((nx + TL::X - 1) / TL::X, (ny + TL::ROWS - 1) / TL::ROWS, (nz + zb - 1) / zb);
+        block = dim3(TL::X, TL::TY);
     } else {
         using TL = Tile<2>;
-        const dim3 grid((Nc + TL::X - 1) / TL::X, 1, (Nc + zb - 1) / zb);
-        launch_dim<2, MODE>(grid, dim3(TL::X, 1), sig, s, tm, uo, duo, L, zb, rc, bc, slot, flag);
+        grid = dim3((nx + TL::X - 1) / TL::X, 1, (ny + zb - 1) / zb);
+        block = dim3(TL::X, 1);
+    }
+    if (dim == 3) {
+        if (duo) launch_duo<3, MODE, true>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
+        else launch_duo<3, MODE, false>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
+    } else {
+        if (duo) launch_duo<2, MODE, true>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
+        else launch_duo<2, MODE, false>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
     }
 }
 
@@ -366,24 +369,24 @@ int relax_tiled_zb(int dim, int N) {
 
 void tile_boxes(int dim, unsigned* box_u, unsigned* box_g) {
     if (dim == 3) {
-        box_u[0] = Tile<3>::HX; box_u[1] = Tile<3>::HY;   box_u[2] = 1;
-        box_g[0] = Tile<3>::HX; box_g[1] = Tile<3>::ROWS; box_g[2] = 1;
+        box_u[0] = Tile<3>::HXU; box_u[1] = Tile<3>::HY;   box_u[2] = 1;
+        box_g[0] = Tile<3>::HXG; box_g[1] = Tile<3>::ROWS; box_g[2] = 1;
     } else {
-        box_u[0] = Tile<2>::HX; box_u[1] = 1; box_u[2] = 1;
-        box_g[0] = Tile<2>::HX; box_g[1] = 1; box_g[2] = 1;
+        box_u[0] = Tile<2>::HXU; box_u[1] = 1; box_u[2] = 1;
+        box_g[0] = Tile<2>::HXG; box_g[1] = 1; box_g[2] = 1;
     }
 }
 
 void launch_relax_tma(int dim, bool sig, const TmaSet& tm, double* uo, double* duo,
-                      const ExtLay& L, const RelaxConst& rc, const BcDev& bc,
+                      const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
                       unsigned long long* slot, int* flag, cudaStream_t s) {
-    launch_mode<MODE_RELAX>(dim, sig, tm, uo, duo, L, rc, bc, slot, flag, s);
+    launch_mode<MODE_RELAX>(dim, sig, tm, uo, duo, L, rg, rc, slot, flag, s);
 }
 
 void launch_residual_tma(int dim, bool sig, const TmaSet& tm, double* r, double* utot,
-                         const ExtLay& L, const RelaxConst& rc, const BcDev& bc,
+                         const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
                          unsigned long long* rmax_slot, cudaStream_t s) {
-    launch_mode<MODE_RESID>(dim, sig, tm, r, utot, L, rc, bc, rmax_slot, nullptr, s);
+    launch_mode<MODE_RESID>(dim, sig, tm, r, utot, L, rg, rc, rmax_slot, nullptr, s);
 }
 
 }  // namespace sgmlb

@@ -1,0 +1,18 @@
+"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel."""
+import collections
+import csv
+import sys
+
+rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10 and r[0] != "ID"]
+tot = collections.defaultdict(float)
+cnt = collections.Counter()
+for r in rows:
+    name = r[4].split("(")[0].replace("unnamed>::", "").replace("void ", "")
+    key = name + " " + r[8] if "k_relax_tma" in name and r[8].startswith("(17, 33, 9)") else name
+    tot[key] += float(r[-1]) * 1e-6
+    cnt[key] += 1
+all_ms = sum(tot.values())
+print(f"{len(rows)} launches, {all_ms:.1f} ms total (serialised, cold-cache ncu timings)")
+print(f"{'kernel':60s} {'launches':>8s} {'ms':>10s} {'share':>7s} {'ms/launch':>10s}")
+for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+    print(f"{k:60s} {cnt[k]:8d} {v:10.2f} {100 * v / all_ms:6.1f}% {v / cnt[k]:10.4f}")
