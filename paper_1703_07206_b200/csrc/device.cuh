@@ -373,12 +373,14 @@ __device__ __forceinline__ void mbar_expect_tx_u32(unsigned bar, unsigned bytes)
 __device__ __forceinline__ void mbar_arrive_u32(unsigned bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
 }
+// try_wait with a suspend-time hint: the thread sleeps in the instruction
+// until the phase completes (or the hint expires) instead of spinning
 __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n"
         "@!P1 bra WAIT_%=;\n"
         "}\n" ::"r"(bar),
         "r"(parity)

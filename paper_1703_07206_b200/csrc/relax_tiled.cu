@@ -19,7 +19,7 @@
 // boxes must start 16-byte aligned in x, so boxes start at the even cell at
 // or below the halo and the window carries an offset xoff in {0, 1}.  The
 // producer role rotates over the warps (warp (m - m0) % NWARPS issues plane
-// m + NST - 2 in step m), so every warp runs the same instruction stream;
+// m + LEAD in step m), so every warp runs the same instruction stream;
 // consumers wait on `full`, each warp releases a slot on `empty`.
 //
 // In 3D every thread computes RT = 2 adjacent rows (y, y+1) of the plane: it
@@ -56,6 +56,7 @@ struct Tile {
     static constexpr int NWARPS = THREADS / 32;
     static constexpr int WR = DIM == 3 ? RT + 2 : 1;   // window rows per plane
     static constexpr int NST = 8;                      // ring depth (planes), power of two
+    static constexpr int LEAD = NST - 3;               // step m issues plane m + LEAD
     static constexpr int PLANE_AL = (PLANE + 15) / 16 * 16;  // slots 128-byte aligned
     static constexpr int GBOX_AL = (GBOX + 15) / 16 * 16;
 };
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
 
     if (m0 < mend) {
         if (tid == 0)
-            for (int q = m0 - 1; q <= mend && q <= m0 + NST - 2; ++q) issue(q);
+            for (int q = m0 - 1; q <= mend && q <= m0 + TL::LEAD; ++q) issue(q);
         wait_plane(m0 - 1);
         read_plane(m0 - 1, X, Xs);
         wait_plane(m0);
@@ -263,9 +264,10 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
         auto step = [&](int m, Win<DIM>& P0, Win<DIM>& P1, Win<DIM>& P2, SWin<DIM, SIG>& S0,
                         SWin<DIM, SIG>& S1, SWin<DIM, SIG>& S2) {
             opos += ostep;
-            // rotating producer: plane m + NST - 2 (the prologue issued up to m0 + NST - 2)
-            if (warp == ((m - m0) & (TL::NWARPS - 1)) && lane == 0 && m > m0 && m + NST - 2 <= mend)
-                issue(m + NST - 2);
+            // rotating producer: plane m + LEAD (the prologue issued up to m0 + LEAD);
+            // its slot held plane m + LEAD - NST, released after step m + LEAD - NST + 1
+            if (warp == ((m - m0) & (TL::NWARPS - 1)) && lane == 0 && m > m0 && m + TL::LEAD <= mend)
+                issue(m + TL::LEAD);
             wait_plane(m + 1);
             read_plane(m + 1, P2, S2);
             const unsigned sm = slot_of(m);
@@ -340,7 +342,9 @@ void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, c
     const int3 hi = make_int3(rg.hi[0], rg.hi[1], rg.hi[2]);
     const int nx = rg.hi[0] - rg.lo[0] + 1, ny = rg.hi[1] - rg.lo[1] + 1, nz = rg.hi[2] - rg.lo[2] + 1;
     if (nx <= 0 || ny <= 0 || (dim == 3 && nz <= 0)) return;  // nothing off the Dirichlet faces
-    const int zb = relax_tiled_zb(dim, L.N);
+    const int cols = dim == 3 ? ((nx + Tile<3>::X - 1) / Tile<3>::X) * ((ny + Tile<3>::ROWS - 1) / Tile<3>::ROWS)
+                              : (nx + Tile<2>::X - 1) / Tile<2>::X;
+    const int zb = relax_tiled_zb(dim, cols, dim == 3 ? nz : ny);
     dim3 grid, block;
     if (dim == 3) {
         using TL = Tile<3>;
@@ -362,9 +366,13 @@ void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, c
 
 }  // namespace
 
-int relax_tiled_zb(int dim, int N) {
-    if (dim == 2) return N >= 1024 ? 128 : 32;
-    return N >= 512 ? 64 : (N >= 128 ? 32 : 16);
+// planes per CTA: long marches amortise the 2-plane prologue, short ones
+// give small levels enough CTAs (about two waves of 148 SMs x 2)
+int relax_tiled_zb(int dim, int cols, int nz) {
+    const int target = 2 * 148 * (dim == 3 ? 2 : 4);
+    int zb = dim == 3 ? 64 : 128;
+    while (zb > 4 && (long long)cols * ((nz + zb - 1) / zb) < target) zb >>= 1;
+    return zb;
 }
 
 void tile_boxes(int dim, unsigned* box_u, unsigned* box_g) {
