@@ -267,6 +267,11 @@ __device__ __forceinline__ void block_max_commit(double v, unsigned long long* s
     }
 }
 
+// warp-level variant: no block barrier (finished warps leave immediately)
+__device__ __forceinline__ void warp_or_commit(int bad, int* flag) {
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 __device__ __forceinline__ void block_or_commit(int bad, int* flag) {
     if (__syncthreads_or(bad)) {
         if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) atomicOr(flag, 1);

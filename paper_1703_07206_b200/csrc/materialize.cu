@@ -109,21 +109,30 @@ __global__ void __launch_bounds__(MBX* MBY)
             // `st` is a literal at both call sites: the straddle selects vanish
             // from the common (same-cell) path
             auto accumulate = [&](bool st) {
+                // all corner loads first (one latency per entry), then the
+                // products in the reference's order
+                double cv[2][2][2][3];
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const bool live = r < nr && q < nq;
+                        const double* row =
+                            ce.du + eix<DIM>(ce.L, X0, (y >> l) + (live ? q : 0),
+                                             DIM == 3 ? (z >> l) + (live ? r : 0) : 0);
+#pragma unroll
+                        for (int cp = 0; cp < 2; ++cp) {
+                            const double* rw = row + cp * dsp;
+                            cv[r][q][cp][0] = live ? __ldg(rw) : 0.0;
+                            cv[r][q][cp][1] = (live && X0 + 1 < Nl) ? __ldg(rw + 1) : 0.0;
+                            cv[r][q][cp][2] = (st && live && X0 + 2 < Nl) ? __ldg(rw + 2) : 0.0;
+                        }
+                    }
 #pragma unroll
                 for (int r = 0; r < 2; ++r)
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         if (r < nr && q < nq) {
-                            const double* row =
-                                ce.du + eix<DIM>(ce.L, X0, (y >> l) + q, DIM == 3 ? (z >> l) + r : 0);
-                            double c0[2], c1[2], c2[2];
-#pragma unroll
-                            for (int cp = 0; cp < 2; ++cp) {
-                                const double* rw = row + cp * dsp;
-                                c0[cp] = __ldg(rw);
-                                c1[cp] = X0 + 1 < Nl ? __ldg(rw + 1) : 0.0;
-                                c2[cp] = (st && X0 + 2 < Nl) ? __ldg(rw + 2) : 0.0;
-                            }
                             const double wzy = DIM == 3 ? wz[r] * wy[q] : wy[q];
                             // reference order per node: corner p = 0 then p = 1 of this
                             // (r, q); a zero-weight p = 1 term adds +-0 (as the reference)
@@ -132,8 +141,8 @@ __global__ void __launch_bounds__(MBX* MBY)
                                 const double w0 = wzy * wx0[k], w1 = wzy * fx[k];
 #pragma unroll
                                 for (int cp = 0; cp < 2; ++cp) {
-                                    const double ca = (st && jk[k]) ? c1[cp] : c0[cp];
-                                    const double cb = (st && jk[k]) ? c2[cp] : c1[cp];
+                                    const double ca = (st && jk[k]) ? cv[r][q][cp][1] : cv[r][q][cp][0];
+                                    const double cb = (st && jk[k]) ? cv[r][q][cp][2] : cv[r][q][cp][1];
                                     const double t0 = w0 * ca;
                                     acc[cp][k] = (r == 0 && q == 0) ? t0 : acc[cp][k] + t0;
                                     acc[cp][k] = acc[cp][k] + w1 * cb;
@@ -170,7 +179,7 @@ __global__ void __launch_bounds__(MBX* MBY)
             }
         }
     }
-    block_or_commit(bad, flag);
+    warp_or_commit(bad, flag);
 }
 
 // ---------------------------------------------------------------------------
