@@ -352,6 +352,8 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
             for (int v = v1; v >= 1; --v)
                 for (int k = 0; k + 1 < cc; ++k) entries.push_back(ChainEntry{DU[v][k], Lv[v], v, 0});
         }
+        for (int v = 1; v < n; ++v)
+            for (double* d : DU[v]) du_bufs.push_back(d);
         if (!entries.empty()) {
             SGML_CUDA(cudaMalloc((void**)&d_chain, entries.size() * sizeof(ChainEntry)));
             SGML_CUDA(cudaMemcpy(d_chain, entries.data(), entries.size() * sizeof(ChainEntry),
@@ -408,7 +410,12 @@ int sgml_solver::faces_of(const double* p) const {
 void sgml_solver::set_faces(double* p, int level, int st) {
     if (all_neumann || faces_of(p) == st) return;
     if (st == FS_OTHER) fail(SGML_ELOGIC, "set_faces: no target content");
-    launch(SGML_CLASS_OTHER, [&] { launch_dirichlet_faces(g.dim, p, Lv[level], bc, st == FS_ZERO, ctx->stream); });
+    // DU arrays: data nodes only (their ghost cells stay 0, the past-the-end
+    // corner reads of the interpolation)
+    const bool mirrors = std::find(du_bufs.begin(), du_bufs.end(), p) == du_bufs.end();
+    launch(SGML_CLASS_OTHER, [&] {
+        launch_dirichlet_faces(g.dim, p, Lv[level], bc, st == FS_ZERO, mirrors, ctx->stream);
+    });
     fstate[p] = st;
 }
 

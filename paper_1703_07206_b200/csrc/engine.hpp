@@ -97,6 +97,7 @@ struct sgml_solver {
     std::vector<std::vector<double*>> DU;     // DU[v][k]
     sgmlb::ChainEntry* d_chain = nullptr;     // per-tooth pending-increment lists
     std::vector<int> tooth_off;               // offset of tooth v1's list in d_chain
+    std::vector<const double*> du_bufs;       // DU arrays (faces without mirror ghosts)
     // TMA descriptors per buffer: window box (tile + halo) and tile box
     std::vector<std::pair<const double*, CUtensorMap>> map_u, map_g;
     const CUtensorMap& umap(const double* p) const;

@@ -82,9 +82,10 @@ void launch_residual_tma(int dim, bool sig, const TmaSet& tm, double* r, double*
                          const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
                          unsigned long long* rmax_slot, cudaStream_t s);
 // Dirichlet-face nodes of an extended level array <- 0 (zero) or their face
-// value (the reference's lowest-face-id rule).
+// value (the reference's lowest-face-id rule), with their mirror ghost cells
+// unless `mirrors` is false (DU arrays keep all-zero ghosts).
 void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc, bool zero,
-                            cudaStream_t s);
+                            bool mirrors, cudaStream_t s);
 // Materialise the level-w input of the next relax step from the tooth's
 // state: Dirichlet value, the finest relaxed level lf = w + frel (ufine) at
 // its subset nodes, or base + the pending increments chain[0..nchain).

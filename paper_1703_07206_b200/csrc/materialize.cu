@@ -123,9 +123,10 @@ __global__ void __launch_bounds__(MBX* MBY)
 #pragma unroll
                         for (int cp = 0; cp < 2; ++cp) {
                             const double* rw = row + cp * dsp;
+                            // past the x end: the DU arrays' ghost cells, never written (0)
                             cv[r][q][cp][0] = live ? __ldg(rw) : 0.0;
-                            cv[r][q][cp][1] = (live && X0 + 1 < Nl) ? __ldg(rw + 1) : 0.0;
-                            cv[r][q][cp][2] = (st && live && X0 + 2 < Nl) ? __ldg(rw + 2) : 0.0;
+                            cv[r][q][cp][1] = live ? __ldg(rw + 1) : 0.0;
+                            cv[r][q][cp][2] = (st && live) ? __ldg(rw + 2) : 0.0;
                         }
                     }
 #pragma unroll
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(128) k_gather_ext(const double* __restrict__ e
 // One thread per (face, a, b); nodes on edges are written by several faces
 // with the same value (the lowest-face-id rule of dirichlet_value).
 template <int DIM>
-__global__ void __launch_bounds__(128) k_dirichlet_faces(double* a, ExtLay L, BcDev bc, int zero) {
+__global__ void __launch_bounds__(128) k_dirichlet_faces(double* a, ExtLay L, BcDev bc, int zero, int mirrors) {
     const int N = L.N;
     const int p = blockIdx.x * 32 + threadIdx.x, q = blockIdx.y * 4 + threadIdx.y, f = blockIdx.z;
     if (p >= N || (DIM == 3 && q >= N) || (DIM == 2 && q > 0) || bc.neu[f]) return;
@@ -248,7 +249,9 @@ __global__ void __launch_bounds__(128) k_dirichlet_faces(double* a, ExtLay L, Bc
     else if (f < 4) { i = p; j = side; k = q; }
     else { i = p; j = q; k = side; }
     if (DIM == 2 && f < 2) { j = p; k = 0; }
-    store_ext<DIM>(a, L, i, j, k, zero ? 0.0 : dirichlet_value<DIM>(bc, N, i, j, k));
+    const double v = zero ? 0.0 : dirichlet_value<DIM>(bc, N, i, j, k);
+    if (mirrors) store_ext<DIM>(a, L, i, j, k, v);
+    else a[eix<DIM>(L, i, j, k)] = v;
 }
 
 inline dim3 ext_grid(int dim, int N) { return dim3((N + 31) / 32, (N + 3) / 4, dim == 3 ? N : 1); }
@@ -301,12 +304,12 @@ void launch_gather_ext(int dim, const double* ext, const ExtLay& L, double* dens
 }
 
 void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc, bool zero,
-                            cudaStream_t s) {
+                            bool mirrors, cudaStream_t s) {
     const int N = L.N;
     if (dim == 2)
-        k_dirichlet_faces<2><<<dim3((N + 31) / 32, 1, 4), dim3(32, 4), 0, s>>>(a, L, bc, zero ? 1 : 0);
+        k_dirichlet_faces<2><<<dim3((N + 31) / 32, 1, 4), dim3(32, 4), 0, s>>>(a, L, bc, zero ? 1 : 0, mirrors ? 1 : 0);
     else
-        k_dirichlet_faces<3><<<dim3((N + 31) / 32, (N + 3) / 4, 6), dim3(32, 4), 0, s>>>(a, L, bc, zero ? 1 : 0);
+        k_dirichlet_faces<3><<<dim3((N + 31) / 32, (N + 3) / 4, 6), dim3(32, 4), 0, s>>>(a, L, bc, zero ? 1 : 0, mirrors ? 1 : 0);
 }
 
 }  // namespace sgmlb
