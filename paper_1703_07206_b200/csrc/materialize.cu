@@ -91,9 +91,10 @@ __global__ void __launch_bounds__(MBX* MBY)
             const double wz[2] = {1.0 - fz, fz};
             const int nq = iy ? 2 : 1, nr = (DIM == 3 && iz) ? 2 : 1;  // warp-uniform
             const int X0 = (X4 << w) >> l;
-            // distance of the second copy's corners; 0 when it is a dummy
-            const ptrdiff_t dsp =
-                ncopy == 2 ? (ptrdiff_t)((Nl - 1) >> 1) * (DIM == 3 ? ce.L.plane : (long long)ce.L.Px) : 0;
+            // strides: q row, r plane, second copy (0 when it is a dummy)
+            const ptrdiff_t sq = ce.L.Px, sr = DIM == 3 ? ce.L.plane : 0;
+            const ptrdiff_t dsp = ncopy == 2 ? (ptrdiff_t)((Nl - 1) >> 1) * (DIM == 3 ? sr : sq) : 0;
+            const double* p00 = ce.du + eix<DIM>(ce.L, X0, y >> l, DIM == 3 ? z >> l : 0);
             // the run of MV nodes straddles two cells only on level w + 1
             const bool straddle = l == w + 1;
             double fx[MV], wx0[MV];
@@ -112,21 +113,20 @@ __global__ void __launch_bounds__(MBX* MBY)
                 // all corner loads first (one latency per entry), then the
                 // products in the reference's order
                 double cv[2][2][2][3];
+                // every corner row exists in memory (rows / planes up to Nl are
+                // ghost cells), so all loads are unconditional; dead rows
+                // (zero weight) are loaded but not used
 #pragma unroll
-                for (int r = 0; r < 2; ++r)
+                for (int r = 0; r < (DIM == 3 ? 2 : 1); ++r)
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
-                        const bool live = r < nr && q < nq;
-                        const double* row =
-                            ce.du + eix<DIM>(ce.L, X0, (y >> l) + (live ? q : 0),
-                                             DIM == 3 ? (z >> l) + (live ? r : 0) : 0);
 #pragma unroll
                         for (int cp = 0; cp < 2; ++cp) {
-                            const double* rw = row + cp * dsp;
+                            const double* rw = p00 + (r * sr + q * sq + cp * dsp);
                             // past the x end: the DU arrays' ghost cells, never written (0)
-                            cv[r][q][cp][0] = live ? __ldg(rw) : 0.0;
-                            cv[r][q][cp][1] = live ? __ldg(rw + 1) : 0.0;
-                            cv[r][q][cp][2] = (st && live) ? __ldg(rw + 2) : 0.0;
+                            cv[r][q][cp][0] = __ldg(rw);
+                            cv[r][q][cp][1] = __ldg(rw + 1);
+                            cv[r][q][cp][2] = st ? __ldg(rw + 2) : 0.0;
                         }
                     }
 #pragma unroll
