@@ -13,8 +13,10 @@ cycles * U(n, n_r) * N^3 / time (cycle.cpp:191-192, sgml_main.cpp:218-219).
   e2e    the drop-in call sgml_solve() with pinned host buffers: f H2D, the
          solve, u D2H inside the timed region.
   roofline  the level-0 relaxation pass (the dominant kernel), algorithmic
-         bytes 24 B/node (read u_prev and g, write u) / its mean launch time
-         from CUDA events recorded around each launch inside the timed region.
+         bytes 24 B per relaxed node (read u_prev and g, write u; (N-2)^3
+         nodes off the Dirichlet faces) / its mean launch time from CUDA
+         events recorded around each launch inside the timed region;
+         roofline_fp64 the same launches against the fp64 issue roof.
   cpu_baseline  the reference core itself (oracle/_ref, compiled from
          /root/reference) on the host's cores, one single_cycle of
          poisson3d_problem(7) (129^3) per sample.
@@ -283,10 +285,18 @@ def run_ours(args, dist):
     for k, name in enumerate(_capi.CLASS_NAMES[:7]):
         cls[name] = {"ms_per_solve": rb.class_ms[k], "launches_per_solve": int(rb.class_launches[k])}
     relax0_ms = rb.class_ms[0] / max(1, rb.class_launches[0])
-    bytes_per_launch = 24.0 * T
+    # the pass covers the nodes off the Dirichlet faces ((N-2)^3 here); the
+    # face nodes keep their value and are not touched
+    relaxed = float((grid.N - 2) ** 3)
+    bytes_per_launch = 24.0 * relaxed
     peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = bytes_per_launch / (relax0_ms / 1e3) / 1e9
+    # the same launches against the fp64 issue roof: 76 fp64 operations per
+    # relaxed node (26 differences, 20 weight products, 25 chain adds,
+    # op / Euler step 5); 62 DADD/clk/SM measured x 148 SMs x 1.965 GHz
+    fp64_ops = 76.0 * relaxed
+    fp64_peak = 62.0 * 148 * 1.965e9
     traffic = None
     if os.path.exists(TRAFFIC_PATH):
         traffic = json.load(open(TRAFFIC_PATH)).get("relax0_bytes_per_launch", {}).get(str(n))
@@ -351,9 +361,13 @@ def run_ours(args, dist):
         "converged": last.converged,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "relax0 (k_relax_tma<3,0,0,0>, level-0 relaxation pass)",
+                     "kernel": "relax0 (k_relax_tma<3,0,0,0,0>, level-0 relaxation pass)",
                      "bytes_per_launch": bytes_per_launch, "mean_launch_ms": relax0_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+        "roofline_fp64": {"achieved": fp64_ops / (relax0_ms / 1e3), "peak": fp64_peak,
+                          "unit": "fp64 ops/s", "frac": fp64_ops / (relax0_ms / 1e3) / fp64_peak,
+                          "ops_per_node": 76,
+                          "peak_source": "scripts/micro/dp_latency.cu: 62 DADD/clk/SM at 1965 MHz"},
         "kernels": cls,
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -325,6 +325,8 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
             if (bc_host.kind[f] == 0) {
                 bval_zero = bval_zero && bc_host.value[f] == 0.0;
                 bval_finite = bval_finite && std::isfinite(bc_host.value[f]);
+                const double av = std::fabs(bc_host.value[f]);
+                bval_tiny = bval_tiny || (av != 0.0 && av < 0x1p-969);
             }
         const uint64_t E0 = ext_size(dim, Lv[0]);
         r = alloc(E0);
@@ -529,7 +531,7 @@ void sgml_solver::residual(const double* e) {
         tm.g = gmap(r);
         tm.s = has_sigma ? umap(S[0]) : tm.u;
         tm.t = gmap(utot);
-        launch(SGML_CLASS_RESIDUAL, [&] { launch_residual_tma(dim, has_sigma, tm, r, utot, Lv[0], rng[0], rc0, d_rmax, s); });
+        launch(SGML_CLASS_RESIDUAL, [&] { launch_residual_tma(dim, has_sigma, tm, r, utot, Lv[0], rng[0], rc0, d_rmax, d_flag, s); });
     } else {
         const double inv_h2 = 1.0 / (g.h * g.h);
         const double pref = dim == 2 ? 0.5 : 3.0 / 13.0;
@@ -568,6 +570,11 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
     // a non-finite Dirichlet value makes the first pass throw
     // (kernels.cpp:228, 343-346); the kernels never write face nodes
     if (!homogeneous && !bval_finite) SGML_CUDA(cudaMemsetAsync(flag, 1, 1, s));
+    // flag[1]: some level array of this cycle holds a nonzero value below
+    // 2^-969 (relax passes then keep the unfused edge terms); every level
+    // array of a cycle is produced within it, Dirichlet values included
+    SGML_CUDA(cudaMemsetAsync(flag + 1, 0, sizeof(int), s));
+    if (!homogeneous && bval_tiny) SGML_CUDA(cudaMemsetAsync(flag + 1, 1, 1, s));
     // restriction pyramid of the cycle's source (once per cycle, F4)
     for (int m = 0; m + 1 < n; ++m)
         launch(SGML_CLASS_PYRAMID, [&] {

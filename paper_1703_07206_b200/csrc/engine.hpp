@@ -186,6 +186,7 @@ struct sgml_solver {
     std::vector<sgmlb::NodeRange> rng;
     bool bval_zero = true;     // every Dirichlet face value is 0
     bool bval_finite = true;
+    bool bval_tiny = false;    // a Dirichlet value in (0, 2^-969)
     std::unordered_map<const double*, int> fstate;
     int face_want(bool homogeneous) const { return (homogeneous || bval_zero) ? FS_ZERO : FS_BVAL; }
     int faces_of(const double* p) const;

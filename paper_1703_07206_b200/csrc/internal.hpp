@@ -71,16 +71,19 @@ struct NodeRange {
 };
 // One relaxation pass over a level array (every node a subset node):
 // uo (with mirror ghosts), duo = uo - ui (nullable, DU arrays), diag max
-// into diag_slot, non-finite flag.
+// into diag_slot.  flag[0] <- 1 on a non-finite output, flag[1] <- 1 on a
+// nonzero output below 2^-969 in magnitude; flag[1] == 0 on entry lets the
+// pass fuse its edge terms (exact for such inputs).
 void launch_relax_tma(int dim, bool sig, const TmaSet& tm, double* uo, double* duo,
                       const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
                       unsigned long long* diag_slot, int* flag, cudaStream_t s);
 // Residual recurrence at level 0 over the range: r -= A(e) + a e (tm.u = e,
 // tm.g = r, r written with mirror ghosts), u_tot += e (tm.t / utot,
-// nullable), max|r| into rmax_slot.  rc = relax_const(level 0).
+// nullable), max|r| into rmax_slot; reads flag[1] as the relaxation pass.
+// rc = relax_const(level 0).
 void launch_residual_tma(int dim, bool sig, const TmaSet& tm, double* r, double* utot,
                          const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
-                         unsigned long long* rmax_slot, cudaStream_t s);
+                         unsigned long long* rmax_slot, int* flag, cudaStream_t s);
 // Dirichlet-face nodes of an extended level array <- 0 (zero) or their face
 // value (the reference's lowest-face-id rule), with their mirror ghost cells
 // unless `mirrors` is false (DU arrays keep all-zero ghosts).

@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(MBX* MBY)
     // 3D: row J, spread plane index S (block-uniform);  2D: spread row S
     const int J = DIM == 3 ? blockIdx.y * MBY + threadIdx.y : 0;
     const int S = DIM == 3 ? blockIdx.z : blockIdx.y * MBY + threadIdx.y;
-    int bad = 0;
+    int bad = 0, tiny = 0;
     if (X4 < Nw && J < Nw && S <= H) {
         const int ncopy = S < H ? 2 : 1;
         const int s0 = S < H ? S : 2 * H;
@@ -176,11 +176,17 @@ __global__ void __launch_bounds__(MBX* MBY)
                     value = __ldg(ufine + eix<DIM>(Lf, I >> frel, Jn >> frel, Kn >> frel));
                 }
                 bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
+                {  // nonzero |value| < 2^-969 (see launch_relax_tma)
+                    const unsigned key = ((unsigned)__double2hiint(value) & 0x7fffffffu) |
+                                         (__double2loint(value) != 0 ? 1u : 0u);
+                    tiny |= key - 1u < 0x035fffffu;
+                }
                 store_ext<DIM>(out, Lw, I, Jn, Kn, value);
             }
         }
     }
     warp_or_commit(bad, flag);
+    warp_or_commit(tiny, flag + 1);
 }
 
 // ---------------------------------------------------------------------------

@@ -184,14 +184,15 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     };
 
     double dmax = 0.0;
-    unsigned badhi = 0;  // max exponent field of the produced values
+    unsigned badhi = 0;             // max exponent field of the produced values
+    unsigned tinymin = 0xffffffffu;  // see finish(): tiny nonzero outputs
 
     // the RT nodes' terms of one stencil plane (offset dr), interleaved term
     // by term so the independent accumulation chains overlap; the first
     // term starts the chain (0 + t differs from t only in the sign of zero)
     auto plane_terms = [&](double (&acc)[RT], double (&smax)[RT], const Win<DIM>& P,
                            const SWin<DIM, SIG>& Ps, const double (&uc)[RT], const double (&sc)[RT],
-                           int dr) {
+                           int dr, bool fm) {
 #pragma unroll
         for (int q = (DIM == 3 ? -1 : 0); q <= (DIM == 3 ? 1 : 0); ++q)
 #pragma unroll
@@ -207,8 +208,14 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                         sbar = 0.5 * (Ps[w][p + 1] + sc[a]);
                         smax[a] = first ? sbar : (smax[a] < sbar ? sbar : smax[a]);
                     }
-                    const double t = stencil_t<SIG>(sbar, P[w][p + 1], uc[a], l2);
-                    acc[a] = first ? t : acc[a] + t;
+                    if (!SIG && fm && l2 == 2) {
+                        // edge: (d * 0.5) is exact for these inputs, so the fused
+                        // multiply-add rounds once exactly like acc + (d * 0.5)
+                        acc[a] = fma(P[w][p + 1] - uc[a], 0.5, acc[a]);
+                    } else {
+                        const double t = stencil_t<SIG>(sbar, P[w][p + 1], uc[a], l2);
+                        acc[a] = first ? t : acc[a] + t;
+                    }
                 }
             }
     };
@@ -239,7 +246,11 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                 value = HAS_A ? num / rc.denom1 : num;
             }
             dmax = dmax < diag ? diag : dmax;
-            badhi = max(badhi, (unsigned)__double2hiint(value) & 0x7ff00000u);
+            const unsigned vhi = (unsigned)__double2hiint(value);
+            badhi = max(badhi, vhi & 0x7ff00000u);
+            // nonzero |value| < 2^-969 (exponent field < 54): key - 1 < 0x035fffff
+            const unsigned key = (vhi & 0x7fffffffu) | (__double2loint(value) != 0 ? 1u : 0u);
+            tinymin = min(tinymin, key - 1u);
             if (DUO) duo[pos] = value - uc;
         }
         uo[pos] = value;
@@ -262,7 +273,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
 
         // one plane: P0 = m-1, P1 = m (held), P2 <- m+1
         auto step = [&](int m, Win<DIM>& P0, Win<DIM>& P1, Win<DIM>& P2, SWin<DIM, SIG>& S0,
-                        SWin<DIM, SIG>& S1, SWin<DIM, SIG>& S2) {
+                        SWin<DIM, SIG>& S1, SWin<DIM, SIG>& S2, bool fm) {
             opos += ostep;
             // rotating producer: plane m + LEAD (the prologue issued up to m0 + LEAD);
             // its slot held plane m + LEAD - NST, released after step m + LEAD - NST + 1
@@ -283,27 +294,38 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                 acc[a] = 0.0;
                 smax[a] = 0.0;
             }
-            plane_terms(acc, smax, P0, S0, uc, sc, -1);
-            plane_terms(acc, smax, P1, S1, uc, sc, 0);
-            plane_terms(acc, smax, P2, S2, uc, sc, 1);
+            plane_terms(acc, smax, P0, S0, uc, sc, -1, fm);
+            plane_terms(acc, smax, P1, S1, uc, sc, 0, fm);
+            plane_terms(acc, smax, P2, S2, uc, sc, 1, fm);
             const bool mir_m = m == 1 || m == N - 2;
 #pragma unroll
             for (int a = 0; a < RT; ++a)
                 if (ok[a]) finish(m, a, mir_m, acc[a], smax[a], uc[a], gc[a], tc[a]);
             release(m);
         };
-        // roles rotate (P0, P1, P2) -> (P1, P2, P0) each plane: period 3
+        // roles rotate (P0, P1, P2) -> (P1, P2, P0) each plane: period 3.
+        // `fm` is a literal at both call sites (two specialised marches)
+        auto march = [&](bool fm) {
 #pragma unroll 1
-        for (int m = m0; m < mend; m += 3) {
-            step(m, X, Y, Z, Xs, Ys, Zs);
-            if (m + 1 >= mend) break;
-            step(m + 1, Y, Z, X, Ys, Zs, Xs);
-            if (m + 2 >= mend) break;
-            step(m + 2, Z, X, Y, Zs, Xs, Ys);
-        }
+            for (int m = m0; m < mend; m += 3) {
+                step(m, X, Y, Z, Xs, Ys, Zs, fm);
+                if (m + 1 >= mend) break;
+                step(m + 1, Y, Z, X, Ys, Zs, Xs, fm);
+                if (m + 2 >= mend) break;
+                step(m + 2, Z, X, Y, Zs, Xs, Ys, fm);
+            }
+        };
+        // edge terms fused when no input value is tiny (flag[1], set by the
+        // producers of this cycle's level arrays): then every difference d of
+        // two inputs is 0 or >= 2^-1021 in magnitude and d * 0.5 is exact
+        if (!SIG && *(volatile const int*)(flag + 1) == 0) march(true);
+        else march(false);
     }
     block_max_commit(dmax, diag_slot);
-    if (!RESID) block_or_commit(badhi == 0x7ff00000u, flag);
+    if (!RESID) {
+        warp_or_commit(badhi == 0x7ff00000u, flag);
+        warp_or_commit(tinymin < 0x035fffffu, flag + 1);
+    }
 }
 
 template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO>
@@ -393,8 +415,8 @@ void launch_relax_tma(int dim, bool sig, const TmaSet& tm, double* uo, double* d
 
 void launch_residual_tma(int dim, bool sig, const TmaSet& tm, double* r, double* utot,
                          const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
-                         unsigned long long* rmax_slot, cudaStream_t s) {
-    launch_mode<MODE_RESID>(dim, sig, tm, r, utot, L, rg, rc, rmax_slot, nullptr, s);
+                         unsigned long long* rmax_slot, int* flag, cudaStream_t s) {
+    launch_mode<MODE_RESID>(dim, sig, tm, r, utot, L, rg, rc, rmax_slot, flag, s);
 }
 
 }  // namespace sgmlb
