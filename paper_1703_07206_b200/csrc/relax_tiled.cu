@@ -23,11 +23,12 @@
 // consumers wait on `full`, each warp releases a slot on `empty`.
 //
 // In 3D every thread computes RT = 2 adjacent rows (y, y+1) of the plane: it
-// keeps a (RT+2) x 3 register window of each of planes m-1, m, m+1 (12
-// values per plane, so 6 shared loads per node) and the two nodes'
-// accumulation chains interleave term by term in the reference's strict
-// 26-term order.  The window roles rotate with period 3, so the march is
-// unrolled three steps and no register moves are issued.
+// keeps a (RT+2) x 3 register window of the two newest planes (12 values per
+// plane, so 6 shared loads per node) and the two nodes' accumulation chains
+// interleave term by term in the reference's strict 26-term order.  Terms
+// are summed as planes arrive (see the march); the window roles alternate
+// with period 2, so the march is unrolled two steps and no register moves
+// are issued.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                         sbar = 0.5 * (Ps[w][p + 1] + sc[a]);
                         smax[a] = first ? sbar : (smax[a] < sbar ? sbar : smax[a]);
                     }
-                    if (!SIG && fm && l2 == 2) {
+                    if (!SIG && fm && l2 == 2 && !first) {
                         // edge: (d * 0.5) is exact for these inputs, so the fused
                         // multiply-add rounds once exactly like acc + (d * 0.5)
                         acc[a] = fma(P[w][p + 1] - uc[a], 0.5, acc[a]);
@@ -258,61 +259,73 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             store_mirrors<DIM>(uo, L, xi, DIM == 3 ? yb + a : m, DIM == 3 ? m : 0, value);
     };
 
-    Win<DIM> X, Y, Z;  // window planes, rotating roles
-    SWin<DIM, SIG> Xs, Ys, Zs;
+    // Streaming march: the reference sums a node's terms plane by plane
+    // (dr = -1, 0, +1), so when plane q arrives the nodes of plane q get
+    // their dr = -1 and dr = 0 terms and the nodes of plane q-1 their dr = +1
+    // terms.  Only two window planes are live (registers for addressing
+    // instead of a third window).
+    Win<DIM> X, Y;  // planes q-1 / q, alternating roles
+    SWin<DIM, SIG> Xs, Ys;
+    double acc[RT], smax[RT];  // partial chains of the nodes of the newest plane
 
     if (m0 < mend) {
         if (tid == 0)
             for (int q = m0 - 1; q <= mend && q <= m0 + TL::LEAD; ++q) issue(q);
         wait_plane(m0 - 1);
         read_plane(m0 - 1, X, Xs);
-        wait_plane(m0);
-        read_plane(m0, Y, Ys);
         release(m0 - 1);
-        opos += (ptrdiff_t)m0 * ostep;
+        opos += (ptrdiff_t)m0 * ostep;  // plane m0 - 1
 
-        // one plane: P0 = m-1, P1 = m (held), P2 <- m+1
-        auto step = [&](int m, Win<DIM>& P0, Win<DIM>& P1, Win<DIM>& P2, SWin<DIM, SIG>& S0,
-                        SWin<DIM, SIG>& S1, SWin<DIM, SIG>& S2, bool fm) {
-            opos += ostep;
-            // rotating producer: plane m + LEAD (the prologue issued up to m0 + LEAD);
-            // its slot held plane m + LEAD - NST, released after step m + LEAD - NST + 1
-            if (warp == ((m - m0) & (TL::NWARPS - 1)) && lane == 0 && m > m0 && m + TL::LEAD <= mend)
-                issue(m + TL::LEAD);
-            wait_plane(m + 1);
-            read_plane(m + 1, P2, S2);
-            const unsigned sm = slot_of(m);
-            double uc[RT], sc[RT], acc[RT], smax[RT], gc[RT], tc[RT];
+        // plane q arrives in B (A holds plane q - 1)
+        auto step = [&](int q, Win<DIM>& A, Win<DIM>& B, SWin<DIM, SIG>& As, SWin<DIM, SIG>& Bs,
+                        bool fm) {
+            // rotating producer: plane q + LEAD (the prologue issued up to m0 + LEAD);
+            // its slot held plane q + LEAD - NST, released in step q + LEAD - NST + 1
+            if (warp == ((q - m0) & (TL::NWARPS - 1)) && lane == 0 && q > m0 && q + TL::LEAD <= mend)
+                issue(q + TL::LEAD);
+            wait_plane(q);
+            read_plane(q, B, Bs);
+            if (q > m0) {  // nodes of plane q - 1: dr = +1 terms, then the update
+                const int m = q - 1;
+                const unsigned sm = slot_of(m);
+                opos += ostep;
+                double uc[RT], sc[RT], gc[RT], tc[RT];
 #pragma unroll
-            for (int a = 0; a < RT; ++a) {
-                const int gi = gbase + TL::HXG * a;  // node in the g box
-                gc[a] = R.g[sm][gi];
-                tc[a] = (DUO && RESID) ? R.t[sm][gi] : 0.0;
-                uc[a] = P1[DIM == 3 ? a + 1 : 0][1];
-                sc[a] = 1.0;
-                if constexpr (SIG) sc[a] = S1[DIM == 3 ? a + 1 : 0][1];
-                acc[a] = 0.0;
-                smax[a] = 0.0;
+                for (int a = 0; a < RT; ++a) {
+                    const int gi = gbase + TL::HXG * a;  // node in the g box
+                    gc[a] = R.g[sm][gi];
+                    tc[a] = (DUO && RESID) ? R.t[sm][gi] : 0.0;
+                    uc[a] = A[DIM == 3 ? a + 1 : 0][1];
+                    sc[a] = 1.0;
+                    if constexpr (SIG) sc[a] = As[DIM == 3 ? a + 1 : 0][1];
+                }
+                plane_terms(acc, smax, B, Bs, uc, sc, 1, fm);
+                const bool mir_m = m == 1 || m == N - 2;
+#pragma unroll
+                for (int a = 0; a < RT; ++a)
+                    if (ok[a]) finish(m, a, mir_m, acc[a], smax[a], uc[a], gc[a], tc[a]);
+                release(m);
             }
-            plane_terms(acc, smax, P0, S0, uc, sc, -1, fm);
-            plane_terms(acc, smax, P1, S1, uc, sc, 0, fm);
-            plane_terms(acc, smax, P2, S2, uc, sc, 1, fm);
-            const bool mir_m = m == 1 || m == N - 2;
+            if (q < mend) {  // nodes of plane q: dr = -1 and dr = 0 terms
+                double uc[RT], sc[RT];
 #pragma unroll
-            for (int a = 0; a < RT; ++a)
-                if (ok[a]) finish(m, a, mir_m, acc[a], smax[a], uc[a], gc[a], tc[a]);
-            release(m);
+                for (int a = 0; a < RT; ++a) {
+                    uc[a] = B[DIM == 3 ? a + 1 : 0][1];
+                    sc[a] = 1.0;
+                    if constexpr (SIG) sc[a] = Bs[DIM == 3 ? a + 1 : 0][1];
+                }
+                plane_terms(acc, smax, A, As, uc, sc, -1, fm);
+                plane_terms(acc, smax, B, Bs, uc, sc, 0, fm);
+            }
         };
-        // roles rotate (P0, P1, P2) -> (P1, P2, P0) each plane: period 3.
-        // `fm` is a literal at both call sites (two specialised marches)
+        // roles alternate each plane: period 2.  `fm` is a literal at both
+        // call sites (two specialised marches)
         auto march = [&](bool fm) {
 #pragma unroll 1
-            for (int m = m0; m < mend; m += 3) {
-                step(m, X, Y, Z, Xs, Ys, Zs, fm);
-                if (m + 1 >= mend) break;
-                step(m + 1, Y, Z, X, Ys, Zs, Xs, fm);
-                if (m + 2 >= mend) break;
-                step(m + 2, Z, X, Y, Zs, Xs, Ys, fm);
+            for (int q = m0; q <= mend; q += 2) {
+                step(q, X, Y, Xs, Ys, fm);
+                if (q + 1 > mend) break;
+                step(q + 1, Y, X, Ys, Xs, fm);
             }
         };
         // edge terms fused when no input value is tiny (flag[1], set by the
