@@ -298,12 +298,17 @@ __device__ __forceinline__ void block_or_commit(int bad, int* flag) {
 namespace sgmlb {
 
 struct ExtLay {
-    int N;            // data nodes per axis
+    int N;            // data nodes per axis (global)
     int Ne;           // N + 2
     int Px;           // row pitch in doubles (even)
+    int Nz;           // 3D: data planes held (N, or a z-slab's own planes)
+    int z0;           // 3D: global index of local data plane 0 (0 unless a z-slab)
     int pad_;
     long long plane;  // stride of the slowest axis: Px * Ne (3D) or Px (2D)
 };
+// Indices passed to eix are LOCAL in z (global - z0).  A z-slab holds planes
+// z0 - 1 .. z0 + Nz (halo planes from the neighbour ranks, or the mirror
+// ghost planes at the global faces).
 
 template <int DIM>
 __device__ __forceinline__ ptrdiff_t eix(const ExtLay& L, int i, int j, int k) {
@@ -311,10 +316,12 @@ __device__ __forceinline__ ptrdiff_t eix(const ExtLay& L, int i, int j, int k) {
                     : (ptrdiff_t)(i + 1) + (ptrdiff_t)L.Px * (j + 1);
 }
 
-// write the even-mirror ghost cells of data node (i, j, k) (rare path)
+// write the even-mirror ghost cells of data node (i, j, k) (rare path; k
+// local: the z mirrors exist at the global faces only)
 template <int DIM>
 __device__ __noinline__ void store_mirrors(double* a, ExtLay L, int i, int j, int k, double v) {
     const int N = L.N;
+    k += DIM == 3 ? L.z0 : 0;  // global
     int ci[3], cj[3], ck[3];
     int ni = 1, nj = 1, nk = 1;
     ci[0] = i;
@@ -331,14 +338,14 @@ __device__ __noinline__ void store_mirrors(double* a, ExtLay L, int i, int j, in
     for (int ia = 0; ia < ni; ++ia)
         for (int ib = 0; ib < nj; ++ib)
             for (int ic = 0; ic < nk; ++ic)
-                if (ia | ib | ic) a[eix<DIM>(L, ci[ia], cj[ib], ck[ic])] = v;
+                if (ia | ib | ic) a[eix<DIM>(L, ci[ia], cj[ib], DIM == 3 ? ck[ic] - L.z0 : 0)] = v;
 }
 
 template <int DIM>
 __device__ __forceinline__ void store_ext(double* a, const ExtLay& L, int i, int j, int k, double v) {
     a[eix<DIM>(L, i, j, k)] = v;
-    const int N = L.N;
-    if (i == 1 || i == N - 2 || j == 1 || j == N - 2 || (DIM == 3 && (k == 1 || k == N - 2)))
+    const int N = L.N, kg = DIM == 3 ? k + L.z0 : 0;
+    if (i == 1 || i == N - 2 || j == 1 || j == N - 2 || (DIM == 3 && (kg == 1 || kg == N - 2)))
         store_mirrors<DIM>(a, L, i, j, k, v);
 }
 

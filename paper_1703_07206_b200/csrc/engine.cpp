@@ -175,7 +175,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 CUtensorMap make_map(int dim, const double* p, const ExtLay& L, const unsigned* box) {
     CUtensorMap m;
-    cuuint64_t dims[3] = {(cuuint64_t)L.Ne, (cuuint64_t)L.Ne, (cuuint64_t)L.Ne};
+    cuuint64_t dims[3] = {(cuuint64_t)L.Ne, (cuuint64_t)L.Ne, (cuuint64_t)(L.Nz + 2)};
     cuuint64_t strides[2] = {(cuuint64_t)L.Px * 8, (cuuint64_t)L.Px * L.Ne * 8};
     cuuint32_t bx[3] = {box[0], box[1], box[2]};
     cuuint32_t es[3] = {1, 1, 1};

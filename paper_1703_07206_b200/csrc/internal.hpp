@@ -39,7 +39,9 @@ void launch_check_finite(const double* f, uint64_t total, int* flag, cudaStream_
 // Compact engine (ghost-extended padded level arrays, device.cuh ExtLay)
 // ---------------------------------------------------------------------------
 
-ExtLay make_ext(int dim, int N);
+// nz < 0: the whole level (Nz = N, z0 = 0); otherwise a z-slab of planes
+// [z0, z0 + nz) with halo planes
+ExtLay make_ext(int dim, int N, int z0 = 0, int nz = -1);
 uint64_t ext_size(int dim, const ExtLay& L);  // doubles to allocate
 
 // One pending interpolation increment: a level-`level` compact variation.
@@ -96,9 +98,10 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
                          const ExtLay& L0, bool base_zero, const double* ufine, const ExtLay& Lf,
                          int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
                          bool homogeneous, int* flag, cudaStream_t s);
-// Restriction pyramid step level m -> m+1.
+// Restriction pyramid step level m -> m+1, output planes
+// [kb, ke) (local; ke < 0: all planes of Lout).
 void launch_pyramid_ext(int dim, const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout,
-                        cudaStream_t s);
+                        cudaStream_t s, int kb = 0, int ke = -1);
 void launch_scatter_ext(int dim, const double* dense, double* ext, const ExtLay& L, cudaStream_t s);
 void launch_gather_ext(int dim, const double* ext, const ExtLay& L, double* dense, cudaStream_t s);
 

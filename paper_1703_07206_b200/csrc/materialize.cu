@@ -16,15 +16,16 @@
 // with I_l(du)(x) = sum over corners r, q, p of ((wz*wy)*wx) * du[corner]
 // (all weights exact dyadics; zero-weight corner rows in y / z are skipped,
 // which changes at most the sign of an exact zero).
-// A thread owns MV = 4 consecutive x nodes in two "spread copies" along the
-// slowest axis (z in 3D, y in 2D): planes S and S + H with H = (Nw - 1) / 2.
+// A thread owns MV = 4 consecutive x nodes in two "spread copies" along y:
+// rows S and S + H with H = (Nw - 1) / 2 (y, not z: 3D level arrays may be
+// z-slabs of a multi-GPU decomposition).
 // Every chain level l has cells of 2^(l-w) target nodes, which divides H, so
 // the two copies see identical interpolation weights: each weight product
 // is formed once and used for 2 x 4 nodes.  For every level coarser than
 // the first, the four x nodes of a copy share one cell, so its 8 corner
 // loads serve four nodes; y and z are uniform across a warp, so zero-weight
-// corner rows are skipped without divergence.  The plane S = H holds the
-// last plane 2H alone (its second copy is computed redundantly and dropped).
+// corner rows are skipped without divergence.  The row S = H holds the
+// last row 2H alone (its second copy is computed redundantly and dropped).
 // Threads whose nodes all lie on Dirichlet faces skip the chain.  Chain
 // descriptors sit in shared memory.
 #include <cuda_runtime.h>
@@ -52,32 +53,32 @@ __global__ void __launch_bounds__(MBX* MBY)
 
     const int Nw = Lw.N, H = (Nw - 1) >> 1;
     const int X4 = (blockIdx.x * MBX + threadIdx.x) * MV;
-    // 3D: row J, spread plane index S (block-uniform);  2D: spread row S
-    const int J = DIM == 3 ? blockIdx.y * MBY + threadIdx.y : 0;
-    const int S = DIM == 3 ? blockIdx.z : blockIdx.y * MBY + threadIdx.y;
+    // spread row index S (warp-uniform); 3D: local plane K (block-uniform),
+    // global plane Kg (z-slab arrays start at global plane Lw.z0)
+    const int S = blockIdx.y * MBY + threadIdx.y;
+    const int K = DIM == 3 ? (int)blockIdx.z : 0;
+    const int Kg = DIM == 3 ? K + Lw.z0 : 0;
     int bad = 0, tiny = 0;
-    if (X4 < Nw && J < Nw && S <= H) {
+    if (X4 < Nw && S <= H) {
         const int ncopy = S < H ? 2 : 1;
         const int s0 = S < H ? S : 2 * H;
         const int nv = min(MV, Nw - X4);
-        // node (k, copy cp): x = X4 + k, spread coordinate s0 + cp * H
-        auto node_j = [&](int cp) { return DIM == 3 ? J : s0 + cp * H; };
-        auto node_k = [&](int cp) { return DIM == 3 ? s0 + cp * H : 0; };
+        // node (k, copy cp): x = X4 + k, y = s0 + cp * H
+        auto node_j = [&](int cp) { return s0 + cp * H; };
         // every node of this thread on a Dirichlet face: nothing to interpolate
         const bool xdir = nv == 1 && X4 == Nw - 1 && !bc.neu[1];
-        const bool rowdir = DIM == 3 ? ((J == 0 && !bc.neu[2]) || (J == Nw - 1 && !bc.neu[3]))
-                                     : (ncopy == 1 && !bc.neu[3]);
-        const bool pdir = DIM == 3 && ncopy == 1 && !bc.neu[5];
+        const bool rowdir = ncopy == 1 && !bc.neu[3];
+        const bool pdir = DIM == 3 && ((Kg == 0 && !bc.neu[4]) || (Kg == Nw - 1 && !bc.neu[5]));
         const int nch = (xdir || rowdir || pdir) ? 0 : nchain;
 
-        const int y = (DIM == 3 ? J : s0) << w, z = DIM == 3 ? s0 << w : 0;
+        const int y = s0 << w, z = Kg << w;
         double val[2][MV];
 #pragma unroll
         for (int cp = 0; cp < 2; ++cp)
 #pragma unroll
             for (int k = 0; k < MV; ++k)
                 val[cp][k] = (!base_zero && k < nv && cp < ncopy)
-                                 ? __ldg(base + eix<DIM>(L0, (X4 + k) << w, node_j(cp) << w, node_k(cp) << w))
+                                 ? __ldg(base + eix<DIM>(L0, (X4 + k) << w, node_j(cp) << w, z - L0.z0))
                                  : 0.0;
 
         for (int c = 0; c < nch; ++c) {
@@ -91,10 +92,10 @@ __global__ void __launch_bounds__(MBX* MBY)
             const double wz[2] = {1.0 - fz, fz};
             const int nq = iy ? 2 : 1, nr = (DIM == 3 && iz) ? 2 : 1;  // warp-uniform
             const int X0 = (X4 << w) >> l;
-            // strides: q row, r plane, second copy (0 when it is a dummy)
+            // strides: q row, r plane, second copy (rows; 0 when it is a dummy)
             const ptrdiff_t sq = ce.L.Px, sr = DIM == 3 ? ce.L.plane : 0;
-            const ptrdiff_t dsp = ncopy == 2 ? (ptrdiff_t)((Nl - 1) >> 1) * (DIM == 3 ? sr : sq) : 0;
-            const double* p00 = ce.du + eix<DIM>(ce.L, X0, y >> l, DIM == 3 ? z >> l : 0);
+            const ptrdiff_t dsp = ncopy == 2 ? (ptrdiff_t)((Nl - 1) >> 1) * sq : 0;
+            const double* p00 = ce.du + eix<DIM>(ce.L, X0, y >> l, DIM == 3 ? (z >> l) - ce.L.z0 : 0);
             // the run of MV nodes straddles two cells only on level w + 1
             const bool straddle = l == w + 1;
             double fx[MV], wx0[MV];
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(MBX* MBY)
 #pragma unroll
         for (int cp = 0; cp < 2; ++cp) {
             if (cp >= ncopy) break;
-            const int Jn = node_j(cp), Kn = node_k(cp);
+            const int Jn = node_j(cp), Kn = Kg;
             const bool jface = Jn == 0 || Jn == Nw - 1 || (DIM == 3 && (Kn == 0 || Kn == Nw - 1));
 #pragma unroll
             for (int k = 0; k < MV; ++k) {
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(MBX* MBY)
                 if ((jface || I == 0 || I == Nw - 1) && on_dirichlet<DIM>(bc, Nw, I, Jn, Kn)) {
                     value = homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, I, Jn, Kn);
                 } else if (ufine && ((I | Jn | Kn) & fmask) == 0) {
-                    value = __ldg(ufine + eix<DIM>(Lf, I >> frel, Jn >> frel, Kn >> frel));
+                    value = __ldg(ufine + eix<DIM>(Lf, I >> frel, Jn >> frel, (Kn >> frel) - Lf.z0));
                 }
                 bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
                 {  // nonzero |value| < 2^-969 (see launch_relax_tma)
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(MBX* MBY)
                                          (__double2loint(value) != 0 ? 1u : 0u);
                     tiny |= key - 1u < 0x035fffffu;
                 }
-                store_ext<DIM>(out, Lw, I, Jn, Kn, value);
+                store_ext<DIM>(out, Lw, I, Jn, K, value);
             }
         }
     }
@@ -202,11 +203,14 @@ __device__ __forceinline__ double axw2(int o) { return o == 0 ? 0.5 : 0.25; }
 
 template <int DIM>
 __global__ void __launch_bounds__(128) k_pyramid_ext(const double* __restrict__ in, ExtLay Lin,
-                                                     double* __restrict__ out, ExtLay Lout) {
+                                                     double* __restrict__ out, ExtLay Lout, int kb) {
     const int Nout = Lout.N;
-    const int I = blockIdx.x * 32 + threadIdx.x, J = blockIdx.y * 4 + threadIdx.y, K = blockIdx.z;
+    // output plane: local kb + blockIdx.z, global + Lout.z0; input plane 2 * global
+    const int I = blockIdx.x * 32 + threadIdx.x, J = blockIdx.y * 4 + threadIdx.y;
+    const int K = DIM == 3 ? kb + (int)blockIdx.z : 0;
     if (I >= Nout || J >= Nout) return;
-    const double* c = in + eix<DIM>(Lin, 2 * I, 2 * J, DIM == 3 ? 2 * K : 0);
+    const int Kin = DIM == 3 ? 2 * (K + Lout.z0) - Lin.z0 : 0;
+    const double* c = in + eix<DIM>(Lin, 2 * I, 2 * J, Kin);
     const ptrdiff_t sy = Lin.Px, sz = (ptrdiff_t)Lin.Px * Lin.Ne;
     double acc = 0.0;
 #pragma unroll
@@ -221,60 +225,74 @@ __global__ void __launch_bounds__(128) k_pyramid_ext(const double* __restrict__ 
     store_ext<DIM>(out, Lout, I, J, K, acc);
 }
 
-// dense x-fastest field -> ghost-extended array (data + mirror ghosts)
+// dense x-fastest field (global) -> ghost-extended array (own planes + mirror ghosts)
 template <int DIM>
 __global__ void __launch_bounds__(128) k_scatter_ext(const double* __restrict__ dense, double* ext,
                                                      ExtLay L) {
     const int N = L.N;
     const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 4 + threadIdx.y, k = blockIdx.z;
     if (i >= N || j >= N) return;
-    store_ext<DIM>(ext, L, i, j, k, dense[lin3(N, i, j, k)]);
+    store_ext<DIM>(ext, L, i, j, k, dense[lin3(N, i, j, DIM == 3 ? k + L.z0 : 0)]);
 }
 
-// ghost-extended array -> dense x-fastest field
+// ghost-extended array (own planes) -> dense x-fastest field (global)
 template <int DIM>
 __global__ void __launch_bounds__(128) k_gather_ext(const double* __restrict__ ext, ExtLay L,
                                                     double* __restrict__ dense) {
     const int N = L.N;
     const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 4 + threadIdx.y, k = blockIdx.z;
     if (i >= N || j >= N) return;
-    dense[lin3(N, i, j, k)] = ext[eix<DIM>(L, i, j, k)];
+    dense[lin3(N, i, j, DIM == 3 ? k + L.z0 : 0)] = ext[eix<DIM>(L, i, j, k)];
 }
 
 // Dirichlet-face nodes (with their mirror ghosts) <- 0 or the face value.
 // One thread per (face, a, b); nodes on edges are written by several faces
-// with the same value (the lowest-face-id rule of dirichlet_value).
+// with the same value (the lowest-face-id rule of dirichlet_value).  z-slab
+// arrays: the x / y faces of the own planes, the z faces where they are own.
 template <int DIM>
 __global__ void __launch_bounds__(128) k_dirichlet_faces(double* a, ExtLay L, BcDev bc, int zero, int mirrors) {
     const int N = L.N;
     const int p = blockIdx.x * 32 + threadIdx.x, q = blockIdx.y * 4 + threadIdx.y, f = blockIdx.z;
-    if (p >= N || (DIM == 3 && q >= N) || (DIM == 2 && q > 0) || bc.neu[f]) return;
+    if (p >= N || (DIM == 2 && q > 0) || bc.neu[f]) return;
     const int side = (f & 1) ? N - 1 : 0;
-    int i, j, k = 0;
-    if (f < 2) { i = side; j = p; k = q; }
-    else if (f < 4) { i = p; j = side; k = q; }
-    else { i = p; j = q; k = side; }
-    if (DIM == 2 && f < 2) { j = p; k = 0; }
-    const double v = zero ? 0.0 : dirichlet_value<DIM>(bc, N, i, j, k);
+    int i, j, kg = 0;
+    if (DIM == 2) {
+        if (f < 2) { i = side; j = p; }
+        else { i = p; j = side; }
+    } else if (f < 4) {
+        if (q >= L.Nz) return;  // q: local plane
+        kg = q + L.z0;
+        if (f < 2) { i = side; j = p; }
+        else { i = p; j = side; }
+    } else {
+        if (q >= N || side < L.z0 || side >= L.z0 + L.Nz) return;
+        i = p; j = q; kg = side;
+    }
+    const double v = zero ? 0.0 : dirichlet_value<DIM>(bc, N, i, j, kg);
+    const int k = DIM == 3 ? kg - L.z0 : 0;
     if (mirrors) store_ext<DIM>(a, L, i, j, k, v);
     else a[eix<DIM>(L, i, j, k)] = v;
 }
 
-inline dim3 ext_grid(int dim, int N) { return dim3((N + 31) / 32, (N + 3) / 4, dim == 3 ? N : 1); }
+inline dim3 ext_grid(int dim, const ExtLay& L) {
+    return dim3((L.N + 31) / 32, (L.N + 3) / 4, dim == 3 ? L.Nz : 1);
+}
 
 }  // namespace
 
-ExtLay make_ext(int dim, int N) {
+ExtLay make_ext(int dim, int N, int z0, int nz) {
     ExtLay L{};
     L.N = N;
     L.Ne = N + 2;
     L.Px = (L.Ne + 1) / 2 * 2;  // even pitch: 16-byte aligned rows for TMA
+    L.Nz = dim == 3 ? (nz < 0 ? N : nz) : 1;
+    L.z0 = dim == 3 ? z0 : 0;
     L.plane = dim == 3 ? (long long)L.Px * L.Ne : (long long)L.Px;
     return L;
 }
 
 uint64_t ext_size(int dim, const ExtLay& L) {
-    return dim == 3 ? (uint64_t)L.Px * L.Ne * L.Ne : (uint64_t)L.Px * L.Ne;
+    return dim == 3 ? (uint64_t)L.Px * L.Ne * (L.Nz + 2) : (uint64_t)L.Px * L.Ne;
 }
 
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
@@ -283,8 +301,7 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
                          bool homogeneous, int* flag, cudaStream_t s) {
     const int Nw = Lw.N;
     const int threads_x = (Nw + MV - 1) / MV, H = (Nw - 1) / 2;
-    const dim3 grid((threads_x + MBX - 1) / MBX, dim == 3 ? (Nw + MBY - 1) / MBY : (H + MBY) / MBY,
-                    dim == 3 ? H + 1 : 1);
+    const dim3 grid((threads_x + MBX - 1) / MBX, (H + MBY) / MBY, dim == 3 ? Lw.Nz : 1);
     if (dim == 2)
         k_materialize4<2><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, base_zero, ufine, Lf, frel,
                                                           chain, nchain, bc, homogeneous, flag);
@@ -294,19 +311,26 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
 }
 
 void launch_pyramid_ext(int dim, const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout,
-                        cudaStream_t s) {
-    if (dim == 2) k_pyramid_ext<2><<<ext_grid(2, Lout.N), dim3(32, 4), 0, s>>>(in, Lin, out, Lout);
-    else k_pyramid_ext<3><<<ext_grid(3, Lout.N), dim3(32, 4), 0, s>>>(in, Lin, out, Lout);
+                        cudaStream_t s, int kb, int ke) {
+    if (dim == 2) {
+        k_pyramid_ext<2><<<ext_grid(2, Lout), dim3(32, 4), 0, s>>>(in, Lin, out, Lout, 0);
+        return;
+    }
+    if (ke < 0) ke = Lout.Nz;
+    if (ke <= kb) return;
+    dim3 g = ext_grid(3, Lout);
+    g.z = ke - kb;
+    k_pyramid_ext<3><<<g, dim3(32, 4), 0, s>>>(in, Lin, out, Lout, kb);
 }
 
 void launch_scatter_ext(int dim, const double* dense, double* ext, const ExtLay& L, cudaStream_t s) {
-    if (dim == 2) k_scatter_ext<2><<<ext_grid(2, L.N), dim3(32, 4), 0, s>>>(dense, ext, L);
-    else k_scatter_ext<3><<<ext_grid(3, L.N), dim3(32, 4), 0, s>>>(dense, ext, L);
+    if (dim == 2) k_scatter_ext<2><<<ext_grid(2, L), dim3(32, 4), 0, s>>>(dense, ext, L);
+    else k_scatter_ext<3><<<ext_grid(3, L), dim3(32, 4), 0, s>>>(dense, ext, L);
 }
 
 void launch_gather_ext(int dim, const double* ext, const ExtLay& L, double* dense, cudaStream_t s) {
-    if (dim == 2) k_gather_ext<2><<<ext_grid(2, L.N), dim3(32, 4), 0, s>>>(ext, L, dense);
-    else k_gather_ext<3><<<ext_grid(3, L.N), dim3(32, 4), 0, s>>>(ext, L, dense);
+    if (dim == 2) k_gather_ext<2><<<ext_grid(2, L), dim3(32, 4), 0, s>>>(ext, L, dense);
+    else k_gather_ext<3><<<ext_grid(3, L), dim3(32, 4), 0, s>>>(ext, L, dense);
 }
 
 void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc, bool zero,

@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                     if constexpr (SIG) sc[a] = As[DIM == 3 ? a + 1 : 0][1];
                 }
                 plane_terms(acc, smax, B, Bs, uc, sc, 1, fm);
-                const bool mir_m = m == 1 || m == N - 2;
+                const int mg = DIM == 3 ? m + L.z0 : m;  // global plane
+                const bool mir_m = mg == 1 || mg == N - 2;
 #pragma unroll
                 for (int a = 0; a < RT; ++a)
                     if (ok[a]) finish(m, a, mir_m, acc[a], smax[a], uc[a], gc[a], tc[a]);
