@@ -154,6 +154,29 @@ int sgml_ctx_synchronize(sgml_ctx* ctx);
 /* the stream every kernel of this ctx is launched on (cudaStream_t) */
 void* sgml_ctx_stream(sgml_ctx* ctx);
 
+/* ---- multi-GPU clique (z-slab solves) ---------------------
+ * One context per rank.  A 3D compact-engine solve (sgml_solve, sgml_solver_*)
+ * on a context that joined a clique of nranks > 1 runs the z-slab
+ * decomposition: every rank passes the same full problem and receives the
+ * full solution; the report is identical on all ranks and bit-identical to
+ * the single-GPU solve (every reduction is a max).  nranks must be a power
+ * of two with at least 2 level-0 planes per rank. */
+typedef struct sgml_group sgml_group;
+/* NCCL, one process per GPU: rank 0 creates the id, every rank joins with it
+ * (libnccl.so.2 is opened at run time) */
+int sgml_nccl_unique_id(unsigned char id[128]);
+int sgml_ctx_join_nccl(sgml_ctx* ctx, int nranks, int rank, const unsigned char id[128]);
+/* in-process ranks (one host thread per rank, devices may be shared): the
+ * parity tests of the decomposition on one GPU */
+int sgml_local_group_create(int nranks, sgml_group** out);
+int sgml_local_group_destroy(sgml_group* g);
+int sgml_ctx_join_local(sgml_ctx* ctx, sgml_group* g, int rank);
+int sgml_ctx_clique(sgml_ctx* ctx, int* nranks, int* rank);
+/* the z-slab plan (host only): levels < *vrep are z-slabs and rank `rank`
+ * owns level-v planes [z0 >> v, (z0 >> v) + nz_v) with nz_v = (nz - last) >> v
+ * + last, last = (rank == nranks - 1); level-0 planes [*z0, *z0 + *nz) */
+int sgml_slab_plan(int n, int nranks, int rank, int* vrep, int* z0, int* nz);
+
 /* ---- grid / schedule (host logic; no device needed) --------------------- */
 int sgml_make_grid(int dim, int n, sgml_grid* out);                      /* grid.cpp:10-23 */
 /* cycle.cpp:28-45: kinds 0 = restrict_source, 1 = relax; returns the step

@@ -107,6 +107,14 @@ _SIGNATURES = {
     "sgml_solver_footprint": ([_P, _U64P], C.c_int),
     "sgml_solve": ([_P, C.c_int, C.c_int, C.POINTER(Bc), _D, _D, C.c_double, C.POINTER(SolverCfg),
                     C.POINTER(SolverOpts), _D, C.POINTER(Report)], C.c_int),
+    "sgml_nccl_unique_id": ([C.c_char_p], C.c_int),
+    "sgml_ctx_join_nccl": ([_P, C.c_int, C.c_int, C.c_char_p], C.c_int),
+    "sgml_local_group_create": ([C.c_int, C.POINTER(_P)], C.c_int),
+    "sgml_local_group_destroy": ([_P], C.c_int),
+    "sgml_ctx_join_local": ([_P, _P, C.c_int], C.c_int),
+    "sgml_ctx_clique": ([_P, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+    "sgml_slab_plan": ([C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                        C.POINTER(C.c_int)], C.c_int),
     "sgml_host_alloc": ([C.c_uint64, C.POINTER(_P)], C.c_int),
     "sgml_host_free": ([_P], C.c_int),
 }

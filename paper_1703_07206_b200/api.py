@@ -26,7 +26,7 @@ __all__ = [
     "CycleSchedule", "build_schedule", "closed_form_work_units", "schedule_work_units",
     "SolverConfig", "SolverOptions", "DiagSample", "CycleRecord", "SolveReport", "ProblemSpec",
     "SolveResult", "single_cycle", "solve", "Solver", "restrict_sigma_levels", "pure_neumann_pin",
-    "kernel_error",
+    "kernel_error", "LocalGroup", "nccl_unique_id", "slab_plan",
 ]
 
 
@@ -161,6 +161,25 @@ class Context:
     def synchronize(self) -> None:
         check(lib().sgml_ctx_synchronize(self._h))
 
+    # ---- multi-GPU clique (z-slab solves) ------------------
+    def join_nccl(self, nranks: int, rank: int, unique_id: bytes) -> None:
+        """Join an NCCL clique (one process per GPU); rank 0 makes the id
+        with nccl_unique_id() and shares it (e.g. torch.distributed)."""
+        if len(unique_id) != 128:
+            raise ValueError("join_nccl: the NCCL unique id is 128 bytes")
+        check(lib().sgml_ctx_join_nccl(self._h, nranks, rank, unique_id))
+
+    def join_local(self, group: "LocalGroup", rank: int) -> None:
+        """Join an in-process clique (one host thread per rank)."""
+        check(lib().sgml_ctx_join_local(self._h, group.handle, rank))
+        self._group = group  # keep the group alive
+
+    def clique(self) -> tuple[int, int]:
+        """(nranks, rank) of the clique this context belongs to."""
+        n, r = C.c_int(), C.c_int()
+        check(lib().sgml_ctx_clique(self._h, C.byref(n), C.byref(r)))
+        return n.value, r.value
+
     def close(self) -> None:
         if self._h:
             lib().sgml_ctx_destroy(self._h)
@@ -171,6 +190,42 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class LocalGroup:
+    """In-process clique of `nranks` ranks (one host thread per rank; the
+    decomposition's parity tests run it on one GPU)."""
+
+    def __init__(self, nranks: int):
+        self._h = C.c_void_p()
+        check(lib().sgml_local_group_create(nranks, C.byref(self._h)))
+        self.nranks = nranks
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().sgml_local_group_destroy(self._h)
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    """A new NCCL clique id (128 bytes) for Context.join_nccl."""
+    buf = C.create_string_buffer(128)
+    check(lib().sgml_nccl_unique_id(buf))
+    return buf.raw
+
+
+def slab_plan(n: int, nranks: int, rank: int) -> tuple[int, int, int]:
+    """(vrep, z0, nz): levels < vrep are z-slabs; `rank` owns level-0 planes
+    [z0, z0 + nz) of the 2^n + 1 (host only)."""
+    v, z0, nz = C.c_int(), C.c_int(), C.c_int()
+    check(lib().sgml_slab_plan(n, nranks, rank, C.byref(v), C.byref(z0), C.byref(nz)))
+    return v.value, z0.value, nz.value
 
 
 _default_ctx: dict = {}

@@ -91,6 +91,82 @@ int sgml_ctx_create(int device, sgml_ctx** out) {
     });
 }
 
+struct sgml_group {
+    std::shared_ptr<sgmlb::LocalGroup> g;
+};
+
+int sgml_nccl_unique_id(unsigned char id[128]) {
+    return guarded([&] {
+        require(id != nullptr, SGML_EINVAL, "nccl_unique_id: null id");
+        sgmlb::nccl_unique_id(id);
+    });
+}
+
+int sgml_ctx_join_nccl(sgml_ctx* ctx, int nranks, int rank, const unsigned char id[128]) {
+    return guarded([&] {
+        require(ctx && id, SGML_EINVAL, "ctx_join_nccl: null argument");
+        require(nranks >= 1 && rank >= 0 && rank < nranks, SGML_EINVAL, "ctx_join_nccl: bad rank");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        SGML_CUDA(cudaSetDevice(ctx->device));
+        delete ctx->cached;
+        ctx->cached = nullptr;
+        ctx->cached_key.clear();
+        ctx->tp = sgmlb::make_nccl_transport(nranks, rank, id);
+    });
+}
+
+int sgml_local_group_create(int nranks, sgml_group** out) {
+    return guarded([&] {
+        require(out != nullptr && nranks >= 1, SGML_EINVAL, "local_group_create: bad arguments");
+        auto g = std::make_unique<sgml_group>();
+        g->g = std::make_shared<sgmlb::LocalGroup>(nranks);
+        *out = g.release();
+    });
+}
+
+int sgml_local_group_destroy(sgml_group* g) {
+    return guarded([&] { delete g; });
+}
+
+int sgml_ctx_join_local(sgml_ctx* ctx, sgml_group* g, int rank) {
+    return guarded([&] {
+        require(ctx && g, SGML_EINVAL, "ctx_join_local: null argument");
+        require(rank >= 0 && rank < g->g->size, SGML_EINVAL, "ctx_join_local: bad rank");
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        delete ctx->cached;
+        ctx->cached = nullptr;
+        ctx->cached_key.clear();
+        ctx->tp.reset(new sgmlb::LocalTransport(g->g, rank));
+    });
+}
+
+int sgml_ctx_clique(sgml_ctx* ctx, int* nranks, int* rank) {
+    return guarded([&] {
+        require(ctx && nranks && rank, SGML_EINVAL, "ctx_clique: null argument");
+        *nranks = ctx->tp ? ctx->tp->size : 1;
+        *rank = ctx->tp ? ctx->tp->rank : 0;
+    });
+}
+
+int sgml_slab_plan(int n, int nranks, int rank, int* vrep, int* z0, int* nz) {
+    return guarded([&] {
+        require(vrep && z0 && nz, SGML_EINVAL, "slab_plan: null argument");
+        require(n >= 1 && n <= 13, SGML_EINVAL, "slab_plan: n must lie in [1, 13]");
+        require(nranks >= 1 && (nranks & (nranks - 1)) == 0, SGML_EINVAL,
+                "slab_plan: the number of ranks must be a power of two");
+        require(nranks <= (1 << (n - 1)) || nranks == 1, SGML_EINVAL,
+                "slab_plan: too many ranks for this grid (>= 2 planes each)");
+        require(rank >= 0 && rank < nranks, SGML_EINVAL, "slab_plan: bad rank");
+        const int t0 = (1 << n) / nranks;
+        int v = 0;
+        if (nranks > 1)
+            while ((t0 >> v) >= 2) ++v;
+        *vrep = v;
+        *z0 = rank * t0;
+        *nz = t0 + (rank == nranks - 1 ? 1 : 0);
+    });
+}
+
 int sgml_ctx_destroy(sgml_ctx* ctx) {
     return guarded([&] {
         if (!ctx) return;

@@ -231,13 +231,13 @@ sgml_solver::~sgml_solver() {
     if (tev0) cudaEventDestroy(tev0);
     if (tev1) cudaEventDestroy(tev1);
     if (d_chain) cudaFree(d_chain);
+    dfree(BS);
     if (d_cycle) cudaFree(d_cycle);
     if (d_flag) cudaFree(d_flag);
     if (h_cycle) cudaFreeHost(h_cycle);
     if (h_flag) cudaFreeHost(h_flag);
 }
 
-static uint64_t pow_dim(int N, int dim) { return dim == 2 ? (uint64_t)N * N : (uint64_t)N * N * N; }
 
 void sgml_solver::check_launch(int cls) {
     static const char* names[] = {"relax0", "relax_coarse", "materialize", "pyramid", "residual",
@@ -310,16 +310,43 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
     Nl.resize(n);
     for (int v = 0; v < n; ++v) Nl[v] = (1 << (n - v)) + 1;
 
+    // multi-GPU clique of the context: z-slab plan
+    tp = ctx->tp.get();
+    nrk = tp ? tp->size : 1;
+    rank = tp ? tp->rank : 0;
+    if (nrk > 1) {
+        if (dim != 3) fail(SGML_EINVAL, "solve: multi-GPU solves are 3D");
+        if (!compact()) fail(SGML_EINVAL, "solve: multi-GPU solves use the compact engine");
+        if (nrk & (nrk - 1)) fail(SGML_EINVAL, "solve: the number of ranks must be a power of two");
+        if (nrk > (1 << (n - 1))) fail(SGML_EINVAL, "solve: too many ranks for this grid (>= 2 planes each)");
+        T0 = (1 << n) / nrk;  // level-0 planes per rank (the last rank also owns plane N-1)
+        vrep = 0;
+        while ((T0 >> vrep) >= 2) ++vrep;  // levels v < vrep hold >= 2 planes per rank
+    }
+
     if (compact()) {
         Lv.resize(n);
-        for (int v = 0; v < n; ++v) Lv[v] = make_ext(dim, Nl[v]);
-        // nodes off the Dirichlet faces, per level; face values
+        for (int v = 0; v < n; ++v) {
+            if (dist(v)) {
+                int kb, cnt;
+                own_planes(v, rank, kb, cnt);
+                Lv[v] = make_ext(dim, Nl[v], kb, cnt);
+            } else {
+                Lv[v] = make_ext(dim, Nl[v]);
+            }
+        }
+        // nodes off the Dirichlet faces, per level (local z indices); face values
         rng.assign(n, NodeRange{});
         for (int v = 0; v < n; ++v)
             for (int ax = 0; ax < 3; ++ax) {
                 const bool live = ax < dim;
                 rng[v].lo[ax] = live && bc_host.kind[2 * ax] == 0 ? 1 : 0;
                 rng[v].hi[ax] = !live ? 0 : (bc_host.kind[2 * ax + 1] == 0 ? Nl[v] - 2 : Nl[v] - 1);
+                if (live && ax == 2 && dist(v)) {
+                    const ExtLay& L = Lv[v];
+                    rng[v].lo[2] = (bc_host.kind[4] == 0 && L.z0 == 0) ? 1 : 0;
+                    rng[v].hi[2] = (bc_host.kind[5] == 0 && L.z0 + L.Nz == Nl[v]) ? L.Nz - 2 : L.Nz - 1;
+                }
             }
         for (int f = 0; f < 2 * dim; ++f)
             if (bc_host.kind[f] == 0) {
@@ -334,6 +361,7 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
         A = alloc(E0);
         B = alloc(E0);
         dense = alloc(T);
+        if (nrk > 1 && vrep < n) BS = alloc(ext_size(dim, Lv[vrep]));
         P.assign(n, nullptr);
         for (int m = 1; m < n; ++m) P[m] = alloc(ext_size(dim, Lv[m]));
         U.assign(n, {nullptr, nullptr});
@@ -421,6 +449,71 @@ void sgml_solver::set_faces(double* p, int level, int st) {
     fstate[p] = st;
 }
 
+// ---------------------------------------------------------------------------
+// z-slab decomposition helpers
+// ---------------------------------------------------------------------------
+
+// rank p's planes of level v: T0 >> v each, the last rank also the plane N-1
+// (levels >= vrep hold one plane per rank in this sizing)
+void sgml_solver::own_planes(int v, int p, int& kb, int& cnt) const {
+    const int t = std::max(1, T0 >> v);
+    kb = p * t;
+    cnt = t + (p == nrk - 1 ? 1 : 0);
+}
+
+void sgml_solver::halo(double* a, int v) {
+    if (!dist(v)) return;
+    tp->halo(a, Lv[v].plane, Lv[v].Nz, d_flag, ctx->stream);
+}
+
+// a replicated level array whose planes were produced rank by rank (own
+// planes, own_planes sizing) -> every rank holds all of them.  The z ghost
+// planes are the even mirrors of planes 1 and N-2 (whichever rank wrote
+// them), so every rank rebuilds them from its gathered copy.
+void sgml_solver::gather_level(double* a, int v) {
+    if (nrk == 1) return;
+    const long long pl = Lv[v].plane;
+    std::vector<long long> off(nrk), cnt(nrk);
+    for (int p = 0; p < nrk; ++p) {
+        int kb, c;
+        own_planes(v, p, kb, c);
+        off[p] = (kb + 1) * pl;
+        cnt[p] = (long long)c * pl;
+    }
+    tp->allgather(a, off, cnt, ctx->stream);
+    const int N = Nl[v];
+    const size_t bytes = (size_t)pl * sizeof(double);
+    SGML_CUDA(cudaMemcpyAsync(a, a + 2 * pl, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    SGML_CUDA(cudaMemcpyAsync(a + (N + 1) * pl, a + (N - 1) * pl, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+// base (level 0, z-slab) sampled on level vrep, replicated on every rank
+void sgml_solver::refresh_bs(const double* base) {
+    int kb, cnt;
+    own_planes(vrep, rank, kb, cnt);
+    launch(SGML_CLASS_OTHER, [&] { launch_sample_ext(base, Lv[0], BS, Lv[vrep], vrep, kb, kb + cnt, ctx->stream); });
+    gather_level(BS, vrep);
+    bs_valid = true;
+}
+
+// one restriction-pyramid step level m -> m+1 (also for sigma)
+void sgml_solver::pyramid_step(const double* in, int m, double* out) {
+    const int dim = g.dim;
+    const cudaStream_t s = ctx->stream;
+    if (dist(m + 1)) {
+        launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid_ext(dim, in, Lv[m], out, Lv[m + 1], s); });
+        halo(out, m + 1);
+    } else if (dist(m)) {
+        // first replicated level: own planes from the slab, then all-gather
+        int kb, cnt;
+        own_planes(m + 1, rank, kb, cnt);
+        launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid_ext(dim, in, Lv[m], out, Lv[m + 1], s, kb, kb + cnt); });
+        gather_level(out, m + 1);
+    } else {
+        launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid_ext(dim, in, Lv[m], out, Lv[m + 1], s); });
+    }
+}
+
 // cycle.cpp:117-133: sigma restricted per level with even (all-Neumann)
 // ghosts; every level must stay positive.  The compact engine keeps level v
 // only on its subset nodes (pyramid); positivity is checked on
@@ -433,8 +526,8 @@ void sgml_solver::load_sigma(const double* sigma_dense) {
     if (compact()) {
         launch(SGML_CLASS_OTHER, [&] { launch_check_positive(sigma_dense, T, d_flag, s); });
         launch(SGML_CLASS_OTHER, [&] { launch_scatter_ext(dim, sigma_dense, S[0], Lv[0], s); });
-        for (int m = 1; m < n; ++m)
-            launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid_ext(dim, S[m - 1], Lv[m - 1], S[m], Lv[m], s); });
+        halo(S[0], 0);
+        for (int m = 1; m < n; ++m) pyramid_step(S[m - 1], m - 1, S[m]);
     } else {
         sgml_bc even{};
         for (int f = 0; f < 6; ++f) even.kind[f] = 1;
@@ -476,6 +569,7 @@ void sgml_solver::load_source(const double* f) {
     const cudaStream_t s = ctx->stream;
     if (compact()) {
         launch(SGML_CLASS_OTHER, [&] { launch_scatter_ext(g.dim, f, r, Lv[0], s); });
+        halo(r, 0);
         fstate[r] = FS_OTHER;
     }
     else
@@ -485,6 +579,17 @@ void sgml_solver::load_source(const double* f) {
 const double* sgml_solver::dense_view(const double* field) {
     if (!compact()) return field;
     launch(SGML_CLASS_OTHER, [&] { launch_gather_ext(g.dim, field, Lv[0], dense, ctx->stream); });
+    if (dist(0)) {  // every rank's planes of the dense field
+        const long long pl = (long long)g.N * g.N;
+        std::vector<long long> off(nrk), cnt(nrk);
+        for (int p = 0; p < nrk; ++p) {
+            int kb, c;
+            own_planes(0, p, kb, c);
+            off[p] = kb * pl;
+            cnt[p] = c * pl;
+        }
+        tp->allgather(dense, off, cnt, ctx->stream);
+    }
     return dense;
 }
 
@@ -532,6 +637,7 @@ void sgml_solver::residual(const double* e) {
         tm.s = has_sigma ? umap(S[0]) : tm.u;
         tm.t = gmap(utot);
         launch(SGML_CLASS_RESIDUAL, [&] { launch_residual_tma(dim, has_sigma, tm, r, utot, Lv[0], rng[0], rc0, d_rmax, d_flag, s); });
+        halo(r, 0);  // the next cycle's pyramid reads r across the slab faces
     } else {
         const double inv_h2 = 1.0 / (g.h * g.h);
         const double pref = dim == 2 ? 0.5 : 3.0 / 13.0;
@@ -551,6 +657,7 @@ const double* sgml_solver::cycle(bool homogeneous) {
 }
 
 void sgml_solver::cycle_dense(const double* src_dense, double* out_dense, bool homogeneous) {
+    if (nrk > 1) fail(SGML_EINVAL, "single_cycle: single-GPU only");
     load_source(src_dense);
     const double* e = cycle(homogeneous);
     if (compact()) {
@@ -573,13 +680,11 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
     // flag[1]: some level array of this cycle holds a nonzero value below
     // 2^-969 (relax passes then keep the unfused edge terms); every level
     // array of a cycle is produced within it, Dirichlet values included
-    SGML_CUDA(cudaMemsetAsync(flag + 1, 0, sizeof(int), s));
+    // flag[2], flag[3]: the neighbours' flag[1] (multi-GPU, sent with the halos)
+    SGML_CUDA(cudaMemsetAsync(flag + 1, 0, 3 * sizeof(int), s));
     if (!homogeneous && bval_tiny) SGML_CUDA(cudaMemsetAsync(flag + 1, 1, 1, s));
     // restriction pyramid of the cycle's source (once per cycle, F4)
-    for (int m = 0; m + 1 < n; ++m)
-        launch(SGML_CLASS_PYRAMID, [&] {
-            launch_pyramid_ext(dim, m == 0 ? r : P[m], Lv[m], P[m + 1], Lv[m + 1], s);
-        });
+    for (int m = 0; m + 1 < n; ++m) pyramid_step(m == 0 ? r : P[m], m, P[m + 1]);
     auto gsrc = [&](int v) { return v == 0 ? (const double*)r : (const double*)P[v]; };
 
     int slot = 0;
@@ -612,10 +717,25 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                 launch_relax_tma(dim, has_sigma, tm, out, duo, Lv[v], rng[v], rc, diag + slot, flag, s);
             });
             ++slot;
+            halo(out, v);  // z-slab levels: the next consumer reads across the slab faces
+            if (duo) halo(duo, v);
             cur = out;
             first = false;
         }
         return cur;
+    };
+    // replicated targets read the base from its replicated level-vrep sample
+    bs_valid = false;
+    auto base_src = [&](int w, const double*& bp, ExtLay& bl, int& wb) {
+        bp = base;
+        bl = Lv[0];
+        wb = 0;
+        if (nrk > 1 && !dist(w) && !base_zero) {
+            if (!bs_valid) refresh_bs(base);
+            bp = BS;
+            bl = Lv[vrep];
+            wb = vrep;
+        }
     };
 
     for (int v1 = n - 1; v1 >= 0; --v1) {
@@ -634,10 +754,12 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                     // fold the pending increments into a full-grid base
                     const ChainEntry* ch = chain_at();
                     launch(SGML_CLASS_MATERIALIZE, [&] {
-                        launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], base_zero, ufinal, Lv[v + 1],
+                        launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lv[v + 1],
                                             v + 1, ch, count, bc, homogeneous, flag, s);
                     });
                     fstate[other] = face_want(homogeneous);
+                    halo(other, 0);
+                    bs_valid = false;
                     std::swap(base, other);
                     base_zero = false;
                     start += count;
@@ -646,11 +768,16 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                 }
                 const ChainEntry* ch = chain_at();
                 const ExtLay Lf = v + 1 < n ? Lv[v + 1] : Lv[v];
+                const double* bp;
+                ExtLay bl;
+                int wb;
+                base_src(v, bp, bl, wb);
                 launch(SGML_CLASS_MATERIALIZE, [&] {
-                    launch_materialize4(dim, in, Lv[v], v, base, Lv[0], base_zero, ufinal, Lf, 1, ch, count, bc,
+                    launch_materialize4(dim, in, Lv[v], v, bp, bl, wb, base_zero, ufinal, Lf, 1, ch, count, bc,
                                         homogeneous, flag, s);
                 });
                 fstate[in] = face_want(homogeneous);
+                halo(in, v);
             }
             ufinal = relax_level(v, in, c, U[v][0], U[v][1]);
             count += c - 1;
@@ -665,10 +792,11 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
             const ChainEntry* ch = chain_at();
             const ExtLay Lf = n > 1 ? Lv[1] : Lv[0];
             launch(SGML_CLASS_MATERIALIZE, [&] {
-                launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], base_zero, ufinal, Lf, 1, ch, count, bc,
+                launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lf, 1, ch, count, bc,
                                     homogeneous, flag, s);
             });
             fstate[other] = face_want(homogeneous);
+            halo(other, 0);
             in0 = other;
         } else {
             in0 = base;
@@ -676,6 +804,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
         base = relax_level(0, in0, c, A, B);
         other = base == A ? B : A;
         base_zero = false;
+        bs_valid = false;
     }
     // tail Relax(0, min(n_r, 2^n))
     base = relax_level(0, base, relax_count(n, cfg.n_r, 0), A, B);
@@ -738,7 +867,7 @@ void sgml_solver::pin_and_emit(double* u_out) {
     const cudaStream_t s = ctx->stream;
     const uint64_t T = g.total;
     double* res = compact() ? dense : utot;
-    if (compact()) launch(SGML_CLASS_OTHER, [&] { launch_gather_ext(g.dim, utot, Lv[0], dense, s); });
+    if (compact()) dense_view(utot);  // (every rank's planes in a multi-GPU solve)
     if (all_neumann && a == 0.0) {
         const double mean = trapezoid_mean_host(ctx, g, res);
         launch(SGML_CLASS_OTHER, [&] { launch_sub_scalar(res, T, mean, s); });
@@ -801,6 +930,7 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
         SGML_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
         const double* e = cycle(homogeneous);
         // kernel_error check before the recurrence touches u_tot and r
+        if (nrk > 1) tp->allreduce_max_i32(d_flag, 1, s);
         SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaStreamSynchronize(s));
         if (h_flag[0]) {
@@ -811,6 +941,9 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
         }
         residual(e);
         SGML_CUDA(cudaGetLastError());
+        // per-pass diag maxima and max|r| over the ranks (max is order-free:
+        // bit-identical to the single-GPU values)
+        if (nrk > 1) tp->allreduce_max_u64(d_cycle, n_slots + 1, s);
         SGML_CUDA(cudaMemcpyAsync(h_cycle, d_cycle, (n_slots + 1) * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaStreamSynchronize(s));

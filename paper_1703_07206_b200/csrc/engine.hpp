@@ -2,6 +2,7 @@
 #pragma once
 
 #include <array>
+#include <memory>
 #include <cstdlib>
 #include <cstdint>
 #include <mutex>
@@ -14,6 +15,7 @@
 #include "../../include/sgml_b200.h"
 #include "device.cuh"
 #include "internal.hpp"
+#include "transport.hpp"
 
 // ---- opaque C-ABI objects ----------------------------------------------
 struct sgml_ctx {
@@ -29,6 +31,8 @@ struct sgml_ctx {
     struct sgml_solver* cached = nullptr;
     std::string cached_key;
     std::mutex mu;
+    // multi-GPU clique this context belongs to (z-slab solves); null: single GPU
+    std::unique_ptr<sgmlb::Transport> tp;
 };
 
 struct sgml_field {
@@ -177,6 +181,22 @@ struct sgml_solver {
     void pin_and_emit(double* u_out_dev);                // pure_neumann_pin + result
     void ensure_literal();
     double* alloc(size_t count);
+
+    // z-slab decomposition (3D compact engine on a clique of nrk ranks,
+    // SURVEY.md §8e).  Level v < vrep is a z-slab per rank (own planes plus
+    // one halo plane each side, exchanged after every producer); levels
+    // v >= vrep are replicated (computed redundantly by every rank from
+    // replicated inputs).  nrk = 1: nothing is distributed.
+    sgmlb::Transport* tp = nullptr;
+    int nrk = 1, rank = 0, vrep = 0, T0 = 0;
+    bool dist(int v) const { return nrk > 1 && v < vrep; }
+    double* BS = nullptr;      // base sampled on level vrep (replicated), for replicated targets
+    bool bs_valid = false;
+    void halo(double* a, int v);                          // after a producer at a z-slab level
+    void gather_level(double* a, int v);                  // replicated level: own planes -> all
+    void own_planes(int v, int p, int& kb, int& cnt) const;  // rank p's planes of level v
+    void refresh_bs(const double* base);
+    void pyramid_step(const double* in, int m, double* out);
 
     // Dirichlet-face bookkeeping of the compact engine.  Relaxation and
     // residual kernels cover only the nodes off the Dirichlet faces

@@ -94,10 +94,15 @@ void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc
 // Materialise the level-w input of the next relax step from the tooth's
 // state: Dirichlet value, the finest relaxed level lf = w + frel (ufine) at
 // its subset nodes, or base + the pending increments chain[0..nchain).
+// base holds the level-wb subset (0: the level-0 array; a multi-GPU solve
+// passes the replicated level-vrep sample for replicated targets).
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
-                         const ExtLay& L0, bool base_zero, const double* ufine, const ExtLay& Lf,
+                         const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
                          int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
                          bool homogeneous, int* flag, cudaStream_t s);
+// 3D: out planes [kb, ke) (local) <- in at positions << shift (level subsample)
+void launch_sample_ext(const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout, int shift, int kb,
+                       int ke, cudaStream_t s);
 // Restriction pyramid step level m -> m+1, output planes
 // [kb, ke) (local; ke < 0: all planes of Lout).
 void launch_pyramid_ext(int dim, const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout,

@@ -43,7 +43,7 @@ constexpr int MBX = 32, MBY = 4;
 template <int DIM>
 __global__ void __launch_bounds__(MBX* MBY)
     k_materialize4(double* __restrict__ out, ExtLay Lw, int w, const double* __restrict__ base,
-                   ExtLay L0, int base_zero, const double* __restrict__ ufine, ExtLay Lf, int frel,
+                   ExtLay L0, int wb, int base_zero, const double* __restrict__ ufine, ExtLay Lf, int frel,
                    const ChainEntry* __restrict__ chain, int nchain, BcDev bc, int homogeneous,
                    int* flag) {
     __shared__ ChainEntry sch[kMaxChain];
@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(MBX* MBY)
 #pragma unroll
             for (int k = 0; k < MV; ++k)
                 val[cp][k] = (!base_zero && k < nv && cp < ncopy)
-                                 ? __ldg(base + eix<DIM>(L0, (X4 + k) << w, node_j(cp) << w, z - L0.z0))
+                                 ? __ldg(base + eix<DIM>(L0, (X4 + k) << (w - wb), node_j(cp) << (w - wb),
+                                                         (z >> wb) - L0.z0))
                                  : 0.0;
 
         for (int c = 0; c < nch; ++c) {
@@ -274,6 +275,17 @@ __global__ void __launch_bounds__(128) k_dirichlet_faces(double* a, ExtLay L, Bc
     else a[eix<DIM>(L, i, j, k)] = v;
 }
 
+// level-(shift) subsample of a level array: out (local planes [kb, kb +
+// gridDim.z)) <- in at the level-0-relative positions << shift
+__global__ void __launch_bounds__(128) k_sample_ext(const double* __restrict__ in, ExtLay Lin,
+                                                    double* __restrict__ out, ExtLay Lout, int shift, int kb) {
+    const int I = blockIdx.x * 32 + threadIdx.x, J = blockIdx.y * 4 + threadIdx.y;
+    const int K = kb + (int)blockIdx.z;
+    if (I >= Lout.N || J >= Lout.N) return;
+    const int kin = ((K + Lout.z0) << shift) - Lin.z0;
+    store_ext<3>(out, Lout, I, J, K, __ldg(in + eix<3>(Lin, I << shift, J << shift, kin)));
+}
+
 inline dim3 ext_grid(int dim, const ExtLay& L) {
     return dim3((L.N + 31) / 32, (L.N + 3) / 4, dim == 3 ? L.Nz : 1);
 }
@@ -296,17 +308,17 @@ uint64_t ext_size(int dim, const ExtLay& L) {
 }
 
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
-                         const ExtLay& L0, bool base_zero, const double* ufine, const ExtLay& Lf,
+                         const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
                          int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
                          bool homogeneous, int* flag, cudaStream_t s) {
     const int Nw = Lw.N;
     const int threads_x = (Nw + MV - 1) / MV, H = (Nw - 1) / 2;
     const dim3 grid((threads_x + MBX - 1) / MBX, (H + MBY) / MBY, dim == 3 ? Lw.Nz : 1);
     if (dim == 2)
-        k_materialize4<2><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, base_zero, ufine, Lf, frel,
+        k_materialize4<2><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, frel,
                                                           chain, nchain, bc, homogeneous, flag);
     else
-        k_materialize4<3><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, base_zero, ufine, Lf, frel,
+        k_materialize4<3><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, frel,
                                                           chain, nchain, bc, homogeneous, flag);
 }
 
@@ -340,6 +352,14 @@ void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc
         k_dirichlet_faces<2><<<dim3((N + 31) / 32, 1, 4), dim3(32, 4), 0, s>>>(a, L, bc, zero ? 1 : 0, mirrors ? 1 : 0);
     else
         k_dirichlet_faces<3><<<dim3((N + 31) / 32, (N + 3) / 4, 6), dim3(32, 4), 0, s>>>(a, L, bc, zero ? 1 : 0, mirrors ? 1 : 0);
+}
+
+void launch_sample_ext(const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout, int shift, int kb,
+                       int ke, cudaStream_t s) {
+    if (ke <= kb) return;
+    dim3 g = ext_grid(3, Lout);
+    g.z = ke - kb;
+    k_sample_ext<<<g, dim3(32, 4), 0, s>>>(in, Lin, out, Lout, shift, kb);
 }
 
 }  // namespace sgmlb

@@ -124,6 +124,13 @@ def solve_problem(name: str, n: int):
     if name == "mixed3d_a":
         g = O.make_grid(3, n)
         return g, bc("low_dir_high_neu"), O.fill("poisson3d", g), None, -0.3
+    if name == "neumann3d_a":
+        # all-Neumann 3D, a = 0.1, compatible cosine source
+        g = O.make_grid(3, n)
+        x = np.arange(g.N) * g.h
+        zz, yy, xx = np.meshgrid(x, x, x, indexing="ij")
+        f = (-3.0 * math.pi ** 2 * np.cos(math.pi * xx) * np.cos(math.pi * yy) * np.cos(math.pi * zz)).reshape(-1)
+        return g, bc("neumann"), f, None, 0.1
     if name == "sigma3d_dirichlet":
         g = O.make_grid(3, n)
         return g, bc("dir_distinct"), O.fill("poisson3d", g), sigma_field(g, 77), 0.0

@@ -1,0 +1,88 @@
+"""Multi-GPU z-slab decomposition on one GPU: nranks in-process
+ranks (host threads, LocalGroup) solve the same problem; every rank's report
+and solution must equal the oracle's bit for bit, exactly as the single-GPU
+solve does (all reductions are maxima, so the decomposition cannot change a
+bit).  The NCCL transport shares this code path; only the plane copies differ."""
+import threading
+
+import pytest
+
+import cases as K
+from cases import O
+import paper_1703_07206_b200 as S
+
+pytestmark = pytest.mark.gpu
+
+
+def sgrid(g):
+    return S.make_grid(g.dim, g.n)
+
+
+def sbc_of(b):
+    return S.BoundarySpec([S.FaceBc(S.BcKind(b.kind[f]), b.value[f]) for f in range(6)])
+
+
+def solve_clique(name, n, nranks, n_r=2, max_cycles=40):
+    g, b, f, s, a = K.solve_problem(name, n)
+    group = S.LocalGroup(nranks)
+    out, err = [None] * nranks, [None] * nranks
+
+    def run(r):
+        try:
+            ctx = S.Context(0)
+            ctx.join_local(group, r)
+            assert ctx.clique() == (nranks, r)
+            prob = S.ProblemSpec(sgrid(g), f, bc=sbc_of(b), sigma=s, a=a)
+            out[r] = S.solve(prob, S.SolverConfig(n_r=n_r, tol=1e-10, max_cycles=max_cycles, safety=0.9),
+                             ctx=ctx)
+        except Exception as exc:  # surfaced below
+            err[r] = exc
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    assert all(not t.is_alive() for t in ts), "a rank hung"
+    for e in err:
+        if e is not None:
+            raise e
+    ref = O.solve(g, b, f, s, a, n_r=n_r, tol=1e-10, max_cycles=max_cycles)
+    return out, ref
+
+
+def check_same(res, ref):
+    rep = res.report
+    assert (rep.converged, rep.nan_detected, rep.stagnated) == (ref.converged, ref.nan_detected, ref.stagnated)
+    assert [(r.cycle, r.work_units, r.residual, r.diag_min) for r in rep.rows] == ref.rows
+    assert [(t.cycle, t.pass_, t.level, t.value) for t in rep.trace] == ref.trace
+    assert rep.normalization == ref.normalization
+    assert rep.node_updates == ref.node_updates
+    assert K.bits_equal(res.u, ref.u)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("nranks", [2, 4])
+@pytest.mark.parametrize("name,n", [("poisson3d", 5), ("capacitor_high", 4), ("mixed3d_a", 4),
+                                    ("sigma3d_dirichlet", 4), ("neumann3d_a", 4)])
+def test_slab_solve_bitwise(name, n, nranks):
+    out, ref = solve_clique(name, n, nranks)
+    for res in out:
+        check_same(res, ref)
+
+
+@pytest.mark.timeout(600)
+def test_slab_solve_eight_ranks_and_other_relax_counts():
+    out, ref = solve_clique("poisson3d", 4, 8)
+    for res in out:
+        check_same(res, ref)
+    out, ref = solve_clique("capacitor_low", 4, 2, n_r=3)
+    for res in out:
+        check_same(res, ref)
+
+
+def test_slab_plan_rejects_bad_cliques():
+    with pytest.raises(ValueError):
+        S.slab_plan(4, 3, 0)        # not a power of two
+    with pytest.raises(ValueError):
+        S.slab_plan(3, 8, 0)        # fewer than 2 planes per rank

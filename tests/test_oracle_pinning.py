@@ -143,6 +143,12 @@ def test_live_reference_single_cycle(n_r):
         for levels in (None, sig):
             a = O.single_cycle(g, K.bc(bcn), src, levels, 0.2, False, n_r, 0.9, 0, 1.0)
             b = O.single_cycle(g, K.bc(bcn), src, levels, 0.2, False, n_r, 0.9, 0, 1.0, impl="ref")
+            if b[0] == 3 and a[0] == 0 and K.BCS[bcn][0][2 * dim - 1] == K.NEU:
+                # SURVEY.md F5 (see test_live_reference_relax): the reference read
+                # past the end of du_prev and met non-finite garbage; heap-layout
+                # dependent, so only the restatement's finiteness is checked
+                assert np.isfinite(a[1]).all()
+                continue
             assert a[0] == b[0] and a[3] == b[3]
             assert K.bits_equal(a[1], b[1])
             assert [t[3] for t in a[2]] == [t[3] for t in b[2]]
