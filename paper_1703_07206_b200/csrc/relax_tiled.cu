@@ -44,45 +44,60 @@ enum { MODE_RELAX = 0, MODE_RESID = 1 };
 
 template <int DIM>
 struct Tile {
-    static constexpr int X = DIM == 3 ? 32 : 128;      // nodes per row (= threads in x)
+    static constexpr int XP = DIM == 3 ? 2 : 1;        // x nodes per thread (adjacent)
+    static constexpr int X = DIM == 3 ? 32 : 128;      // threads in x
+    static constexpr int NX = X * XP;                  // nodes per row
     static constexpr int TY = DIM == 3 ? 8 : 1;        // thread rows
     static constexpr int RT = DIM == 3 ? 2 : 1;        // node rows per thread
     static constexpr int ROWS = TY * RT;               // node rows per CTA
-    static constexpr int HXU = X + 4;                  // u / sigma box width (halo + alignment)
-    static constexpr int HXG = X + 2;                  // g / u_tot box width (alignment)
+    // box widths: 3D tiles start at even x (box = halo exactly); 2D tiles
+    // start at lo.x and carry the alignment offset xoff in {0, 1}
+    static constexpr int HXU = DIM == 3 ? NX + 2 : NX + 4;  // u / sigma box width
+    static constexpr int HXG = NX + 2;                      // g / u_tot box width
     static constexpr int HY = DIM == 3 ? ROWS + 2 : 1;
     static constexpr int PLANE = HXU * HY;             // u / sigma box (tile + halo)
     static constexpr int GBOX = HXG * ROWS;            // g / u_tot box (tile rows)
     static constexpr int THREADS = X * TY;
     static constexpr int NWARPS = THREADS / 32;
     static constexpr int WR = DIM == 3 ? RT + 2 : 1;   // window rows per plane
-    static constexpr int NST = 8;                      // ring depth (planes), power of two
-    static constexpr int LEAD = NST - 3;               // step m issues plane m + LEAD
+    static constexpr int WC = XP + 2;                  // window columns per row
     static constexpr int PLANE_AL = (PLANE + 15) / 16 * 16;  // slots 128-byte aligned
     static constexpr int GBOX_AL = (GBOX + 15) / 16 * 16;
 };
 
+// ring depth (planes) and producer lead: 3D relax passes keep two CTAs per
+// SM in 2 x 107 KB; the residual pass (one more stream) uses a shallower ring
+template <int DIM, bool SIG, int MODE>
+struct Ring {
+    static constexpr int NST = DIM == 2 ? 8 : (MODE == MODE_RESID && !SIG ? 4 : 6);
+    static constexpr int LEAD = NST - 3 > 1 ? NST - 3 : NST - 2;  // step q issues plane q + LEAD
+};
+
 template <int DIM, bool SIG, int MODE>
 struct __align__(128) TRing {
-    double u[Tile<DIM>::NST][Tile<DIM>::PLANE_AL];
-    double g[Tile<DIM>::NST][Tile<DIM>::GBOX_AL];
-    double s[SIG ? Tile<DIM>::NST : 1][SIG ? Tile<DIM>::PLANE_AL : 16];
-    double t[MODE == MODE_RESID ? Tile<DIM>::NST : 1][MODE == MODE_RESID ? Tile<DIM>::GBOX_AL : 16];
-    unsigned long long full[Tile<DIM>::NST];
-    unsigned long long empty[Tile<DIM>::NST];
+    static constexpr int NST = Ring<DIM, SIG, MODE>::NST;
+    double u[NST][Tile<DIM>::PLANE_AL];
+    double g[NST][Tile<DIM>::GBOX_AL];
+    double s[SIG ? NST : 1][SIG ? Tile<DIM>::PLANE_AL : 16];
+    double t[MODE == MODE_RESID ? NST : 1][MODE == MODE_RESID ? Tile<DIM>::GBOX_AL : 16];
+    unsigned long long full[NST];
+    unsigned long long empty[NST];
 };
 
 template <int DIM>
-using Win = double[Tile<DIM>::WR][3];
+using Win = double[Tile<DIM>::WR][Tile<DIM>::WC];
 template <int DIM, bool SIG>
-using SWin = double[SIG ? Tile<DIM>::WR : 1][SIG ? 3 : 1];
+using SWin = double[SIG ? Tile<DIM>::WR : 1][SIG ? Tile<DIM>::WC : 1];
+template <int DIM>
+using NodeD = double[Tile<DIM>::RT][Tile<DIM>::XP];
 
 // MODE_RELAX:  uo <- relaxed u (with mirror ghosts), duo <- u - u_prev (DUO),
 //              tm_g = source g, diag_slot <- max |A(u)+a u - g| over the range.
 // MODE_RESID:  tm_u = e, tm_g = r, uo = r (updated in place: r -= A(e) + a e),
 //              tm_t / duo = u_tot (+= e, DUO), diag_slot <- max|r|
 //              (kernels.cpp:407-415; r is 0 on Dirichlet faces).
-// Range: data nodes [lo.x, hi.x] x [lo.y, hi.y] x [lo.z, hi.z] (2D: x, y).
+// Range: data nodes [lo.x, hi.x] x [lo.y, hi.y] x [lo.z, hi.z] (2D: x, y),
+// z indices local to the array (z-slabs).
 template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO>
 __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) : 4)
     k_relax_tma(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_g,
@@ -90,7 +105,8 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                 double* uo, double* duo, ExtLay L, int3 lo, int3 hi, int zb, RelaxConst rc,
                 unsigned long long* diag_slot, int* flag) {
     using TL = Tile<DIM>;
-    constexpr int NST = TL::NST, RT = TL::RT, WR = TL::WR;
+    constexpr int NST = Ring<DIM, SIG, MODE>::NST, LEAD = Ring<DIM, SIG, MODE>::LEAD;
+    constexpr int RT = TL::RT, WR = TL::WR, XP = TL::XP, WC = TL::WC;
     constexpr bool RESID = MODE == MODE_RESID;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TRing<DIM, SIG, MODE>& R = *reinterpret_cast<TRing<DIM, SIG, MODE>*>(smem_raw);
@@ -99,29 +115,34 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     const int tid = tx + TL::X * ty;
     const int lane = tid & 31, warp = tid >> 5;
     const int N = L.N;
-    const int x0 = lo.x + blockIdx.x * TL::X;
+    const int x0 = (DIM == 3 ? (lo.x & ~1) : lo.x) + blockIdx.x * TL::NX;
     const int y0 = DIM == 3 ? lo.y + blockIdx.y * TL::ROWS : 0;
     const int zlo = DIM == 3 ? lo.z : lo.y, zhi = DIM == 3 ? hi.z : hi.y;  // marching axis
     const int m0 = zlo + blockIdx.z * zb;
     const int mend = min(m0 + zb, zhi + 1);  // exclusive
     const int xb = x0 & ~1;                   // box start cell (ext index of data x0 - 1 is x0)
-    const int xoff = x0 - xb;
-    const int xi = x0 + tx;
-    const int yb = y0 + ty * RT;  // first node row of this thread (3D)
-    bool ok[RT];
+    const int xoff = x0 - xb;                 // 0 in 3D
+    const int xi = x0 + tx * XP;              // first node column of this thread
+    const int yb = y0 + ty * RT;              // first node row of this thread (3D)
+    bool ok[RT][XP];
 #pragma unroll
-    for (int a = 0; a < RT; ++a) ok[a] = xi <= hi.x && (DIM == 2 || yb + a <= hi.y);
+    for (int a = 0; a < RT; ++a)
+#pragma unroll
+        for (int b = 0; b < XP; ++b)
+            ok[a][b] = xi + b >= lo.x && xi + b <= hi.x && (DIM == 2 || yb + a <= hi.y);
 
-    // per-row output offsets at plane m = -1 (advanced by one plane per step)
-    // and whether the row's nodes have mirror ghost cells in x / y
+    // output offset of node (0, 0) at plane m = -1 (advanced one plane per
+    // step) and whether the nodes have mirror ghost cells in x / y
     ptrdiff_t opos = DIM == 3 ? eix<DIM>(L, xi, yb, -1) : (ptrdiff_t)(xi + 1);
     const ptrdiff_t ostep = DIM == 3 ? (ptrdiff_t)L.plane : (ptrdiff_t)L.Px;
-    bool mir_row[RT];
+    bool mir[RT][XP];
 #pragma unroll
-    for (int a = 0; a < RT; ++a) {
-        const int j = yb + a;
-        mir_row[a] = xi == 1 || xi == N - 2 || (DIM == 3 && (j == 1 || j == N - 2));
-    }
+    for (int a = 0; a < RT; ++a)
+#pragma unroll
+        for (int b = 0; b < XP; ++b) {
+            const int i = xi + b, j = yb + a;
+            mir[a][b] = i == 1 || i == N - 2 || (DIM == 3 && (j == 1 || j == N - 2));
+        }
 
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
@@ -139,7 +160,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     // producer (one lane): plane m -> slot; waits for the slot's previous use
     auto issue = [&](int m) {
         const unsigned p = (unsigned)(m - m0 + 1);
-        const unsigned s = p & (NST - 1), k = p / NST;
+        const unsigned s = p % NST, k = p / NST;
         if (k > 0) mbar_wait_u32(a_empty + 8 * s, (k - 1) & 1);
         const bool comp = m >= m0 && m < mend;
         const unsigned bytes = BU + (SIG ? BU : 0u) + (comp ? BG + (DUO && RESID ? BG : 0u) : 0u);
@@ -161,39 +182,44 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             }
         }
     };
-    auto slot_of = [&](int m) { return (unsigned)(m - m0 + 1) & (NST - 1); };
-    auto wait_plane = [&](int m) {
-        const unsigned p = (unsigned)(m - m0 + 1);
-        mbar_wait_u32(a_full + 8 * (p & (NST - 1)), (p / NST) & 1);
-    };
-    auto release = [&](int m) {
+    auto release = [&](unsigned slot) {
         __syncwarp();
-        if (lane == 0) mbar_arrive_u32(a_empty + 8 * slot_of(m));
+        if (lane == 0) mbar_arrive_u32(a_empty + 8 * slot);
     };
 
-    const int wbase = tx + xoff + TL::HXU * (DIM == 3 ? ty * RT : 0);  // window origin in the u box
-    const int gbase = tx + 1 + xoff + TL::HXG * (DIM == 3 ? ty * RT : 0);
-    auto read_plane = [&](int m, Win<DIM>& P, SWin<DIM, SIG>& Ps) {
-        const unsigned slot = slot_of(m);
+    const int wbase = tx * XP + xoff + TL::HXU * (DIM == 3 ? ty * RT : 0);  // window origin in the u box
+    const int gbase = tx * XP + 1 + xoff + TL::HXG * (DIM == 3 ? ty * RT : 0);
+    auto read_plane = [&](unsigned slot, Win<DIM>& P, SWin<DIM, SIG>& Ps) {
 #pragma unroll
-        for (int w = 0; w < WR; ++w)
+        for (int w = 0; w < WR; ++w) {
+            const double* row = &R.u[slot][wbase + TL::HXU * w];
+            if constexpr (XP == 2) {
+                // 16-byte aligned pairs: box columns 2 tx .. 2 tx + 3
+                const double2 lo2 = *reinterpret_cast<const double2*>(row);
+                const double2 hi2 = *reinterpret_cast<const double2*>(row + 2);
+                P[w][0] = lo2.x; P[w][1] = lo2.y; P[w][2] = hi2.x; P[w][3] = hi2.y;
+            } else {
 #pragma unroll
-            for (int p = 0; p < 3; ++p) {
-                P[w][p] = R.u[slot][wbase + p + TL::HXU * w];
-                if constexpr (SIG) Ps[w][p] = R.s[slot][wbase + p + TL::HXU * w];
+                for (int c = 0; c < WC; ++c) P[w][c] = row[c];
             }
+            if constexpr (SIG) {
+                const double* srow = &R.s[slot][wbase + TL::HXU * w];
+#pragma unroll
+                for (int c = 0; c < WC; ++c) Ps[w][c] = srow[c];
+            }
+        }
     };
 
     double dmax = 0.0;
     unsigned badhi = 0;             // max exponent field of the produced values
     unsigned tinymin = 0xffffffffu;  // see finish(): tiny nonzero outputs
 
-    // the RT nodes' terms of one stencil plane (offset dr), interleaved term
-    // by term so the independent accumulation chains overlap; the first
-    // term starts the chain (0 + t differs from t only in the sign of zero)
-    auto plane_terms = [&](double (&acc)[RT], double (&smax)[RT], const Win<DIM>& P,
-                           const SWin<DIM, SIG>& Ps, const double (&uc)[RT], const double (&sc)[RT],
-                           int dr, bool fm) {
+    // the thread's RT x XP nodes' terms of one stencil plane (offset dr),
+    // interleaved term by term so the independent accumulation chains
+    // overlap; the first term starts the chain (0 + t differs from t only
+    // in the sign of zero)
+    auto plane_terms = [&](NodeD<DIM>& acc, NodeD<DIM>& smax, const Win<DIM>& P, const SWin<DIM, SIG>& Ps,
+                           const NodeD<DIM>& uc, const NodeD<DIM>& sc, int dr, bool fm) {
 #pragma unroll
         for (int q = (DIM == 3 ? -1 : 0); q <= (DIM == 3 ? 1 : 0); ++q)
 #pragma unroll
@@ -202,28 +228,30 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                 const int l2 = dr * dr + q * q + p * p;
                 const bool first = dr == -1 && q == (DIM == 3 ? -1 : 0) && p == -1;
 #pragma unroll
-                for (int a = 0; a < RT; ++a) {
-                    const int w = DIM == 3 ? a + q + 1 : 0;
-                    double sbar = 1.0;
-                    if constexpr (SIG) {
-                        sbar = 0.5 * (Ps[w][p + 1] + sc[a]);
-                        smax[a] = first ? sbar : (smax[a] < sbar ? sbar : smax[a]);
+                for (int a = 0; a < RT; ++a)
+#pragma unroll
+                    for (int b = 0; b < XP; ++b) {
+                        const int w = DIM == 3 ? a + q + 1 : 0, c = b + p + 1;
+                        double sbar = 1.0;
+                        if constexpr (SIG) {
+                            sbar = 0.5 * (Ps[w][c] + sc[a][b]);
+                            smax[a][b] = first ? sbar : (smax[a][b] < sbar ? sbar : smax[a][b]);
+                        }
+                        if (!SIG && fm && l2 == 2 && !first) {
+                            // edge: (d * 0.5) is exact for these inputs, so the fused
+                            // multiply-add rounds once exactly like acc + (d * 0.5)
+                            acc[a][b] = fma(P[w][c] - uc[a][b], 0.5, acc[a][b]);
+                        } else {
+                            const double t = stencil_t<SIG>(sbar, P[w][c], uc[a][b], l2);
+                            acc[a][b] = first ? t : acc[a][b] + t;
+                        }
                     }
-                    if (!SIG && fm && l2 == 2 && !first) {
-                        // edge: (d * 0.5) is exact for these inputs, so the fused
-                        // multiply-add rounds once exactly like acc + (d * 0.5)
-                        acc[a] = fma(P[w][p + 1] - uc[a], 0.5, acc[a]);
-                    } else {
-                        const double t = stencil_t<SIG>(sbar, P[w][p + 1], uc[a], l2);
-                        acc[a] = first ? t : acc[a] + t;
-                    }
-                }
             }
     };
 
     // finish one node: op, diag / residual, Euler step, store
-    auto finish = [&](int m, int a, bool mir_m, double acc, double smax, double uc, double gc, double tc) {
-        const ptrdiff_t pos = opos + (DIM == 3 ? a * (ptrdiff_t)L.Px : 0);
+    auto finish = [&](int m, int a, int b, bool mir_m, double acc, double smax, double uc, double gc, double tc) {
+        const ptrdiff_t pos = opos + (DIM == 3 ? a * (ptrdiff_t)L.Px : 0) + b;
         const double op = (acc * rc.pref) * rc.inv_s2;
         double value;
         if constexpr (RESID) {
@@ -255,68 +283,84 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             if (DUO) duo[pos] = value - uc;
         }
         uo[pos] = value;
-        if (mir_row[a] || mir_m)
-            store_mirrors<DIM>(uo, L, xi, DIM == 3 ? yb + a : m, DIM == 3 ? m : 0, value);
+        if (mir[a][b] || mir_m)
+            store_mirrors<DIM>(uo, L, xi + b, DIM == 3 ? yb + a : m, DIM == 3 ? m : 0, value);
     };
 
     // Streaming march: the reference sums a node's terms plane by plane
     // (dr = -1, 0, +1), so when plane q arrives the nodes of plane q get
     // their dr = -1 and dr = 0 terms and the nodes of plane q-1 their dr = +1
-    // terms.  Only two window planes are live (registers for addressing
-    // instead of a third window).
+    // terms.  Only two window planes are live.  The ring position of plane
+    // q (slot, phase) is carried from step to step.
     Win<DIM> X, Y;  // planes q-1 / q, alternating roles
     SWin<DIM, SIG> Xs, Ys;
-    double acc[RT], smax[RT];  // partial chains of the nodes of the newest plane
+    NodeD<DIM> acc, smax;  // partial chains of the nodes of the newest plane
 
     if (m0 < mend) {
         if (tid == 0)
-            for (int q = m0 - 1; q <= mend && q <= m0 + TL::LEAD; ++q) issue(q);
-        wait_plane(m0 - 1);
-        read_plane(m0 - 1, X, Xs);
-        release(m0 - 1);
+            for (int q = m0 - 1; q <= mend && q <= m0 + LEAD; ++q) issue(q);
+        mbar_wait_u32(a_full, 0);  // plane m0 - 1: slot 0, phase 0
+        read_plane(0, X, Xs);
+        release(0);
         opos += (ptrdiff_t)m0 * ostep;  // plane m0 - 1
+        unsigned sq = 1, ph = 0;         // ring slot / phase of plane q = m0
+        int pcount = warp;               // steps until this warp issues (rotating producer)
 
-        // plane q arrives in B (A holds plane q - 1)
+        // plane q arrives in B (A holds plane q - 1, in ring slot sp)
         auto step = [&](int q, Win<DIM>& A, Win<DIM>& B, SWin<DIM, SIG>& As, SWin<DIM, SIG>& Bs,
                         bool fm) {
-            // rotating producer: plane q + LEAD (the prologue issued up to m0 + LEAD);
-            // its slot held plane q + LEAD - NST, released in step q + LEAD - NST + 1
-            if (warp == ((q - m0) & (TL::NWARPS - 1)) && lane == 0 && q > m0 && q + TL::LEAD <= mend)
-                issue(q + TL::LEAD);
-            wait_plane(q);
-            read_plane(q, B, Bs);
+            // rotating producer: warp (q - m0) % NWARPS issues plane q + LEAD (the
+            // prologue issued up to m0 + LEAD); its slot held plane q + LEAD - NST,
+            // released in step q + LEAD - NST + 1
+            if (pcount == 0) {
+                if (lane == 0 && q > m0 && q + LEAD <= mend) issue(q + LEAD);
+                pcount = TL::NWARPS;
+            }
+            --pcount;
+            const unsigned sp = sq == 0 ? NST - 1 : sq - 1;
+            mbar_wait_u32(a_full + 8 * sq, ph);
+            read_plane(sq, B, Bs);
             if (q > m0) {  // nodes of plane q - 1: dr = +1 terms, then the update
                 const int m = q - 1;
-                const unsigned sm = slot_of(m);
                 opos += ostep;
-                double uc[RT], sc[RT], gc[RT], tc[RT];
+                NodeD<DIM> uc, sc, gc, tc;
 #pragma unroll
-                for (int a = 0; a < RT; ++a) {
-                    const int gi = gbase + TL::HXG * a;  // node in the g box
-                    gc[a] = R.g[sm][gi];
-                    tc[a] = (DUO && RESID) ? R.t[sm][gi] : 0.0;
-                    uc[a] = A[DIM == 3 ? a + 1 : 0][1];
-                    sc[a] = 1.0;
-                    if constexpr (SIG) sc[a] = As[DIM == 3 ? a + 1 : 0][1];
-                }
+                for (int a = 0; a < RT; ++a)
+#pragma unroll
+                    for (int b = 0; b < XP; ++b) {
+                        const int gi = gbase + TL::HXG * a + b;  // node in the g box
+                        gc[a][b] = R.g[sp][gi];
+                        tc[a][b] = (DUO && RESID) ? R.t[sp][gi] : 0.0;
+                        uc[a][b] = A[DIM == 3 ? a + 1 : 0][b + 1];
+                        sc[a][b] = 1.0;
+                        if constexpr (SIG) sc[a][b] = As[DIM == 3 ? a + 1 : 0][b + 1];
+                    }
                 plane_terms(acc, smax, B, Bs, uc, sc, 1, fm);
                 const int mg = DIM == 3 ? m + L.z0 : m;  // global plane
                 const bool mir_m = mg == 1 || mg == N - 2;
 #pragma unroll
                 for (int a = 0; a < RT; ++a)
-                    if (ok[a]) finish(m, a, mir_m, acc[a], smax[a], uc[a], gc[a], tc[a]);
-                release(m);
+#pragma unroll
+                    for (int b = 0; b < XP; ++b)
+                        if (ok[a][b]) finish(m, a, b, mir_m, acc[a][b], smax[a][b], uc[a][b], gc[a][b], tc[a][b]);
+                release(sp);
             }
             if (q < mend) {  // nodes of plane q: dr = -1 and dr = 0 terms
-                double uc[RT], sc[RT];
+                NodeD<DIM> uc, sc;
 #pragma unroll
-                for (int a = 0; a < RT; ++a) {
-                    uc[a] = B[DIM == 3 ? a + 1 : 0][1];
-                    sc[a] = 1.0;
-                    if constexpr (SIG) sc[a] = Bs[DIM == 3 ? a + 1 : 0][1];
-                }
+                for (int a = 0; a < RT; ++a)
+#pragma unroll
+                    for (int b = 0; b < XP; ++b) {
+                        uc[a][b] = B[DIM == 3 ? a + 1 : 0][b + 1];
+                        sc[a][b] = 1.0;
+                        if constexpr (SIG) sc[a][b] = Bs[DIM == 3 ? a + 1 : 0][b + 1];
+                    }
                 plane_terms(acc, smax, A, As, uc, sc, -1, fm);
                 plane_terms(acc, smax, B, Bs, uc, sc, 0, fm);
+            }
+            if (++sq == NST) {
+                sq = 0;
+                ph ^= 1;
             }
         };
         // roles alternate each plane: period 2.  `fm` is a literal at both
@@ -380,17 +424,20 @@ void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, c
     const int3 hi = make_int3(rg.hi[0], rg.hi[1], rg.hi[2]);
     const int nx = rg.hi[0] - rg.lo[0] + 1, ny = rg.hi[1] - rg.lo[1] + 1, nz = rg.hi[2] - rg.lo[2] + 1;
     if (nx <= 0 || ny <= 0 || (dim == 3 && nz <= 0)) return;  // nothing off the Dirichlet faces
-    const int cols = dim == 3 ? ((nx + Tile<3>::X - 1) / Tile<3>::X) * ((ny + Tile<3>::ROWS - 1) / Tile<3>::ROWS)
-                              : (nx + Tile<2>::X - 1) / Tile<2>::X;
+    // 3D tiles start at the even column at or below lo.x (16-byte TMA boxes
+    // with the halo exactly); 2D tiles start at lo.x
+    const int nxt = dim == 3 ? rg.hi[0] - (rg.lo[0] & ~1) + 1 : nx;
+    const int tilesx = dim == 3 ? (nxt + Tile<3>::NX - 1) / Tile<3>::NX : (nxt + Tile<2>::NX - 1) / Tile<2>::NX;
+    const int cols = dim == 3 ? tilesx * ((ny + Tile<3>::ROWS - 1) / Tile<3>::ROWS) : tilesx;
     const int zb = relax_tiled_zb(dim, cols, dim == 3 ? nz : ny);
     dim3 grid, block;
     if (dim == 3) {
         using TL = Tile<3>;
-        grid = dim3((nx + TL::X - 1) / TL::X, (ny + TL::ROWS - 1) / TL::ROWS, (nz + zb - 1) / zb);
+        grid = dim3(tilesx, (ny + TL::ROWS - 1) / TL::ROWS, (nz + zb - 1) / zb);
         block = dim3(TL::X, TL::TY);
     } else {
         using TL = Tile<2>;
-        grid = dim3((nx + TL::X - 1) / TL::X, 1, (ny + zb - 1) / zb);
+        grid = dim3(tilesx, 1, (ny + zb - 1) / zb);
         block = dim3(TL::X, 1);
     }
     if (dim == 3) {
