@@ -124,25 +124,21 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     const int xoff = x0 - xb;                 // 0 in 3D
     const int xi = x0 + tx * XP;              // first node column of this thread
     const int yb = y0 + ty * RT;              // first node row of this thread (3D)
-    bool ok[RT][XP];
-#pragma unroll
-    for (int a = 0; a < RT; ++a)
-#pragma unroll
-        for (int b = 0; b < XP; ++b)
-            ok[a][b] = xi + b >= lo.x && xi + b <= hi.x && (DIM == 2 || yb + a <= hi.y);
-
-    // output offset of node (0, 0) at plane m = -1 (advanced one plane per
-    // step) and whether the nodes have mirror ghost cells in x / y
-    ptrdiff_t opos = DIM == 3 ? eix<DIM>(L, xi, yb, -1) : (ptrdiff_t)(xi + 1);
-    const ptrdiff_t ostep = DIM == 3 ? (ptrdiff_t)L.plane : (ptrdiff_t)L.Px;
-    bool mir[RT][XP];
+    // node (a, b) in range / with mirror ghost cells in x, y: bit a * XP + b
+    unsigned okm = 0, mirm = 0;
 #pragma unroll
     for (int a = 0; a < RT; ++a)
 #pragma unroll
         for (int b = 0; b < XP; ++b) {
             const int i = xi + b, j = yb + a;
-            mir[a][b] = i == 1 || i == N - 2 || (DIM == 3 && (j == 1 || j == N - 2));
+            if (i >= lo.x && i <= hi.x && (DIM == 2 || j <= hi.y)) okm |= 1u << (a * XP + b);
+            if (i == 1 || i == N - 2 || (DIM == 3 && (j == 1 || j == N - 2))) mirm |= 1u << (a * XP + b);
         }
+    constexpr unsigned ALL = (1u << (RT * XP)) - 1;
+
+    // output offset of node (0, 0) at plane m = -1 (advanced one plane per step)
+    ptrdiff_t opos = DIM == 3 ? eix<DIM>(L, xi, yb, -1) : (ptrdiff_t)(xi + 1);
+    const ptrdiff_t ostep = DIM == 3 ? (ptrdiff_t)L.plane : (ptrdiff_t)L.Px;
 
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
@@ -211,8 +207,10 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     };
 
     double dmax = 0.0;
-    unsigned badhi = 0;             // max exponent field of the produced values
-    unsigned tinymin = 0xffffffffu;  // see finish(): tiny nonzero outputs
+    // exponent fields of the produced values: max (== 0x7ff: non-finite) and
+    // min (< 54: |value| < 2^-969 or zero; zeros make the flag conservative,
+    // which only costs the fused edge terms)
+    unsigned emax = 0, emin = 0x7ff00000u;
 
     // the thread's RT x XP nodes' terms of one stencil plane (offset dr),
     // interleaved term by term so the independent accumulation chains
@@ -250,7 +248,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     };
 
     // finish one node: op, diag / residual, Euler step, store
-    auto finish = [&](int m, int a, int b, bool mir_m, double acc, double smax, double uc, double gc, double tc) {
+    auto finish = [&](int m, int a, int b, double acc, double smax, double uc, double gc, double tc) {
         const ptrdiff_t pos = opos + (DIM == 3 ? a * (ptrdiff_t)L.Px : 0) + b;
         const double op = (acc * rc.pref) * rc.inv_s2;
         double value;
@@ -275,16 +273,13 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                 value = HAS_A ? num / rc.denom1 : num;
             }
             dmax = dmax < diag ? diag : dmax;
-            const unsigned vhi = (unsigned)__double2hiint(value);
-            badhi = max(badhi, vhi & 0x7ff00000u);
-            // nonzero |value| < 2^-969 (exponent field < 54): key - 1 < 0x035fffff
-            const unsigned key = (vhi & 0x7fffffffu) | (__double2loint(value) != 0 ? 1u : 0u);
-            tinymin = min(tinymin, key - 1u);
+            const unsigned e = (unsigned)__double2hiint(value) & 0x7ff00000u;
+            emax = max(emax, e);
+            emin = min(emin, e);
             if (DUO) duo[pos] = value - uc;
         }
         uo[pos] = value;
-        if (mir[a][b] || mir_m)
-            store_mirrors<DIM>(uo, L, xi + b, DIM == 3 ? yb + a : m, DIM == 3 ? m : 0, value);
+        return value;
     };
 
     // Streaming march: the reference sums a node's terms plane by plane
@@ -337,12 +332,32 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                     }
                 plane_terms(acc, smax, B, Bs, uc, sc, 1, fm);
                 const int mg = DIM == 3 ? m + L.z0 : m;  // global plane
-                const bool mir_m = mg == 1 || mg == N - 2;
+                const unsigned mm = (mg == 1 || mg == N - 2) ? ALL : mirm;
+                NodeD<DIM> val;
+                if (okm == ALL) {  // (block-uniform except at the range edges)
 #pragma unroll
-                for (int a = 0; a < RT; ++a)
+                    for (int a = 0; a < RT; ++a)
 #pragma unroll
-                    for (int b = 0; b < XP; ++b)
-                        if (ok[a][b]) finish(m, a, b, mir_m, acc[a][b], smax[a][b], uc[a][b], gc[a][b], tc[a][b]);
+                        for (int b = 0; b < XP; ++b)
+                            val[a][b] = finish(m, a, b, acc[a][b], smax[a][b], uc[a][b], gc[a][b], tc[a][b]);
+                } else {
+#pragma unroll
+                    for (int a = 0; a < RT; ++a)
+#pragma unroll
+                        for (int b = 0; b < XP; ++b)
+                            val[a][b] = (okm >> (a * XP + b)) & 1u
+                                            ? finish(m, a, b, acc[a][b], smax[a][b], uc[a][b], gc[a][b], tc[a][b])
+                                            : 0.0;
+                }
+                if (mm & okm) {  // rare: nodes next to a face write their mirror ghosts
+#pragma unroll
+                    for (int a = 0; a < RT; ++a)
+#pragma unroll
+                        for (int b = 0; b < XP; ++b)
+                            if ((mm & okm) >> (a * XP + b) & 1u)
+                                store_mirrors<DIM>(uo, L, xi + b, DIM == 3 ? yb + a : m, DIM == 3 ? m : 0,
+                                                   val[a][b]);
+                }
                 release(sp);
             }
             if (q < mend) {  // nodes of plane q: dr = -1 and dr = 0 terms
@@ -383,8 +398,8 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     }
     block_max_commit(dmax, diag_slot);
     if (!RESID) {
-        warp_or_commit(badhi == 0x7ff00000u, flag);
-        warp_or_commit(tinymin < 0x035fffffu, flag + 1);
+        warp_or_commit(emax == 0x7ff00000u, flag);
+        warp_or_commit(emin < 0x03600000u, flag + 1);
     }
 }
 
