@@ -341,12 +341,16 @@ __device__ __noinline__ void store_mirrors(double* a, ExtLay L, int i, int j, in
                 if (ia | ib | ic) a[eix<DIM>(L, ci[ia], cj[ib], DIM == 3 ? ck[ic] - L.z0 : 0)] = v;
 }
 
+// store with the mirror ghosts: the x mirror (same row) inline, y / z
+// mirrors (rows / planes 1 and N-2, usually warp-uniform) out of line
 template <int DIM>
 __device__ __forceinline__ void store_ext(double* a, const ExtLay& L, int i, int j, int k, double v) {
-    a[eix<DIM>(L, i, j, k)] = v;
+    double* p = a + eix<DIM>(L, i, j, k);
+    *p = v;
     const int N = L.N, kg = DIM == 3 ? k + L.z0 : 0;
-    if (i == 1 || i == N - 2 || j == 1 || j == N - 2 || (DIM == 3 && (kg == 1 || kg == N - 2)))
-        store_mirrors<DIM>(a, L, i, j, k, v);
+    if (i == 1) p[-2] = v;
+    if (i == N - 2) p[2] = v;  // (both when N == 3)
+    if (j == 1 || j == N - 2 || (DIM == 3 && (kg == 1 || kg == N - 2))) store_mirrors<DIM>(a, L, i, j, k, v);
 }
 
 // ---- mbarrier / TMA (sm_90+; used on sm_100a) ------------------------------

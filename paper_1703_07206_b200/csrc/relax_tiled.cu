@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
         for (int b = 0; b < XP; ++b) {
             const int i = xi + b, j = yb + a;
             if (i >= lo.x && i <= hi.x && (DIM == 2 || j <= hi.y)) okm |= 1u << (a * XP + b);
-            if (i == 1 || i == N - 2 || (DIM == 3 && (j == 1 || j == N - 2))) mirm |= 1u << (a * XP + b);
+            if (DIM == 3 && (j == 1 || j == N - 2)) mirm |= 1u << (a * XP + b);  // (x mirrors inline)
         }
     constexpr unsigned ALL = (1u << (RT * XP)) - 1;
 
@@ -279,6 +279,10 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             if (DUO) duo[pos] = value - uc;
         }
         uo[pos] = value;
+        // x mirror ghost (same row)
+        const int i = xi + b;
+        if (i == 1) uo[pos - 2] = value;
+        if (i == N - 2) uo[pos + 2] = value;  // (both when N == 3)
         return value;
     };
 
