@@ -356,6 +356,8 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
                 bval_tiny = bval_tiny || (av != 0.0 && av < 0x1p-969);
             }
         const uint64_t E0 = ext_size(dim, Lv[0]);
+        // the interpolation kernels index level arrays with 32-bit offsets
+        if (E0 >= (1ULL << 31)) fail(SGML_EINVAL, "solve: grid too large for the compact engine (n <= 10 in 3D)");
         r = alloc(E0);
         utot = alloc(E0);
         A = alloc(E0);

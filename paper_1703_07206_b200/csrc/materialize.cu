@@ -93,20 +93,22 @@ __global__ void __launch_bounds__(MBX* MBY)
             const double wz[2] = {1.0 - fz, fz};
             const int nq = iy ? 2 : 1, nr = (DIM == 3 && iz) ? 2 : 1;  // warp-uniform
             const int X0 = (X4 << w) >> l;
-            // strides: q row, r plane, second copy (rows; 0 when it is a dummy)
-            const ptrdiff_t sq = ce.L.Px, sr = DIM == 3 ? ce.L.plane : 0;
-            const ptrdiff_t dsp = ncopy == 2 ? (ptrdiff_t)((Nl - 1) >> 1) * sq : 0;
-            const double* p00 = ce.du + eix<DIM>(ce.L, X0, y >> l, DIM == 3 ? (z >> l) - ce.L.z0 : 0);
-            // the run of MV nodes straddles two cells only on level w + 1
+            // 32-bit element offsets (level arrays hold < 2^31 doubles, see
+            // sgml_solver::build): q row, r plane, second copy (rows; 0 when it
+            // is a dummy)
+            const int sq = ce.L.Px, sr = DIM == 3 ? (int)ce.L.plane : 0;
+            const int dsp = ncopy == 2 ? ((Nl - 1) >> 1) * sq : 0;
+            const int o00 = (int)eix<DIM>(ce.L, X0, y >> l, DIM == 3 ? (z >> l) - ce.L.z0 : 0);
+            // the run of MV nodes straddles two cells only on level w + 1 (X4 is a
+            // multiple of 4: nodes 0, 1 in cell X0, nodes 2, 3 in cell X0 + 1, at
+            // fractions 0 and 1/2)
             const bool straddle = l == w + 1;
             double fx[MV], wx0[MV];
-            int jk[MV];
 #pragma unroll
             for (int k = 0; k < MV; ++k) {
                 const int x = (X4 + k) << w;
                 fx[k] = (double)(x & msk) * inv;
                 wx0[k] = 1.0 - fx[k];
-                jk[k] = straddle ? (x >> l) - X0 : 0;
             }
             double acc[2][MV];
             // `st` is a literal at both call sites: the straddle selects vanish
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(MBX* MBY)
                     for (int q = 0; q < 2; ++q) {
 #pragma unroll
                         for (int cp = 0; cp < 2; ++cp) {
-                            const double* rw = p00 + (r * sr + q * sq + cp * dsp);
+                            const double* rw = ce.du + (o00 + r * sr + q * sq + cp * dsp);
                             // past the x end: the DU arrays' ghost cells, never written (0)
                             cv[r][q][cp][0] = __ldg(rw);
                             cv[r][q][cp][1] = __ldg(rw + 1);
@@ -144,8 +146,9 @@ __global__ void __launch_bounds__(MBX* MBY)
                                 const double w0 = wzy * wx0[k], w1 = wzy * fx[k];
 #pragma unroll
                                 for (int cp = 0; cp < 2; ++cp) {
-                                    const double ca = (st && jk[k]) ? cv[r][q][cp][1] : cv[r][q][cp][0];
-                                    const double cb = (st && jk[k]) ? cv[r][q][cp][2] : cv[r][q][cp][1];
+                                    const int j = st ? (k >> 1) : 0;
+                                    const double ca = cv[r][q][cp][j];
+                                    const double cb = cv[r][q][cp][j + 1];
                                     const double t0 = w0 * ca;
                                     acc[cp][k] = (r == 0 && q == 0) ? t0 : acc[cp][k] + t0;
                                     acc[cp][k] = acc[cp][k] + w1 * cb;
