@@ -77,7 +77,7 @@ typedef struct {
     int engine;     /* 0 = level-compact B200 engine (default), 1 = literal full-grid passes */
     int use_graph;  /* capture each cycle's launch sequence in a CUDA graph */
     int timing;     /* record per-kernel-class device time in the report */
-    int pad_;
+    int timing_classes; /* 0: every class; else a mask of (1 << SGML_CLASS_*) to time */
 } sgml_solver_opts;
 
 /* cycle.hpp:81-89 */

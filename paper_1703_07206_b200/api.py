@@ -472,10 +472,11 @@ class SolverOptions:
     engine: str = "compact"     # "compact" (B200 level-compact) or "literal" (reference-shaped)
     use_graph: bool = False
     timing: bool = False
+    timing_classes: int = 0     # 0: time every kernel class; else a mask of 1 << class index
 
     def to_c(self) -> _capi.SolverOpts:
         return _capi.SolverOpts(0 if self.engine == "compact" else 1, int(self.use_graph),
-                                int(self.timing), 0)
+                                int(self.timing), int(self.timing_classes))
 
 
 @dataclass

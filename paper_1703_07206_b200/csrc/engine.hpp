@@ -150,7 +150,7 @@ struct sgml_solver {
             check_launch(cls);
             return;
         }
-        if (!opts.timing) {
+        if (!opts.timing || (opts.timing_classes && !((opts.timing_classes >> cls) & 1))) {
             fn();
             return;
         }
