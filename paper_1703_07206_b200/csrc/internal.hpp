@@ -98,7 +98,7 @@ void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc
 // passes the replicated level-vrep sample for replicated targets).
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
                          const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
-                         int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
+                         int frel, const ChainEntry* chain, int nchain, int maxl, const BcDev& bc,
                          bool homogeneous, int* flag, cudaStream_t s);
 // 3D: out planes [kb, ke) (local) <- in at positions << shift (level subsample)
 void launch_sample_ext(const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout, int shift, int kb,

@@ -40,7 +40,7 @@ namespace {
 constexpr int MV = 4;
 constexpr int MBX = 32, MBY = 4;
 
-template <int DIM>
+template <int DIM, int NC>
 __global__ void __launch_bounds__(MBX* MBY)
     k_materialize4(double* __restrict__ out, ExtLay Lw, int w, const double* __restrict__ base,
                    ExtLay L0, int wb, int base_zero, const double* __restrict__ ufine, ExtLay Lf, int frel,
@@ -51,7 +51,8 @@ __global__ void __launch_bounds__(MBX* MBY)
     for (int c = tid; c < nchain; c += MBX * MBY) sch[c] = chain[c];
     __syncthreads();
 
-    const int Nw = Lw.N, H = (Nw - 1) >> 1;
+    // NC copies along y at spacing D = (Nw - 1) / NC: rows s0 + c D
+    const int Nw = Lw.N, D = (Nw - 1) / NC;
     const int X4 = (blockIdx.x * MBX + threadIdx.x) * MV;
     // spread row index S (warp-uniform); 3D: local plane K (block-uniform),
     // global plane Kg (z-slab arrays start at global plane Lw.z0)
@@ -59,12 +60,12 @@ __global__ void __launch_bounds__(MBX* MBY)
     const int K = DIM == 3 ? (int)blockIdx.z : 0;
     const int Kg = DIM == 3 ? K + Lw.z0 : 0;
     int bad = 0, tiny = 0;
-    if (X4 < Nw && S <= H) {
-        const int ncopy = S < H ? 2 : 1;
-        const int s0 = S < H ? S : 2 * H;
+    if (X4 < Nw && S <= D) {
+        const int ncopy = S < D ? NC : 1;
+        const int s0 = S < D ? S : NC * D;
         const int nv = min(MV, Nw - X4);
-        // node (k, copy cp): x = X4 + k, y = s0 + cp * H
-        auto node_j = [&](int cp) { return s0 + cp * H; };
+        // node (k, copy cp): x = X4 + k, y = s0 + cp * D
+        auto node_j = [&](int cp) { return s0 + cp * D; };
         // every node of this thread on a Dirichlet face: nothing to interpolate
         const bool xdir = nv == 1 && X4 == Nw - 1 && !bc.neu[1];
         const bool rowdir = ncopy == 1 && !bc.neu[3];
@@ -72,9 +73,9 @@ __global__ void __launch_bounds__(MBX* MBY)
         const int nch = (xdir || rowdir || pdir) ? 0 : nchain;
 
         const int y = s0 << w, z = Kg << w;
-        double val[2][MV];
+        double val[NC][MV];
 #pragma unroll
-        for (int cp = 0; cp < 2; ++cp)
+        for (int cp = 0; cp < NC; ++cp)
 #pragma unroll
             for (int k = 0; k < MV; ++k)
                 val[cp][k] = (!base_zero && k < nv && cp < ncopy)
@@ -94,10 +95,10 @@ __global__ void __launch_bounds__(MBX* MBY)
             const int nq = iy ? 2 : 1, nr = (DIM == 3 && iz) ? 2 : 1;  // warp-uniform
             const int X0 = (X4 << w) >> l;
             // 32-bit element offsets (level arrays hold < 2^31 doubles, see
-            // sgml_solver::build): q row, r plane, second copy (rows; 0 when it
-            // is a dummy)
+            // sgml_solver::build): q row, r plane, copy spacing (D in level-l
+            // rows; 0 when the copies are dummies)
             const int sq = ce.L.Px, sr = DIM == 3 ? (int)ce.L.plane : 0;
-            const int dsp = ncopy == 2 ? ((Nl - 1) >> 1) * sq : 0;
+            const int dsp = ncopy == NC ? ((Nl - 1) / NC) * sq : 0;
             const int o00 = (int)eix<DIM>(ce.L, X0, y >> l, DIM == 3 ? (z >> l) - ce.L.z0 : 0);
             // the run of MV nodes straddles two cells only on level w + 1 (X4 is a
             // multiple of 4: nodes 0, 1 in cell X0, nodes 2, 3 in cell X0 + 1, at
@@ -110,63 +111,57 @@ __global__ void __launch_bounds__(MBX* MBY)
                 fx[k] = (double)(x & msk) * inv;
                 wx0[k] = 1.0 - fx[k];
             }
-            double acc[2][MV];
+            double acc[NC][MV];
             // `st` is a literal at both call sites: the straddle selects vanish
             // from the common (same-cell) path
             auto accumulate = [&](bool st) {
-                // all corner loads first (one latency per entry), then the
-                // products in the reference's order
-                double cv[2][2][2][3];
-                // every corner row exists in memory (rows / planes up to Nl are
-                // ghost cells), so all loads are unconditional; dead rows
-                // (zero weight) are loaded but not used
 #pragma unroll
-                for (int r = 0; r < (DIM == 3 ? 2 : 1); ++r)
+                for (int r = 0; r < 2; ++r) {
+                    if (r >= nr) break;
+                    // corner loads of this plane first (both rows, all copies),
+                    // then the products in the reference's order.  Every row exists
+                    // in memory (rows up to Nl are ghost cells); past the x end
+                    // the DU arrays' ghost cells, never written (0)
+                    double cv[2][NC][3];
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {
+                    for (int q = 0; q < 2; ++q)
 #pragma unroll
-                        for (int cp = 0; cp < 2; ++cp) {
+                        for (int cp = 0; cp < NC; ++cp) {
                             const double* rw = ce.du + (o00 + r * sr + q * sq + cp * dsp);
-                            // past the x end: the DU arrays' ghost cells, never written (0)
-                            cv[r][q][cp][0] = __ldg(rw);
-                            cv[r][q][cp][1] = __ldg(rw + 1);
-                            cv[r][q][cp][2] = st ? __ldg(rw + 2) : 0.0;
+                            cv[q][cp][0] = __ldg(rw);
+                            cv[q][cp][1] = __ldg(rw + 1);
+                            cv[q][cp][2] = st ? __ldg(rw + 2) : 0.0;
                         }
-                    }
-#pragma unroll
-                for (int r = 0; r < 2; ++r)
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
-                        if (r < nr && q < nq) {
-                            const double wzy = DIM == 3 ? wz[r] * wy[q] : wy[q];
-                            // reference order per node: corner p = 0 then p = 1 of this
-                            // (r, q); a zero-weight p = 1 term adds +-0 (as the reference)
+                        if (q >= nq) break;
+                        const double wzy = DIM == 3 ? wz[r] * wy[q] : wy[q];
+                        // reference order per node: corner p = 0 then p = 1 of this
+                        // (r, q); a zero-weight p = 1 term adds +-0 (as the reference)
 #pragma unroll
-                            for (int k = 0; k < MV; ++k) {
-                                const double w0 = wzy * wx0[k], w1 = wzy * fx[k];
+                        for (int k = 0; k < MV; ++k) {
+                            const double w0 = wzy * wx0[k], w1 = wzy * fx[k];
+                            const int j = st ? (k >> 1) : 0;
 #pragma unroll
-                                for (int cp = 0; cp < 2; ++cp) {
-                                    const int j = st ? (k >> 1) : 0;
-                                    const double ca = cv[r][q][cp][j];
-                                    const double cb = cv[r][q][cp][j + 1];
-                                    const double t0 = w0 * ca;
-                                    acc[cp][k] = (r == 0 && q == 0) ? t0 : acc[cp][k] + t0;
-                                    acc[cp][k] = acc[cp][k] + w1 * cb;
-                                }
+                            for (int cp = 0; cp < NC; ++cp) {
+                                const double t0 = w0 * cv[q][cp][j];
+                                acc[cp][k] = (r == 0 && q == 0) ? t0 : acc[cp][k] + t0;
+                                acc[cp][k] = acc[cp][k] + w1 * cv[q][cp][j + 1];
                             }
                         }
                     }
+                }
             };
             if (straddle) accumulate(true);
             else accumulate(false);
 #pragma unroll
-            for (int cp = 0; cp < 2; ++cp)
+            for (int cp = 0; cp < NC; ++cp)
 #pragma unroll
                 for (int k = 0; k < MV; ++k) val[cp][k] = val[cp][k] + acc[cp][k];
         }
         const int fmask = (1 << frel) - 1;
 #pragma unroll
-        for (int cp = 0; cp < 2; ++cp) {
+        for (int cp = 0; cp < NC; ++cp) {
             if (cp >= ncopy) break;
             const int Jn = node_j(cp), Kn = Kg;
             const bool jface = Jn == 0 || Jn == Nw - 1 || (DIM == 3 && (Kn == 0 || Kn == Nw - 1));
@@ -312,17 +307,21 @@ uint64_t ext_size(int dim, const ExtLay& L) {
 
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
                          const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
-                         int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
+                         int frel, const ChainEntry* chain, int nchain, int maxl, const BcDev& bc,
                          bool homogeneous, int* flag, cudaStream_t s) {
     const int Nw = Lw.N;
-    const int threads_x = (Nw + MV - 1) / MV, H = (Nw - 1) / 2;
-    const dim3 grid((threads_x + MBX - 1) / MBX, (H + MBY) / MBY, dim == 3 ? Lw.Nz : 1);
-    if (dim == 2)
-        k_materialize4<2><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, frel,
-                                                          chain, nchain, bc, homogeneous, flag);
-    else
-        k_materialize4<3><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, frel,
-                                                          chain, nchain, bc, homogeneous, flag);
+    // two copies (y and y + (Nw-1)/2): measured faster than four, whose 16
+    // nodes per thread cost occupancy (maxl is kept for that variant)
+    (void)maxl;
+    constexpr int NC = 2;
+    const int threads_x = (Nw + MV - 1) / MV, D = (Nw - 1) / NC;
+    const dim3 grid((threads_x + MBX - 1) / MBX, (D + MBY) / MBY, dim == 3 ? Lw.Nz : 1);
+#define SGML_MAT(DD, CC)                                                                               \
+    k_materialize4<DD, CC><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, \
+                                                           frel, chain, nchain, bc, homogeneous, flag)
+    if (dim == 2) SGML_MAT(2, NC);
+    else SGML_MAT(3, NC);
+#undef SGML_MAT
 }
 
 void launch_pyramid_ext(int dim, const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout,
