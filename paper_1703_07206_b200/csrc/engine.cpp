@@ -911,6 +911,7 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
 
     load_source(f);
     SGML_CUDA(cudaMemsetAsync(utot, 0, (compact() ? ext_size(g.dim, Lv[0]) : T) * sizeof(double), s));
+    if (compact()) fstate[utot] = FS_ZERO;  // (a reused engine's u_tot held last solve's faces)
     if (all_neumann) zero_mean_r();
     double norm = max_abs_r(f);  // D = max|f|; 0 falls back to the cycle-0 residual
     bool norm_pending = norm == 0.0;

@@ -1,0 +1,66 @@
+"""Full-size known answers (measured with the reference CPU
+solver): the configs the CPU oracle is too slow to re-run inside a test.
+Residual histories printed with %.17g are compared bit for bit; the others
+(cycle counts plus 4 significant digits) as published there."""
+import numpy as np
+import pytest
+
+from cases import O
+import paper_1703_07206_b200 as S
+
+pytestmark = pytest.mark.gpu
+needs_ref = pytest.mark.skipif(O.ref_lib() is None, reason="reference builders not built on this host")
+
+CFG = dict(n_r=2, tol=1e-10, max_cycles=60, safety=0.9)
+
+
+def gpu_solve(g, b, f, s=None, a=0.0):
+    bc = S.BoundarySpec([S.FaceBc(S.BcKind(b.kind[i]), b.value[i]) for i in range(6)])
+    res = S.solve(S.ProblemSpec(S.make_grid(g.dim, g.n), f, bc=bc, sigma=s, a=a), S.SolverConfig(**CFG))
+    return res, [r.residual for r in res.report.rows]
+
+
+def test_c2_poisson3d_257_history():
+    g = O.make_grid(3, 8)
+    res, hist = gpu_solve(g, O.all_dirichlet(0.0), O.fill("poisson3d", g))
+    assert res.report.converged
+    assert hist == [0.11335979565403487, 0.005997060095500154, 0.00043150202291021811,
+                    2.4230559383467491e-05, 1.6655190490280649e-06, 1.0116808154153438e-07,
+                    6.6355677192962395e-09, 4.1406301066115113e-10, 2.6713213473875857e-11]
+
+
+@pytest.mark.timeout(300)
+def test_poisson3d_513_history():
+    g = O.make_grid(3, 9)
+    res, hist = gpu_solve(g, O.all_dirichlet(0.0), O.fill("poisson3d", g))
+    assert res.report.converged and np.isfinite(res.u).all()
+    assert hist == [0.082998742327690306, 0.0049866810189616731, 0.00023545805115274265,
+                    1.3188481581819795e-05, 6.6391902103485231e-07, 3.5857651114910131e-08,
+                    1.8475091494005053e-09, 9.8038677002216647e-11]
+
+
+@pytest.mark.parametrize("kind,cycles,final", [("high", 22, 4.78e-11), ("low", 13, 4.92e-11)])
+def test_c5_capacitor_129_cycles(kind, cycles, final):
+    g = O.make_grid(3, 7)
+    s = O.fill("capacitor_sigma", g, -1.0 if kind == "high" else 1.0)
+    b = O.make_bc([O.NEUMANN] * 4 + [O.DIRICHLET] * 2, [0.0] * 4 + [-1.0, 1.0])
+    res, hist = gpu_solve(g, b, np.zeros(g.total), s)
+    assert res.report.converged and len(hist) == cycles
+    assert abs(hist[-1] - final) <= 0.01 * final
+
+
+@needs_ref
+def test_c4_trifoil_psi_x_257_history():
+    g, b, f, s, a = O.ref_problem("trifoil_x", 8)
+    res, hist = gpu_solve(g, b, f, s, a)
+    assert res.report.converged
+    assert hist == [0.0088687730914004011, 9.3461830428292285e-05, 2.1708718370897767e-06,
+                    6.3410191925299958e-08, 2.0156174911833852e-09, 6.9009471648630163e-11]
+
+
+@needs_ref
+def test_c3_deformation_2049_cycles():
+    g, b, f, s, a = O.ref_problem("deformation_circle", 11)
+    res, hist = gpu_solve(g, b, f, s, a)
+    assert res.report.converged and len(hist) == 11
+    assert abs(hist[-1] - 2.851e-11) <= 0.001 * 2.851e-11

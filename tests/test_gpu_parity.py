@@ -295,3 +295,11 @@ def test_solver_object_repeated_runs_identical():
     assert K.bits_equal(u1.numpy(), u2.numpy())
     ref = O.solve(g, K.bc("dir0"), f, tol=1e-10)
     assert K.bits_equal(u1.numpy(), ref.u)
+
+
+def test_solve_twice_with_nonzero_dirichlet_values():
+    # the cached engine's buffers keep their face contents between solves
+    # (u_tot picks up the face values in cycle 0 of every solve)
+    for name, n in (("capacitor_high", 3), ("capacitor_low", 3), ("sigma3d_dirichlet", 3)):
+        for _ in range(2):
+            check_solve(name, n)
