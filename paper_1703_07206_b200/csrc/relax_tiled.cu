@@ -212,12 +212,34 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     // which only costs the fused edge terms)
     unsigned emax = 0, emin = 0x7ff00000u;
 
+    // Pair sharing.  A term's difference between two nodes of this thread is
+    // the negative of the partner's (IEEE subtraction and the products by
+    // 0.5 / fl(1/3) / sbar are sign-symmetric; sbar's sum commutes), so each
+    // such pair is evaluated once: PV for the pairs (plane q-1 node, plane q
+    // node) shared by the dr = +1 terms of the finishing nodes and the dr = -1
+    // terms of the starting ones, IP for the pairs inside plane q (dr = 0
+    // terms).  Values are the term t, or the difference d where the edge term
+    // is fused (fm).  Only the sign of an exact zero can differ from the
+    // reference's own evaluation.
+    using PairT = double[RT][XP][3][3];
+    auto inside = [](int a, int b) { return a >= 0 && a < RT && b >= 0 && b < XP; };
+    // term value from a difference (and sbar) for squared offset l2; keep_d:
+    // an edge term the consumer fuses (fma(d, 0.5, acc)) stays the difference
+    auto term_of = [&](double d, double sbar, int l2, bool keep_d) {
+        double t = d;
+        if (SIG) t = sbar * t;
+        if (l2 == 2 && !keep_d) t = t * 0.5;
+        else if (l2 == 3) t = t * kInv3;
+        return t;
+    };
     // the thread's RT x XP nodes' terms of one stencil plane (offset dr),
     // interleaved term by term so the independent accumulation chains
-    // overlap; the first term starts the chain (0 + t differs from t only
-    // in the sign of zero)
+    // overlap; the first term starts the chain (0 + t differs from t only in
+    // the sign of zero).  mode 1: dr = +1 of the finishing nodes (PV), mode 2:
+    // dr = -1 of the starting nodes (-PV), mode 3: dr = 0 (IP), 0: no pairs.
     auto plane_terms = [&](NodeD<DIM>& acc, NodeD<DIM>& smax, const Win<DIM>& P, const SWin<DIM, SIG>& Ps,
-                           const NodeD<DIM>& uc, const NodeD<DIM>& sc, int dr, bool fm) {
+                           const NodeD<DIM>& uc, const NodeD<DIM>& sc, int dr, bool fm, int mode,
+                           const PairT& PV, const PairT& PS, const PairT& IP, const PairT& IS) {
 #pragma unroll
         for (int q = (DIM == 3 ? -1 : 0); q <= (DIM == 3 ? 1 : 0); ++q)
 #pragma unroll
@@ -225,26 +247,85 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                 if (dr == 0 && q == 0 && p == 0) continue;
                 const int l2 = dr * dr + q * q + p * p;
                 const bool first = dr == -1 && q == (DIM == 3 ? -1 : 0) && p == -1;
+                const bool fuse = !SIG && fm && l2 == 2 && !first;
 #pragma unroll
                 for (int a = 0; a < RT; ++a)
 #pragma unroll
                     for (int b = 0; b < XP; ++b) {
-                        const int w = DIM == 3 ? a + q + 1 : 0, c = b + p + 1;
-                        double sbar = 1.0;
-                        if constexpr (SIG) {
-                            sbar = 0.5 * (Ps[w][c] + sc[a][b]);
-                            smax[a][b] = first ? sbar : (smax[a][b] < sbar ? sbar : smax[a][b]);
+                        const int aq = DIM == 3 ? a + q : a, bp = b + p;  // partner inside the thread?
+                        // (across the planes only the straight pairs: the others would
+                        // stay live through the whole step)
+                        const bool pair = mode != 0 && inside(aq, bp) && (mode == 3 || (q == 0 && p == 0));
+                        double v, sbar = 1.0;  // v: the term, or the difference when fused
+                        if (pair && mode == 1) {
+                            v = PV[a][b][q + 1][p + 1];
+                            if (SIG) sbar = PS[a][b][q + 1][p + 1];
+                        } else if (pair && mode == 2) {
+                            v = -PV[aq][bp][1 - q][p < 0 ? 2 : (p > 0 ? 0 : 1)];
+                            if (SIG) sbar = PS[aq][bp][1 - q][p < 0 ? 2 : (p > 0 ? 0 : 1)];
+                        } else if (pair && mode == 3) {
+                            const bool canon = q > 0 || (q == 0 && p > 0);
+                            v = canon ? IP[a][b][q + 1][p + 1] : -IP[aq][bp][1 - q][1 - p];
+                            if (SIG) sbar = canon ? IS[a][b][q + 1][p + 1] : IS[aq][bp][1 - q][1 - p];
+                        } else {
+                            const int w = DIM == 3 ? a + q + 1 : 0, c = b + p + 1;
+                            if (SIG) sbar = 0.5 * (Ps[w][c] + sc[a][b]);
+                            v = term_of(P[w][c] - uc[a][b], sbar, l2, fuse);
                         }
-                        if (!SIG && fm && l2 == 2 && !first) {
+                        if constexpr (SIG) smax[a][b] = first ? sbar : (smax[a][b] < sbar ? sbar : smax[a][b]);
+                        if (fuse) {
                             // edge: (d * 0.5) is exact for these inputs, so the fused
                             // multiply-add rounds once exactly like acc + (d * 0.5)
-                            acc[a][b] = fma(P[w][c] - uc[a][b], 0.5, acc[a][b]);
+                            acc[a][b] = fma(v, 0.5, acc[a][b]);
                         } else {
-                            const double t = stencil_t<SIG>(sbar, P[w][c], uc[a][b], l2);
-                            acc[a][b] = first ? t : acc[a][b] + t;
+                            acc[a][b] = first ? v : acc[a][b] + v;
                         }
                     }
             }
+    };
+    // PV / PS from the windows A (plane q-1) and B (plane q)
+    auto pairs_between = [&](const Win<DIM>& A, const Win<DIM>& B, const SWin<DIM, SIG>& As,
+                             const SWin<DIM, SIG>& Bs, bool fm, PairT& PV, PairT& PS) {
+#pragma unroll
+        for (int a = 0; a < RT; ++a)
+#pragma unroll
+            for (int b = 0; b < XP; ++b)
+#pragma unroll
+                for (int q = (DIM == 3 ? -1 : 0); q <= (DIM == 3 ? 1 : 0); ++q)
+#pragma unroll
+                    for (int p = -1; p <= 1; ++p) {
+                        const int aq = DIM == 3 ? a + q : a, bp = b + p;
+                        if (!inside(aq, bp) || q != 0 || p != 0) continue;
+                        const int wa = DIM == 3 ? a + 1 : 0, wb = DIM == 3 ? aq + 1 : 0;
+                        const double d = B[wb][bp + 1] - A[wa][b + 1];
+                        double sb = 1.0;
+                        if (SIG) sb = 0.5 * (Bs[wb][bp + 1] + As[wa][b + 1]);
+                        const int l2 = 1 + q * q + p * p;
+                        PV[a][b][q + 1][p + 1] = term_of(d, sb, l2, !SIG && fm);  // (pairs never start a chain)
+                        if (SIG) PS[a][b][q + 1][p + 1] = sb;
+                    }
+    };
+    // IP / IS inside plane B (canonical direction only)
+    auto pairs_within = [&](const Win<DIM>& B, const SWin<DIM, SIG>& Bs, bool fm, PairT& IP, PairT& IS) {
+#pragma unroll
+        for (int a = 0; a < RT; ++a)
+#pragma unroll
+            for (int b = 0; b < XP; ++b)
+#pragma unroll
+                for (int q = 0; q <= (DIM == 3 ? 1 : 0); ++q)
+#pragma unroll
+                    for (int p = -1; p <= 1; ++p) {
+                        if (!(q > 0 || (q == 0 && p > 0))) continue;
+                        const int aq = DIM == 3 ? a + q : a, bp = b + p;
+                        if (!inside(aq, bp)) continue;
+                        const int wc = DIM == 3 ? a + 1 : 0, wn = DIM == 3 ? aq + 1 : 0;
+                        const double d = B[wn][bp + 1] - B[wc][b + 1];
+                        double sb = 1.0;
+                        if (SIG) sb = 0.5 * (Bs[wn][bp + 1] + Bs[wc][b + 1]);
+                        const int l2 = q * q + p * p;
+                        IP[a][b][q + 1][p + 1] = term_of(d, sb, l2, !SIG && fm);
+                        if (SIG) IS[a][b][q + 1][p + 1] = sb;
+                    }
     };
 
     // finish one node: op, diag / residual, Euler step, store
@@ -319,6 +400,8 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             const unsigned sp = sq == 0 ? NST - 1 : sq - 1;
             mbar_wait_u32(a_full + 8 * sq, ph);
             read_plane(sq, B, Bs);
+            PairT PV, PS, IP, IS;
+            pairs_between(A, B, As, Bs, fm, PV, PS);
             if (q > m0) {  // nodes of plane q - 1: dr = +1 terms, then the update
                 const int m = q - 1;
                 opos += ostep;
@@ -334,7 +417,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                         sc[a][b] = 1.0;
                         if constexpr (SIG) sc[a][b] = As[DIM == 3 ? a + 1 : 0][b + 1];
                     }
-                plane_terms(acc, smax, B, Bs, uc, sc, 1, fm);
+                plane_terms(acc, smax, B, Bs, uc, sc, 1, fm, 1, PV, PS, IP, IS);
                 const int mg = DIM == 3 ? m + L.z0 : m;  // global plane
                 const unsigned mm = (mg == 1 || mg == N - 2) ? ALL : mirm;
                 NodeD<DIM> val;
@@ -374,8 +457,9 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                         sc[a][b] = 1.0;
                         if constexpr (SIG) sc[a][b] = Bs[DIM == 3 ? a + 1 : 0][b + 1];
                     }
-                plane_terms(acc, smax, A, As, uc, sc, -1, fm);
-                plane_terms(acc, smax, B, Bs, uc, sc, 0, fm);
+                plane_terms(acc, smax, A, As, uc, sc, -1, fm, 2, PV, PS, IP, IS);
+                pairs_within(B, Bs, fm, IP, IS);
+                plane_terms(acc, smax, B, Bs, uc, sc, 0, fm, 3, PV, PS, IP, IS);
             }
             if (++sq == NST) {
                 sq = 0;
