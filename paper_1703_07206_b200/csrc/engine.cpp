@@ -223,6 +223,7 @@ sgml_solver::~sgml_solver() {
     dfree(r); dfree(utot); dfree(A); dfree(B); dfree(fin); dfree(dense);
     for (size_t m = 1; m < P.size(); ++m) dfree(P[m]);
     for (double* s : S) dfree(s);
+    for (double* d : DT) dfree(d);
     for (size_t v = 1; v < U.size(); ++v) { dfree(U[v][0]); dfree(U[v][1]); }
     for (auto& lst : DU) for (double* d : lst) dfree(d);
     dfree(Lg); dfree(Lscr); dfree(Lu); dfree(Lup); dfree(Ldu); dfree(Ldup);
@@ -393,7 +394,11 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
         }
         if (has_sigma) {
             S.assign(n, nullptr);
-            for (int m = 0; m < n; ++m) S[m] = alloc(ext_size(dim, Lv[m]));
+            DT.assign(n, nullptr);
+            for (int m = 0; m < n; ++m) {
+                S[m] = alloc(ext_size(dim, Lv[m]));
+                DT[m] = alloc(ext_size(dim, Lv[m]));
+            }
         }
         // TMA descriptors: window arrays (relax inputs, sigma) and tile arrays
         // (sources, residual, u_tot)
@@ -407,7 +412,10 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
             add_maps(P[v], Lv[v], false, true);
         }
         if (has_sigma)
-            for (int v = 0; v < n; ++v) add_maps(S[v], Lv[v], true, false);
+            for (int v = 0; v < n; ++v) {
+                add_maps(S[v], Lv[v], true, false);
+                add_maps(DT[v], Lv[v], false, true);
+            }
     } else {
         r = alloc(T);
         utot = alloc(T);
@@ -530,6 +538,11 @@ void sgml_solver::load_sigma(const double* sigma_dense) {
         launch(SGML_CLASS_OTHER, [&] { launch_scatter_ext(dim, sigma_dense, S[0], Lv[0], s); });
         halo(S[0], 0);
         for (int m = 1; m < n; ++m) pyramid_step(S[m - 1], m - 1, S[m]);
+        // per-node pseudo-time steps of the sigma relaxation, per level
+        for (int m = 0; m < n; ++m) {
+            const RelaxConst rcm = relax_const(dim, m, g.h, a, cfg.safety, false);
+            launch(SGML_CLASS_OTHER, [&] { launch_dtau_ext(dim, S[m], Lv[m], DT[m], rcm, s); });
+        }
     } else {
         sgml_bc even{};
         for (int f = 0; f < 6; ++f) even.kind[f] = 1;
@@ -714,7 +727,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
             tm.u = umap(cur);
             tm.g = gmap(gsrc(v));
             tm.s = has_sigma ? umap(S[v]) : tm.u;
-            tm.t = tm.g;
+            tm.t = has_sigma ? gmap(DT[v]) : tm.g;
             launch(v == 0 ? SGML_CLASS_RELAX0 : SGML_CLASS_RELAX_COARSE, [&] {
                 launch_relax_tma(dim, has_sigma, tm, out, duo, Lv[v], rng[v], rc, diag + slot, flag, s);
             });

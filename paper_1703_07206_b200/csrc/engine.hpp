@@ -97,6 +97,7 @@ struct sgml_solver {
     std::vector<sgmlb::ExtLay> Lv;
     std::vector<double*> P;                   // P[m], m >= 1 (P[0] is r)
     std::vector<double*> S;                   // S[m] sigma pyramid, S[0] full sigma
+    std::vector<double*> DT;                  // DT[m] per-node pseudo-time step (sigma relax)
     std::vector<std::array<double*, 2>> U;    // U[v][0..1], v >= 1
     std::vector<std::vector<double*>> DU;     // DU[v][k]
     sgmlb::ChainEntry* d_chain = nullptr;     // per-tooth pending-increment lists

@@ -100,6 +100,9 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
                          const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
                          int frel, const ChainEntry* chain, int nchain, int maxl, const BcDev& bc,
                          bool homogeneous, int* flag, cudaStream_t s);
+// per-node pseudo-time step of the sigma relaxation at every node of a level
+// array (own planes), from the level's sigma (with ghosts / halos)
+void launch_dtau_ext(int dim, const double* sig, const ExtLay& L, double* dt, const RelaxConst& rc, cudaStream_t s);
 // 3D: out planes [kb, ke) (local) <- in at positions << shift (level subsample)
 void launch_sample_ext(const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout, int shift, int kb,
                        int ke, cudaStream_t s);

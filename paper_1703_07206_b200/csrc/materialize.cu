@@ -284,6 +284,34 @@ __global__ void __launch_bounds__(128) k_sample_ext(const double* __restrict__ i
     store_ext<3>(out, Lout, I, J, K, __ldg(in + eix<3>(Lin, I << shift, J << shift, kin)));
 }
 
+// Per-node pseudo-time step of the sigma relaxation (kernels.cpp:132-136):
+// dtau = (safety K) / (inv_s2 smax) with smax = max over the 2^d... 26 (8)
+// neighbours of sbar = 0.5 (sigma_n + sigma_c).  It depends on sigma only,
+// so it is evaluated once per solve and level; the max is order-free and
+// sbar's sum commutes, so this is the relaxation pass's own value bit for bit.
+template <int DIM>
+__global__ void __launch_bounds__(128) k_dtau_ext(const double* __restrict__ sig, ExtLay L, double* __restrict__ dt,
+                                                  RelaxConst rc) {
+    const int N = L.N;
+    const int i = blockIdx.x * 32 + threadIdx.x, j = blockIdx.y * 4 + threadIdx.y, k = blockIdx.z;
+    if (i >= N || j >= N) return;
+    const ptrdiff_t c = eix<DIM>(L, i, j, k);
+    const double sc = sig[c];
+    const ptrdiff_t sy = L.Px, sz = DIM == 3 ? (ptrdiff_t)L.plane : 0;
+    double smax = 0.0;
+#pragma unroll
+    for (int r = (DIM == 3 ? -1 : 0); r <= (DIM == 3 ? 1 : 0); ++r)
+#pragma unroll
+        for (int q = -1; q <= 1; ++q)
+#pragma unroll
+            for (int p = -1; p <= 1; ++p) {
+                if (r == 0 && q == 0 && p == 0) continue;
+                const double sbar = 0.5 * (sig[c + r * sz + q * sy + p] + sc);
+                smax = smax < sbar ? sbar : smax;
+            }
+    dt[c] = (rc.safety * rc.kdim) / (rc.inv_s2 * smax);
+}
+
 inline dim3 ext_grid(int dim, const ExtLay& L) {
     return dim3((L.N + 31) / 32, (L.N + 3) / 4, dim == 3 ? L.Nz : 1);
 }
@@ -362,6 +390,11 @@ void launch_sample_ext(const double* in, const ExtLay& Lin, double* out, const E
     dim3 g = ext_grid(3, Lout);
     g.z = ke - kb;
     k_sample_ext<<<g, dim3(32, 4), 0, s>>>(in, Lin, out, Lout, shift, kb);
+}
+
+void launch_dtau_ext(int dim, const double* sig, const ExtLay& L, double* dt, const RelaxConst& rc, cudaStream_t s) {
+    if (dim == 2) k_dtau_ext<2><<<ext_grid(2, L), dim3(32, 4), 0, s>>>(sig, L, dt, rc);
+    else k_dtau_ext<3><<<ext_grid(3, L), dim3(32, 4), 0, s>>>(sig, L, dt, rc);
 }
 
 }  // namespace sgmlb

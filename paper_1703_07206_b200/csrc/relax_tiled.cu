@@ -79,7 +79,7 @@ struct __align__(128) TRing {
     double u[NST][Tile<DIM>::PLANE_AL];
     double g[NST][Tile<DIM>::GBOX_AL];
     double s[SIG ? NST : 1][SIG ? Tile<DIM>::PLANE_AL : 16];
-    double t[MODE == MODE_RESID ? NST : 1][MODE == MODE_RESID ? Tile<DIM>::GBOX_AL : 16];
+    double t[(MODE == MODE_RESID || SIG) ? NST : 1][(MODE == MODE_RESID || SIG) ? Tile<DIM>::GBOX_AL : 16];
     unsigned long long full[NST];
     unsigned long long empty[NST];
 };
@@ -159,7 +159,9 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
         const unsigned s = p % NST, k = p / NST;
         if (k > 0) mbar_wait_u32(a_empty + 8 * s, (k - 1) & 1);
         const bool comp = m >= m0 && m < mend;
-        const unsigned bytes = BU + (SIG ? BU : 0u) + (comp ? BG + (DUO && RESID ? BG : 0u) : 0u);
+        // t box: u_tot (residual) or the per-node pseudo-time step (sigma relax)
+        constexpr bool TBOX = (DUO && RESID) || (SIG && !RESID);
+        const unsigned bytes = BU + (SIG ? BU : 0u) + (comp ? BG + (TBOX ? BG : 0u) : 0u);
         const unsigned bar = a_full + 8 * s;
         mbar_expect_tx_u32(bar, bytes);
         if (DIM == 3) {
@@ -167,14 +169,14 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             if (SIG) tma_load_3d_u32(a_s + s * (TL::PLANE_AL * 8), &tm_s, xb, y0, m + 1, bar);
             if (comp) {
                 tma_load_3d_u32(a_g + s * (TL::GBOX_AL * 8), &tm_g, xb, y0 + 1, m + 1, bar);
-                if (DUO && RESID) tma_load_3d_u32(a_t + s * (TL::GBOX_AL * 8), &tm_t, xb, y0 + 1, m + 1, bar);
+                if (TBOX) tma_load_3d_u32(a_t + s * (TL::GBOX_AL * 8), &tm_t, xb, y0 + 1, m + 1, bar);
             }
         } else {
             tma_load_2d_u32(a_u + s * (TL::PLANE_AL * 8), &tm_u, xb, m + 1, bar);
             if (SIG) tma_load_2d_u32(a_s + s * (TL::PLANE_AL * 8), &tm_s, xb, m + 1, bar);
             if (comp) {
                 tma_load_2d_u32(a_g + s * (TL::GBOX_AL * 8), &tm_g, xb, m + 1, bar);
-                if (DUO && RESID) tma_load_2d_u32(a_t + s * (TL::GBOX_AL * 8), &tm_t, xb, m + 1, bar);
+                if (TBOX) tma_load_2d_u32(a_t + s * (TL::GBOX_AL * 8), &tm_t, xb, m + 1, bar);
             }
         }
     };
@@ -272,7 +274,6 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                             if (SIG) sbar = 0.5 * (Ps[w][c] + sc[a][b]);
                             v = term_of(P[w][c] - uc[a][b], sbar, l2, fuse);
                         }
-                        if constexpr (SIG) smax[a][b] = first ? sbar : (smax[a][b] < sbar ? sbar : smax[a][b]);
                         if (fuse) {
                             // edge: (d * 0.5) is exact for these inputs, so the fused
                             // multiply-add rounds once exactly like acc + (d * 0.5)
@@ -342,7 +343,9 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             const double omg = op - gc;
             const double diag = HAS_A ? fabs((op + rc.a * uc) - gc) : fabs(omg);
             if constexpr (SIG) {
-                const double dtau = (rc.safety * rc.kdim) / (rc.inv_s2 * smax);
+                // per-node step precomputed from sigma (k_dtau_ext: the same
+                // expression on max sbar, which depends on sigma only)
+                const double dtau = tc;
                 if (!(dtau > 0.0)) {
                     value = __longlong_as_double(0x7ff8000000000000LL);
                 } else {
@@ -412,7 +415,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
                     for (int b = 0; b < XP; ++b) {
                         const int gi = gbase + TL::HXG * a + b;  // node in the g box
                         gc[a][b] = R.g[sp][gi];
-                        tc[a][b] = (DUO && RESID) ? R.t[sp][gi] : 0.0;
+                        tc[a][b] = ((DUO && RESID) || (SIG && !RESID)) ? R.t[sp][gi] : 0.0;
                         uc[a][b] = A[DIM == 3 ? a + 1 : 0][b + 1];
                         sc[a][b] = 1.0;
                         if constexpr (SIG) sc[a][b] = As[DIM == 3 ? a + 1 : 0][b + 1];
