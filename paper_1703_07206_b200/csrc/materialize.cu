@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(MBX* MBY)
     k_materialize4(double* __restrict__ out, ExtLay Lw, int w, const double* __restrict__ base,
                    ExtLay L0, int wb, int base_zero, const double* __restrict__ ufine, ExtLay Lf, int frel,
                    const ChainEntry* __restrict__ chain, int nchain, BcDev bc, int homogeneous,
-                   int* flag) {
+                   int* flag, int xtail) {
     __shared__ ChainEntry sch[kMaxChain];
     const int tid = threadIdx.x + MBX * threadIdx.y;
     for (int c = tid; c < nchain; c += MBX * MBY) sch[c] = chain[c];
@@ -183,6 +183,10 @@ __global__ void __launch_bounds__(MBX* MBY)
                 }
                 store_ext<DIM>(out, Lw, I, Jn, K, value);
             }
+            // Dirichlet x-high face: the last group also writes node Nw - 1 (the
+            // grid stops at Nw - 2, so no block is spent on that column)
+            if (xtail && X4 + MV == Nw - 1)
+                out[eix<DIM>(Lw, Nw - 1, Jn, K)] = homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, Nw - 1, Jn, Kn);
         }
     }
     warp_or_commit(bad, flag);
@@ -342,11 +346,14 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
     // nodes per thread cost occupancy (maxl is kept for that variant)
     (void)maxl;
     constexpr int NC = 2;
-    const int threads_x = (Nw + MV - 1) / MV, D = (Nw - 1) / NC;
+    // Dirichlet x-high face (Nw - 1 a multiple of MV): threads cover x < Nw - 1
+    // and the last group writes the face node (xtail)
+    const int xtail = (!bc.neu[1] && (Nw - 1) % MV == 0) ? 1 : 0;
+    const int threads_x = xtail ? (Nw - 1) / MV : (Nw + MV - 1) / MV, D = (Nw - 1) / NC;
     const dim3 grid((threads_x + MBX - 1) / MBX, (D + MBY) / MBY, dim == 3 ? Lw.Nz : 1);
 #define SGML_MAT(DD, CC)                                                                               \
     k_materialize4<DD, CC><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, \
-                                                           frel, chain, nchain, bc, homogeneous, flag)
+                                                           frel, chain, nchain, bc, homogeneous, flag, xtail)
     if (dim == 2) SGML_MAT(2, NC);
     else SGML_MAT(3, NC);
 #undef SGML_MAT
