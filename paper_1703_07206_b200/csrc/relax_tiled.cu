@@ -332,15 +332,19 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     // finish one node: op, diag / residual, Euler step, store
     auto finish = [&](int m, int a, int b, double acc, double smax, double uc, double gc, double tc) {
         const ptrdiff_t pos = opos + (DIM == 3 ? a * (ptrdiff_t)L.Px : 0) + b;
-        const double op = (acc * rc.pref) * rc.inv_s2;
+        // inv_s2 = 1 / (2^v h)^2 is a power of two (h = 2^-n), so op = (acc
+        // pref) inv_s2 is an exact scaling and op - g == fma(acc pref, inv_s2,
+        // -g) bit for bit (one multiply saved where op is not needed itself)
+        const double ap = acc * rc.pref;
+        const double op = ap * rc.inv_s2;
         double value;
         if constexpr (RESID) {
-            value = gc - (HAS_A ? op + rc.a * uc : op);
+            value = HAS_A ? gc - (op + rc.a * uc) : fma(-ap, rc.inv_s2, gc);
             const double ar = fabs(value);
             dmax = dmax < ar ? ar : dmax;
             if (DUO) duo[pos] = tc + uc;
         } else {
-            const double omg = op - gc;
+            const double omg = fma(ap, rc.inv_s2, -gc);
             const double diag = HAS_A ? fabs((op + rc.a * uc) - gc) : fabs(omg);
             if constexpr (SIG) {
                 // per-node step precomputed from sigma (k_dtau_ext: the same
