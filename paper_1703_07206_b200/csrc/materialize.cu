@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(MBX* MBY)
         auto node_j = [&](int cp) { return s0 + cp * D; };
         // every node of this thread on a Dirichlet face: nothing to interpolate
         const bool xdir = nv == 1 && X4 == Nw - 1 && !bc.neu[1];
-        const bool rowdir = ncopy == 1 && !bc.neu[3];
+        const bool rowdir = S == D && !bc.neu[3];  // the lone last row
         const bool pdir = DIM == 3 && ((Kg == 0 && !bc.neu[4]) || (Kg == Nw - 1 && !bc.neu[5]));
         const int nch = (xdir || rowdir || pdir) ? 0 : nchain;
 
