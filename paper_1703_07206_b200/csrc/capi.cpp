@@ -4,6 +4,7 @@
 // device fields, and implements the kernel-level entry points of
 // kernels.hpp on top of the literal sm_100a kernels.
 #include <cmath>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -363,7 +364,7 @@ int sgml_relaxation_interpolation(sgml_field* u, const sgml_field* u_prev, sgml_
         const RelaxConst rc = relax_const(gr.dim, level, gr.h, a, safety, homogeneous != 0);
         launch_relax_literal(gr.dim, sigma != nullptr, u->d, du->d, u_prev->d, du_prev->d, g->d,
                              sigma ? sigma->d : nullptr, gr.N, level, rc, to_dev(*bc), ctx->d_slots,
-                             ctx->d_flags, s);
+                             ctx->d_flags, 0, s);
         SGML_CUDA(cudaGetLastError());
         SGML_CUDA(cudaMemcpyAsync(ctx->h_slots, ctx->d_slots, sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s));
@@ -500,21 +501,28 @@ int sgml_single_cycle(sgml_ctx* ctx, sgml_field* state_u, const sgml_field* sour
             fail(SGML_EBADSTEP, "relaxation_interpolation: non-positive pseudo-time step");
         }
         SGML_CUDA(cudaMemsetAsync(sv.d_cycle, 0, (sv.n_slots + 1) * sizeof(unsigned long long), s));
-        SGML_CUDA(cudaMemsetAsync(sv.d_flag, 0, sizeof(int), s));
+        sv.reset_fail_flags();
         sv.cycle_dense(source->d, state_u->d, homogeneous != 0);
         SGML_CUDA(cudaMemcpyAsync(sv.h_cycle, sv.d_cycle, sv.n_slots * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaMemcpyAsync(sv.h_flag, sv.d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaStreamSynchronize(s));
         SGML_CUDA(cudaGetLastError());
+        // a failing pass throws after the samples and work units of the steps
+        // before it (cycle.cpp:88-107): pass_index[p] counts the units before pass p
+        int passes = sv.n_slots;
+        if (sv.h_flag[0]) passes = std::min(sv.first_failing_pass(homogeneous != 0), sv.n_slots);
         const double inv_norm = normalization > 0.0 ? 1.0 / normalization : 1.0;
-        for (int p = 0; p < sv.n_slots; ++p) {
+        for (int p = 0; p < passes; ++p) {
             if (rep->n_trace < rep->trace_cap)
                 rep->trace[rep->n_trace] = sgml_diag_sample{cycle_index, sv.pass_index[p], sv.pass_level[p], 0,
                                                             slot_to_double(sv.h_cycle[p]) * inv_norm};
             rep->n_trace++;
         }
-        if (sv.h_flag[0]) fail(SGML_ENONFINITE, "relaxation_interpolation: non-finite value produced");
+        if (sv.h_flag[0]) {
+            *work += passes < sv.n_slots ? (uint64_t)sv.pass_index[passes] : sv.units_per_cycle;
+            fail(SGML_ENONFINITE, "relaxation_interpolation: non-finite value produced");
+        }
         *work += sv.units_per_cycle;
     });
 }

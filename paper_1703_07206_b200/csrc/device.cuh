@@ -272,9 +272,27 @@ __device__ __forceinline__ void warp_or_commit(int bad, int* flag) {
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+// a failing pass: flag[0] <- 1 and flag[4] <- min(flag[4], slot) (the first
+// failing pass of the cycle in the reference's order, for the partial trace)
+__device__ __forceinline__ void warp_bad_commit(int bad, int* flag, int slot) {
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) {
+        atomicOr(flag, 1);
+        atomicMin(flag + 4, slot);
+    }
+}
+
 __device__ __forceinline__ void block_or_commit(int bad, int* flag) {
     if (__syncthreads_or(bad)) {
         if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) atomicOr(flag, 1);
+    }
+}
+
+__device__ __forceinline__ void block_bad_commit(int bad, int* flag, int slot) {
+    if (__syncthreads_or(bad)) {
+        if (threadIdx.x == 0 && threadIdx.y == 0 && threadIdx.z == 0) {
+            atomicOr(flag, 1);
+            atomicMin(flag + 4, slot);
+        }
     }
 }
 

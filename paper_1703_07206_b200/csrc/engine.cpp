@@ -303,9 +303,9 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
     n_slots = (int)pass_level.size();
 
     SGML_CUDA(cudaMalloc((void**)&d_cycle, (n_slots + 4) * sizeof(unsigned long long)));
-    SGML_CUDA(cudaMalloc((void**)&d_flag, 4 * sizeof(int)));
+    SGML_CUDA(cudaMalloc((void**)&d_flag, 8 * sizeof(int)));
     SGML_CUDA(cudaMallocHost((void**)&h_cycle, (n_slots + 4) * sizeof(unsigned long long)));
-    SGML_CUDA(cudaMallocHost((void**)&h_flag, 4 * sizeof(int)));
+    SGML_CUDA(cudaMallocHost((void**)&h_flag, 8 * sizeof(int)));
 
     const uint64_t T = g.total;
     Nl.resize(n);
@@ -376,14 +376,24 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
             const int cmax = relax_count(n, cfg.n_r, v);
             for (int k = 0; k + 1 < cmax; ++k) DU[v].push_back(alloc(Ev));
         }
-        // tooth v1's increments in application order: levels v1..1, passes 1..c-1
+        // tooth v1's increments in application order: levels v1..1, passes 1..c-1;
+        // fslot = the pass that applies the increment (pass k + 2 of level v in
+        // tooth v1, numbered like pass_level: teeth n-1..0, levels v1..0)
         std::vector<ChainEntry> entries;
         tooth_off.assign(n, 0);
+        std::vector<int> tooth_slot(n, 0);
+        for (int v1 = n - 1, sl = 0; v1 >= 0; --v1) {
+            tooth_slot[v1] = sl;
+            sl += (v1 + 1) * relax_count(n, cfg.n_r, v1);
+        }
         for (int v1 = 0; v1 < n; ++v1) {
             tooth_off[v1] = (int)entries.size();
             const int cc = relax_count(n, cfg.n_r, v1);
-            for (int v = v1; v >= 1; --v)
-                for (int k = 0; k + 1 < cc; ++k) entries.push_back(ChainEntry{DU[v][k], Lv[v], v, 0});
+            for (int v = v1; v >= 1; --v) {
+                const int first_slot = tooth_slot[v1] + (v1 - v) * cc;
+                for (int k = 0; k + 1 < cc; ++k)
+                    entries.push_back(ChainEntry{DU[v][k], Lv[v], v, first_slot + k + 1});
+            }
         }
         for (int v = 1; v < n; ++v)
             for (double* d : DU[v]) du_bufs.push_back(d);
@@ -729,7 +739,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
             tm.s = has_sigma ? umap(S[v]) : tm.u;
             tm.t = has_sigma ? gmap(DT[v]) : tm.g;
             launch(v == 0 ? SGML_CLASS_RELAX0 : SGML_CLASS_RELAX_COARSE, [&] {
-                launch_relax_tma(dim, has_sigma, tm, out, duo, Lv[v], rng[v], rc, diag + slot, flag, s);
+                launch_relax_tma(dim, has_sigma, tm, out, duo, Lv[v], rng[v], rc, diag + slot, flag, slot, s);
             });
             ++slot;
             halo(out, v);  // z-slab levels: the next consumer reads across the slab faces
@@ -770,7 +780,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                     const ChainEntry* ch = chain_at();
                     launch(SGML_CLASS_MATERIALIZE, [&] {
                         launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lv[v + 1],
-                                            v + 1, ch, count, v1, bc, homogeneous, flag, s);
+                                            v + 1, ch, count, v1, bc, homogeneous, flag, diag_mode, s);
                     });
                     fstate[other] = face_want(homogeneous);
                     halo(other, 0);
@@ -789,7 +799,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                 base_src(v, bp, bl, wb);
                 launch(SGML_CLASS_MATERIALIZE, [&] {
                     launch_materialize4(dim, in, Lv[v], v, bp, bl, wb, base_zero, ufinal, Lf, 1, ch, count, v1,
-                                        bc, homogeneous, flag, s);
+                                        bc, homogeneous, flag, diag_mode, s);
                 });
                 fstate[in] = face_want(homogeneous);
                 halo(in, v);
@@ -808,7 +818,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
             const ExtLay Lf = n > 1 ? Lv[1] : Lv[0];
             launch(SGML_CLASS_MATERIALIZE, [&] {
                 launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lf, 1, ch, count, v1,
-                                    bc, homogeneous, flag, s);
+                                    bc, homogeneous, flag, diag_mode, s);
             });
             fstate[other] = face_want(homogeneous);
             halo(other, 0);
@@ -866,7 +876,7 @@ const double* sgml_solver::cycle_literal(bool homogeneous) {
                 std::swap(du, dup);
                 launch(SGML_CLASS_LITERAL, [&] {
                     launch_relax_literal(dim, has_sigma, u, du, up, dup, Lg, has_sigma ? Lsig[v] : nullptr,
-                                         N, v, rc, bc, d_cycle + slot, d_flag, s);
+                                         N, v, rc, bc, d_cycle + slot, d_flag, slot, s);
                 });
                 ++slot;
             }
@@ -891,6 +901,52 @@ void sgml_solver::pin_and_emit(double* u_out) {
         SGML_CUDA(cudaMemcpyAsync(u_out, res, T * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
+// flag[0] (some pass failed) and flag[4] (the first failing pass, atomicMin)
+void sgml_solver::reset_fail_flags() {
+    SGML_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), ctx->stream));
+    SGML_CUDA(cudaMemsetAsync(d_flag + 4, 0x7f, sizeof(int), ctx->stream));
+}
+
+// After a failed cycle: the first pass of the cycle the reference would throw
+// at (kernels.cpp:343-346), with the cycle's per-pass diag maxima in h_cycle.
+// The literal engine checks every node in every pass.  The compact engine's
+// relaxation kernels report their own pass, but the interpolated nodes exist
+// only as lazy chains: the cycle is re-run (same inputs: r is untouched until
+// the recurrence) with the materialisations checking every partial sum of
+// their chains, each chain entry carrying the pass that applies it.
+int sgml_solver::first_failing_pass(bool homogeneous) {
+    const cudaStream_t s = ctx->stream;
+    if (compact()) {
+        SGML_CUDA(cudaMemsetAsync(d_cycle, 0, (n_slots + 1) * sizeof(unsigned long long), s));
+        reset_fail_flags();
+        diag_mode = true;
+        try {
+            cycle(homogeneous);
+        } catch (...) {
+            diag_mode = false;
+            throw;
+        }
+        diag_mode = false;
+    }
+    SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, 8 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    SGML_CUDA(cudaStreamSynchronize(s));
+    int first = h_flag[4];  // 0x7f7f7f7f: flagged outside any pass (the first pass)
+    if (first == 0x7f7f7f7f) first = 0;
+    if (nrk > 1) {
+        // min over the ranks as a max of the complement
+        h_flag[5] = 0x7f7f7f7f - first;
+        SGML_CUDA(cudaMemcpyAsync(d_flag + 5, h_flag + 5, sizeof(int), cudaMemcpyHostToDevice, s));
+        tp->allreduce_max_i32(d_flag + 5, 1, s);
+        tp->allreduce_max_u64(d_cycle, n_slots + 1, s);
+        SGML_CUDA(cudaMemcpyAsync(h_flag + 5, d_flag + 5, sizeof(int), cudaMemcpyDeviceToHost, s));
+    }
+    SGML_CUDA(cudaMemcpyAsync(h_cycle, d_cycle, (n_slots + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                              s));
+    SGML_CUDA(cudaStreamSynchronize(s));
+    if (nrk > 1) first = 0x7f7f7f7f - h_flag[5];
+    return first;
+}
+
 // ---------------------------------------------------------------------------
 // solve (cycle.cpp:140-247)
 // ---------------------------------------------------------------------------
@@ -910,7 +966,7 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
     SGML_CUDA(cudaEventRecord(tev0, s));
 
     // input validation (cycle.cpp:150-152)
-    SGML_CUDA(cudaMemsetAsync(d_flag, 0, 4 * sizeof(int), s));
+    SGML_CUDA(cudaMemsetAsync(d_flag, 0, 8 * sizeof(int), s));
     launch(SGML_CLASS_OTHER, [&] { launch_check_finite(f, T, d_flag, s); });
     SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
     SGML_CUDA(cudaStreamSynchronize(s));
@@ -943,14 +999,25 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
             break;
         }
         SGML_CUDA(cudaMemsetAsync(d_cycle, 0, (n_slots + 1) * sizeof(unsigned long long), s));
-        SGML_CUDA(cudaMemsetAsync(d_flag, 0, sizeof(int), s));
+        reset_fail_flags();
         const double* e = cycle(homogeneous);
         // kernel_error check before the recurrence touches u_tot and r
         if (nrk > 1) tp->allreduce_max_i32(d_flag, 1, s);
         SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaStreamSynchronize(s));
         if (h_flag[0]) {
-            // no row for this cycle (cycle.cpp:186-190)
+            // the reference throws at the first failing pass: the trace keeps
+            // the samples of the passes before it, the cycle gets no row
+            // (cycle.cpp:98-107, 182-190)
+            const int fail_slot = first_failing_pass(homogeneous);
+            const double inv_norm = !norm_pending && norm > 0.0 ? 1.0 / norm : 1.0;
+            for (int p = 0; p < fail_slot && p < n_slots; ++p) {
+                double d;
+                std::memcpy(&d, &h_cycle[p], sizeof(double));
+                if (rep->n_trace < rep->trace_cap)
+                    rep->trace[rep->n_trace] = sgml_diag_sample{cyc, pass_index[p], pass_level[p], 0, d * inv_norm};
+                rep->n_trace++;
+            }
             rep->nan_detected = 1;
             rep->converged = 0;
             break;

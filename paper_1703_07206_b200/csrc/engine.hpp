@@ -114,7 +114,10 @@ struct sgml_solver {
     std::vector<double*> Lsig;                // full sigma levels
     // per-cycle device scratch: [0..n_slots) diag, n_slots = rmax
     unsigned long long* d_cycle = nullptr;
+    // flag[0] failed pass, [1] tiny level value, [2..3] neighbours' [1],
+    // [4] first failing pass (min), [5] scratch
     int* d_flag = nullptr;
+    bool diag_mode = false;  // materialisations attribute non-finite values to passes
     unsigned long long* h_cycle = nullptr;
     int* h_flag = nullptr;
     uint64_t bytes = 0;
@@ -178,6 +181,8 @@ struct sgml_solver {
     void zero_mean_r();                                  // zero_mean_projection(r)
     double max_abs_r(const double* f_dense);             // max |r| (data nodes)
     void residual(const double* e);                      // fused recurrence step
+    void reset_fail_flags();
+    int first_failing_pass(bool homogeneous);            // after a failed cycle
     const double* dense_view(const double* engine_field);  // dense device view
     void pin_and_emit(double* u_out_dev);                // pure_neumann_pin + result
     void ensure_literal();

@@ -21,7 +21,7 @@ void launch_restrict_pass(int dim, const double* in, double* out, int N, int lam
 void launch_relax_literal(int dim, bool sig, double* u, double* du, const double* up,
                           const double* dup, const double* g, const double* sigma, int N, int level,
                           const RelaxConst& rc, const BcDev& bc, unsigned long long* diag_slot,
-                          int* flag, cudaStream_t s);
+                          int* flag, int pass_slot, cudaStream_t s);
 // kernels.cpp:243-297 (+ cycle.cpp:194-198 fused): r -= A(e) + a e,
 // r = 0 on Dirichlet faces, u_tot += e (if non-null), max|r| (if non-null).
 void launch_residual(int dim, bool sig, double* r, const double* e, double* utot,
@@ -49,7 +49,7 @@ struct ChainEntry {
     const double* du;
     ExtLay L;
     int level;
-    int pad_;
+    int fslot;  // cycle slot of the reference pass that adds this increment
 };
 // Most increments one materialisation applies before the engine folds them
 // into a full-grid base (only reached for large n_r).
@@ -78,7 +78,7 @@ struct NodeRange {
 // pass fuse its edge terms (exact for such inputs).
 void launch_relax_tma(int dim, bool sig, const TmaSet& tm, double* uo, double* duo,
                       const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
-                      unsigned long long* diag_slot, int* flag, cudaStream_t s);
+                      unsigned long long* diag_slot, int* flag, int pass_slot, cudaStream_t s);
 // Residual recurrence at level 0 over the range: r -= A(e) + a e (tm.u = e,
 // tm.g = r, r written with mirror ghosts), u_tot += e (tm.t / utot,
 // nullable), max|r| into rmax_slot; reads flag[1] as the relaxation pass.
@@ -96,10 +96,12 @@ void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc
 // its subset nodes, or base + the pending increments chain[0..nchain).
 // base holds the level-wb subset (0: the level-0 array; a multi-GPU solve
 // passes the replicated level-vrep sample for replicated targets).
+// diag: also report the first chain entry whose partial sum turns non-finite
+// at an interpolated node (flag[4] <- min entry fslot; failure re-runs only)
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
                          const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
                          int frel, const ChainEntry* chain, int nchain, int maxl, const BcDev& bc,
-                         bool homogeneous, int* flag, cudaStream_t s);
+                         bool homogeneous, int* flag, bool diag, cudaStream_t s);
 // per-node pseudo-time step of the sigma relaxation at every node of a level
 // array (own planes), from the level's sigma (with ghosts / halos)
 void launch_dtau_ext(int dim, const double* sig, const ExtLay& L, double* dt, const RelaxConst& rc, cudaStream_t s);

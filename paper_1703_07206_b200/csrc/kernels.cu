@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(BX* BY)
     k_relax_literal(double* __restrict__ u, double* __restrict__ du, const double* __restrict__ up,
                     const double* __restrict__ dup, const double* __restrict__ g,
                     const double* __restrict__ sig, int N, int level, RelaxConst rc, BcDev bc,
-                    unsigned long long* diag_slot, int* flag) {
+                    unsigned long long* diag_slot, int* flag, int pass_slot) {
     const int i = blockIdx.x * BX + threadIdx.x, j = blockIdx.y * BY + threadIdx.y, k = blockIdx.z;
     const int lam = 1 << level, mask = lam - 1;
     double diag = 0.0;
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(BX* BY)
         du[pos] = duv;
     }
     block_max_commit(diag, diag_slot);
-    block_or_commit(bad, flag);
+    block_bad_commit(bad, flag, pass_slot);
 }
 
 template <int DIM, bool SIG>
@@ -254,15 +254,15 @@ void launch_restrict_pass(int dim, const double* in, double* out, int N, int lam
 
 void launch_relax_literal(int dim, bool sig, double* u, double* du, const double* up,
                           const double* dup, const double* g, const double* sigma, int N, int level,
-                          const RelaxConst& rc, const BcDev& bc, unsigned long long* slot, int* flag,
+                          const RelaxConst& rc, const BcDev& bc, unsigned long long* slot, int* flag, int pass_slot,
                           cudaStream_t s) {
     const dim3 gr = grid_for(dim, N), bl(BX, BY);
     if (dim == 2) {
-        if (sig) k_relax_literal<2, true><<<gr, bl, 0, s>>>(u, du, up, dup, g, sigma, N, level, rc, bc, slot, flag);
-        else k_relax_literal<2, false><<<gr, bl, 0, s>>>(u, du, up, dup, g, sigma, N, level, rc, bc, slot, flag);
+        if (sig) k_relax_literal<2, true><<<gr, bl, 0, s>>>(u, du, up, dup, g, sigma, N, level, rc, bc, slot, flag, pass_slot);
+        else k_relax_literal<2, false><<<gr, bl, 0, s>>>(u, du, up, dup, g, sigma, N, level, rc, bc, slot, flag, pass_slot);
     } else {
-        if (sig) k_relax_literal<3, true><<<gr, bl, 0, s>>>(u, du, up, dup, g, sigma, N, level, rc, bc, slot, flag);
-        else k_relax_literal<3, false><<<gr, bl, 0, s>>>(u, du, up, dup, g, sigma, N, level, rc, bc, slot, flag);
+        if (sig) k_relax_literal<3, true><<<gr, bl, 0, s>>>(u, du, up, dup, g, sigma, N, level, rc, bc, slot, flag, pass_slot);
+        else k_relax_literal<3, false><<<gr, bl, 0, s>>>(u, du, up, dup, g, sigma, N, level, rc, bc, slot, flag, pass_slot);
     }
 }
 

@@ -40,7 +40,7 @@ namespace {
 constexpr int MV = 4;
 constexpr int MBX = 32, MBY = 4;
 
-template <int DIM, int NC>
+template <int DIM, int NC, bool DIAG>
 __global__ void __launch_bounds__(MBX* MBY)
     k_materialize4(double* __restrict__ out, ExtLay Lw, int w, const double* __restrict__ base,
                    ExtLay L0, int wb, int base_zero, const double* __restrict__ ufine, ExtLay Lf, int frel,
@@ -73,6 +73,21 @@ __global__ void __launch_bounds__(MBX* MBY)
         const int nch = (xdir || rowdir || pdir) ? 0 : nchain;
 
         const int y = s0 << w, z = Kg << w;
+        // DIAG (failure re-runs): the interpolated nodes of this thread (not on
+        // a Dirichlet face, not taken from ufine) and the first chain entry
+        // whose partial sum turns non-finite at one of them
+        unsigned interp = 0;
+        int firstbad = 0x7fffffff;
+        if (DIAG) {
+            const int fm = (1 << frel) - 1;
+            for (int cp = 0; cp < ncopy; ++cp)
+                for (int k = 0; k < nv; ++k) {
+                    const int I = X4 + k, Jn = node_j(cp);
+                    const bool dir = on_dirichlet<DIM>(bc, Nw, I, Jn, Kg);
+                    const bool fine = ufine && ((I | Jn | Kg) & fm) == 0;
+                    if (!dir && !fine) interp |= 1u << (cp * MV + k);
+                }
+        }
         double val[NC][MV];
 #pragma unroll
         for (int cp = 0; cp < NC; ++cp)
@@ -158,6 +173,19 @@ __global__ void __launch_bounds__(MBX* MBY)
             for (int cp = 0; cp < NC; ++cp)
 #pragma unroll
                 for (int k = 0; k < MV; ++k) val[cp][k] = val[cp][k] + acc[cp][k];
+            if (DIAG) {
+#pragma unroll
+                for (int cp = 0; cp < NC; ++cp)
+#pragma unroll
+                    for (int k = 0; k < MV; ++k)
+                        if ((interp >> (cp * MV + k)) & 1u)
+                            if ((__double_as_longlong(val[cp][k]) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL)
+                                firstbad = min(firstbad, ce.fslot);
+            }
+        }
+        if (DIAG && firstbad != 0x7fffffff) {
+            atomicOr(flag, 1);
+            atomicMin(flag + 4, firstbad);
         }
         const int fmask = (1 << frel) - 1;
 #pragma unroll
@@ -340,7 +368,7 @@ uint64_t ext_size(int dim, const ExtLay& L) {
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
                          const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
                          int frel, const ChainEntry* chain, int nchain, int maxl, const BcDev& bc,
-                         bool homogeneous, int* flag, cudaStream_t s) {
+                         bool homogeneous, int* flag, bool diag, cudaStream_t s) {
     const int Nw = Lw.N;
     // two copies (y and y + (Nw-1)/2): measured faster than four, whose 16
     // nodes per thread cost occupancy (maxl is kept for that variant)
@@ -351,11 +379,16 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
     const int xtail = (!bc.neu[1] && (Nw - 1) % MV == 0) ? 1 : 0;
     const int threads_x = xtail ? (Nw - 1) / MV : (Nw + MV - 1) / MV, D = (Nw - 1) / NC;
     const dim3 grid((threads_x + MBX - 1) / MBX, (D + MBY) / MBY, dim == 3 ? Lw.Nz : 1);
-#define SGML_MAT(DD, CC)                                                                               \
-    k_materialize4<DD, CC><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, \
-                                                           frel, chain, nchain, bc, homogeneous, flag, xtail)
-    if (dim == 2) SGML_MAT(2, NC);
-    else SGML_MAT(3, NC);
+#define SGML_MAT(DD, CC, GG)                                                                     \
+    k_materialize4<DD, CC, GG><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, wb, base_zero, ufine, \
+                                                               Lf, frel, chain, nchain, bc, homogeneous, flag, xtail)
+    if (dim == 2) {
+        if (diag) SGML_MAT(2, NC, true);
+        else SGML_MAT(2, NC, false);
+    } else {
+        if (diag) SGML_MAT(3, NC, true);
+        else SGML_MAT(3, NC, false);
+    }
 #undef SGML_MAT
 }
 

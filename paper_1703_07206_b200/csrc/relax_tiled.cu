@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     k_relax_tma(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_g,
                 const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_t,
                 double* uo, double* duo, ExtLay L, int3 lo, int3 hi, int zb, RelaxConst rc,
-                unsigned long long* diag_slot, int* flag) {
+                unsigned long long* diag_slot, int* flag, int pass_slot) {
     using TL = Tile<DIM>;
     constexpr int NST = Ring<DIM, SIG, MODE>::NST, LEAD = Ring<DIM, SIG, MODE>::LEAD;
     constexpr int RT = TL::RT, WR = TL::WR, XP = TL::XP, WC = TL::WC;
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     }
     block_max_commit(dmax, diag_slot);
     if (!RESID) {
-        warp_or_commit(emax == 0x7ff00000u, flag);
+        warp_bad_commit(emax == 0x7ff00000u, flag, pass_slot);
         warp_or_commit(emin < 0x03600000u, flag + 1);
     }
 }
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
 template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO>
 void launch_t(dim3 grid, dim3 block, cudaStream_t s, const TmaSet& tm, double* uo, double* duo,
               const ExtLay& L, int3 lo, int3 hi, int zb, const RelaxConst& rc,
-              unsigned long long* slot, int* flag) {
+              unsigned long long* slot, int* flag, int pass_slot) {
     const int bytes = (int)sizeof(TRing<DIM, SIG, MODE>);
     static bool configured = false;
     if (!configured) {
@@ -510,26 +510,26 @@ void launch_t(dim3 grid, dim3 block, cudaStream_t s, const TmaSet& tm, double* u
         configured = true;
     }
     k_relax_tma<DIM, SIG, HAS_A, MODE, DUO><<<grid, block, bytes, s>>>(tm.u, tm.g, tm.s, tm.t, uo, duo, L, lo,
-                                                                       hi, zb, rc, slot, flag);
+                                                                       hi, zb, rc, slot, flag, pass_slot);
 }
 
 template <int DIM, int MODE, bool DUO>
 void launch_duo(dim3 grid, dim3 block, bool sig, cudaStream_t s, const TmaSet& tm, double* uo,
                 double* duo, const ExtLay& L, int3 lo, int3 hi, int zb, const RelaxConst& rc,
-                unsigned long long* slot, int* flag) {
+                unsigned long long* slot, int* flag, int pass_slot) {
     if (sig) {
-        if (rc.has_a) launch_t<DIM, true, true, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
-        else launch_t<DIM, true, false, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
+        if (rc.has_a) launch_t<DIM, true, true, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag, pass_slot);
+        else launch_t<DIM, true, false, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag, pass_slot);
     } else {
-        if (rc.has_a) launch_t<DIM, false, true, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
-        else launch_t<DIM, false, false, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
+        if (rc.has_a) launch_t<DIM, false, true, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag, pass_slot);
+        else launch_t<DIM, false, false, MODE, DUO>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag, pass_slot);
     }
 }
 
 template <int MODE>
 void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, const ExtLay& L,
                  const NodeRange& rg, const RelaxConst& rc, unsigned long long* slot, int* flag,
-                 cudaStream_t s) {
+                 int pass_slot, cudaStream_t s) {
     const int3 lo = make_int3(rg.lo[0], rg.lo[1], rg.lo[2]);
     const int3 hi = make_int3(rg.hi[0], rg.hi[1], rg.hi[2]);
     const int nx = rg.hi[0] - rg.lo[0] + 1, ny = rg.hi[1] - rg.lo[1] + 1, nz = rg.hi[2] - rg.lo[2] + 1;
@@ -551,11 +551,11 @@ void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, c
         block = dim3(TL::X, 1);
     }
     if (dim == 3) {
-        if (duo) launch_duo<3, MODE, true>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
-        else launch_duo<3, MODE, false>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
+        if (duo) launch_duo<3, MODE, true>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag, pass_slot);
+        else launch_duo<3, MODE, false>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag, pass_slot);
     } else {
-        if (duo) launch_duo<2, MODE, true>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
-        else launch_duo<2, MODE, false>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag);
+        if (duo) launch_duo<2, MODE, true>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag, pass_slot);
+        else launch_duo<2, MODE, false>(grid, block, sig, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag, pass_slot);
     }
 }
 
@@ -582,14 +582,14 @@ void tile_boxes(int dim, unsigned* box_u, unsigned* box_g) {
 
 void launch_relax_tma(int dim, bool sig, const TmaSet& tm, double* uo, double* duo,
                       const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
-                      unsigned long long* slot, int* flag, cudaStream_t s) {
-    launch_mode<MODE_RELAX>(dim, sig, tm, uo, duo, L, rg, rc, slot, flag, s);
+                      unsigned long long* slot, int* flag, int pass_slot, cudaStream_t s) {
+    launch_mode<MODE_RELAX>(dim, sig, tm, uo, duo, L, rg, rc, slot, flag, pass_slot, s);
 }
 
 void launch_residual_tma(int dim, bool sig, const TmaSet& tm, double* r, double* utot,
                          const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
                          unsigned long long* rmax_slot, int* flag, cudaStream_t s) {
-    launch_mode<MODE_RESID>(dim, sig, tm, r, utot, L, rg, rc, rmax_slot, flag, s);
+    launch_mode<MODE_RESID>(dim, sig, tm, r, utot, L, rg, rc, rmax_slot, flag, 0, s);
 }
 
 }  // namespace sgmlb

@@ -239,6 +239,53 @@ def test_solve_tiny_dirichlet_value_bitwise():
     assert K.bits_equal(res.u, ref.u)
 
 
+@pytest.mark.parametrize("engine", ["compact", "literal"])
+@pytest.mark.parametrize("name,n,safety,scale", [
+    ("poisson3d", 4, 20.0, 1e300), ("sinsin2d", 5, 30.0, 1e305), ("capacitor_high", 3, 50.0, 1.0),
+    ("poisson3d", 5, 40.0, 1e250), ("sinsin2d", 6, 10.0, 1e200), ("sinsin2d", 6, 3.0, 1e300),
+    ("poisson3d", 5, 4.0, 1e300), ("neumann3d_a", 4, 20.0, 1e250)])
+def test_solve_overflow_partial_trace(name, n, safety, scale, engine):
+    # a pass that overflows mid-cycle throws kernel_error in the reference
+    # (kernels.cpp:343-346): nan_detected, no row for the cycle, and the trace
+    # keeps the samples of the passes before the failing one (cycle.cpp:98-107)
+    g, b, f, s, a = K.solve_problem(name, n)
+    f = f * scale
+    if name == "capacitor_high":
+        b = O.make_bc(list(b.kind), [0, 0, 0, 0, -1e308, 1e308])
+    ref = O.solve(g, b, f, s, a, tol=1e-10, max_cycles=40, safety=safety)
+    res = S.solve(S.ProblemSpec(sgrid(g), f, bc=sbc_of(b), sigma=s, a=a),
+                  S.SolverConfig(tol=1e-10, max_cycles=40, safety=safety), S.SolverOptions(engine=engine))
+    rep = res.report
+    assert (rep.converged, rep.nan_detected, rep.stagnated) == (ref.converged, ref.nan_detected, ref.stagnated)
+    assert [(r.cycle, r.work_units, r.residual, r.diag_min) for r in rep.rows] == ref.rows
+    assert [(t.cycle, t.pass_, t.level, t.value) for t in rep.trace] == ref.trace
+    assert K.bits_equal(res.u, ref.u)
+
+
+@pytest.mark.parametrize("engine", ["compact", "literal"])
+@pytest.mark.parametrize("name,n,safety,scale", [
+    ("poisson3d", 4, 20.0, 1e300), ("sinsin2d", 6, 3.0, 1e300), ("capacitor_high", 3, 50.0, 1.0)])
+def test_single_cycle_overflow_partial_trace(name, n, safety, scale, engine):
+    # single_cycle throws at the failing pass with the samples and work units
+    # of the steps before it already recorded (cycle.cpp:88-107)
+    g, b, f, s, a = K.solve_problem(name, n)
+    f = f * scale
+    if name == "capacitor_high":
+        b = O.make_bc(list(b.kind), [0, 0, 0, 0, -1e308, 1e308])
+    levels = O.sigma_levels(g, s) if s is not None else None
+    st, _, trace_ref, w_ref = O.single_cycle(g, b, f, levels, a, False, 2, safety, 0, 1.0)
+    assert st != 0
+    state = S.SolveState(sgrid(g))
+    rep = S.SolveReport()
+    work = S.Work(3)
+    slv = S.restrict_sigma_levels(dev(g, s), g.n) if s is not None else []
+    with pytest.raises(S.kernel_error):
+        S.single_cycle(state, dev(g, f), slv, a, sbc_of(b), False, S.build_schedule(n, 2), safety, 0, 1.0,
+                       rep, work, S.SolverOptions(engine=engine))
+    assert work.value == 3 + w_ref
+    assert [(t.cycle, t.pass_, t.level, t.value) for t in rep.trace] == trace_ref
+
+
 def test_solve_larger_3d():
     check_solve("poisson3d", 6)          # 65^3
     check_solve("capacitor_high", 5)     # 33^3, sigma + mixed faces
