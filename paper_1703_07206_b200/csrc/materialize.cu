@@ -41,7 +41,7 @@ constexpr int MV = 4;
 constexpr int MBX = 32, MBY = 4;
 
 template <int DIM, int NC, bool DIAG>
-__global__ void __launch_bounds__(MBX* MBY)
+__global__ void __launch_bounds__(MBX* MBY, 5)
     k_materialize4(double* __restrict__ out, ExtLay Lw, int w, const double* __restrict__ base,
                    ExtLay L0, int wb, int base_zero, const double* __restrict__ ufine, ExtLay Lf, int frel,
                    const ChainEntry* __restrict__ chain, int nchain, BcDev bc, int homogeneous,
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(MBX* MBY)
     const int K = DIM == 3 ? (int)blockIdx.z : 0;
     const int Kg = DIM == 3 ? K + Lw.z0 : 0;
     int bad = 0, tiny = 0;
-    if (X4 < Nw && S <= D) {
+    if (S <= D && X4 < Nw) {
         const int ncopy = S < D ? NC : 1;
         const int s0 = S < D ? S : NC * D;
         const int nv = min(MV, Nw - X4);
@@ -71,32 +71,52 @@ __global__ void __launch_bounds__(MBX* MBY)
         const bool rowdir = S == D && !bc.neu[3];  // the lone last row
         const bool pdir = DIM == 3 && ((Kg == 0 && !bc.neu[4]) || (Kg == Nw - 1 && !bc.neu[5]));
         const int nch = (xdir || rowdir || pdir) ? 0 : nchain;
-
         const int y = s0 << w, z = Kg << w;
+        const int fmask = (1 << frel) - 1;
+        // rows / plane of this warp clear of the y / z faces by two nodes (no
+        // Dirichlet node, no mirror ghost; warp-uniform)
+        const bool rows_in = (DIM == 2 || (Kg >= 2 && Kg <= Nw - 3)) && s0 >= 2 && node_j(ncopy - 1) <= Nw - 3;
+        // interior fast path of a lane: also clear of the x faces; frel = 1.
+        // The level-(w+1) nodes (even x at even rows / planes; both copies
+        // have the row parity of s0 when D is even) take ufine, loaded up front
+        const bool inner = rows_in && frel == 1 && X4 >= 2 && X4 + MV <= Nw - 2 &&
+                           (!ufine || (D & 1) == 0);
+        const bool rowfine = inner && ufine && ((s0 | Kg) & 1) == 0;
+        double uf[NC][2];
+#pragma unroll
+        for (int cp = 0; cp < NC; ++cp) {
+            uf[cp][0] = uf[cp][1] = 0.0;
+            if (rowfine && cp < ncopy) {
+                const double* pf = ufine + (int)eix<DIM>(Lf, X4 >> 1, node_j(cp) >> 1, (Kg >> 1) - Lf.z0);
+                uf[cp][0] = __ldg(pf);
+                uf[cp][1] = __ldg(pf + 1);
+            }
+        }
         // DIAG (failure re-runs): the interpolated nodes of this thread (not on
         // a Dirichlet face, not taken from ufine) and the first chain entry
         // whose partial sum turns non-finite at one of them
         unsigned interp = 0;
         int firstbad = 0x7fffffff;
         if (DIAG) {
-            const int fm = (1 << frel) - 1;
             for (int cp = 0; cp < ncopy; ++cp)
                 for (int k = 0; k < nv; ++k) {
                     const int I = X4 + k, Jn = node_j(cp);
                     const bool dir = on_dirichlet<DIM>(bc, Nw, I, Jn, Kg);
-                    const bool fine = ufine && ((I | Jn | Kg) & fm) == 0;
+                    const bool fine = ufine && ((I | Jn | Kg) & fmask) == 0;
                     if (!dir && !fine) interp |= 1u << (cp * MV + k);
                 }
         }
         double val[NC][MV];
+        {
+            const int bsh = w - wb;
+            const double* bp = base + (int)eix<DIM>(L0, X4 << bsh, s0 << bsh, (z >> wb) - L0.z0);
+            const int bcs = (D << bsh) * L0.Px;  // copy spacing in base elements
 #pragma unroll
-        for (int cp = 0; cp < NC; ++cp)
+            for (int cp = 0; cp < NC; ++cp)
 #pragma unroll
-            for (int k = 0; k < MV; ++k)
-                val[cp][k] = (!base_zero && k < nv && cp < ncopy)
-                                 ? __ldg(base + eix<DIM>(L0, (X4 + k) << (w - wb), node_j(cp) << (w - wb),
-                                                         (z >> wb) - L0.z0))
-                                 : 0.0;
+                for (int k = 0; k < MV; ++k)
+                    val[cp][k] = (!base_zero && k < nv && cp < ncopy) ? __ldg(bp + cp * bcs + (k << bsh)) : 0.0;
+        }
 
         for (int c = 0; c < nch; ++c) {
             const ChainEntry ce = sch[c];
@@ -187,34 +207,53 @@ __global__ void __launch_bounds__(MBX* MBY)
             atomicOr(flag, 1);
             atomicMin(flag + 4, firstbad);
         }
-        const int fmask = (1 << frel) - 1;
+        // final values (Dirichlet faces, ufine nodes) and the checks
+        if (inner) {
 #pragma unroll
-        for (int cp = 0; cp < NC; ++cp) {
-            if (cp >= ncopy) break;
-            const int Jn = node_j(cp), Kn = Kg;
-            const bool jface = Jn == 0 || Jn == Nw - 1 || (DIM == 3 && (Kn == 0 || Kn == Nw - 1));
+            for (int cp = 0; cp < NC; ++cp) {
+                if (cp >= ncopy) break;
+                double* po = out + (int)eix<DIM>(Lw, X4, node_j(cp), K);
 #pragma unroll
-            for (int k = 0; k < MV; ++k) {
-                if (k >= nv) break;
-                const int I = X4 + k;
-                double value = val[cp][k];
-                if ((jface || I == 0 || I == Nw - 1) && on_dirichlet<DIM>(bc, Nw, I, Jn, Kn)) {
-                    value = homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, I, Jn, Kn);
-                } else if (ufine && ((I | Jn | Kn) & fmask) == 0) {
-                    value = __ldg(ufine + eix<DIM>(Lf, I >> frel, Jn >> frel, (Kn >> frel) - Lf.z0));
-                }
-                bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
-                {  // nonzero |value| < 2^-969 (see launch_relax_tma)
-                    const unsigned key = ((unsigned)__double2hiint(value) & 0x7fffffffu) |
-                                         (__double2loint(value) != 0 ? 1u : 0u);
+                for (int k = 0; k < MV; ++k) {
+                    double value = val[cp][k];
+                    if (rowfine && (k & 1) == 0) value = uf[cp][k >> 1];
+                    const unsigned hi = (unsigned)__double2hiint(value) & 0x7fffffffu;
+                    bad |= hi >= 0x7ff00000u;
+                    const unsigned key = hi | min((unsigned)__double2loint(value), 1u);
                     tiny |= key - 1u < 0x035fffffu;
+                    po[k] = value;
                 }
-                store_ext<DIM>(out, Lw, I, Jn, K, value);
             }
-            // Dirichlet x-high face: the last group also writes node Nw - 1 (the
-            // grid stops at Nw - 2, so no block is spent on that column)
-            if (xtail && X4 + MV == Nw - 1)
-                out[eix<DIM>(Lw, Nw - 1, Jn, K)] = homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, Nw - 1, Jn, Kn);
+        } else {
+#pragma unroll
+            for (int cp = 0; cp < NC; ++cp) {
+                if (cp >= ncopy) break;
+                const int Jn = node_j(cp), Kn = Kg;
+                const bool jface = Jn == 0 || Jn == Nw - 1 || (DIM == 3 && (Kn == 0 || Kn == Nw - 1));
+#pragma unroll
+                for (int k = 0; k < MV; ++k) {
+                    if (k >= nv) break;
+                    const int I = X4 + k;
+                    double value = val[cp][k];
+                    if ((jface || I == 0 || I == Nw - 1) && on_dirichlet<DIM>(bc, Nw, I, Jn, Kn)) {
+                        value = homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, I, Jn, Kn);
+                    } else if (ufine && ((I | Jn | Kn) & fmask) == 0) {
+                        value = __ldg(ufine + eix<DIM>(Lf, I >> frel, Jn >> frel, (Kn >> frel) - Lf.z0));
+                    }
+                    bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
+                    {  // nonzero |value| < 2^-969 (see launch_relax_tma)
+                        const unsigned key = ((unsigned)__double2hiint(value) & 0x7fffffffu) |
+                                             (__double2loint(value) != 0 ? 1u : 0u);
+                        tiny |= key - 1u < 0x035fffffu;
+                    }
+                    store_ext<DIM>(out, Lw, I, Jn, K, value);
+                }
+                // Dirichlet x-high face: the last group also writes node Nw - 1 (the
+                // grid stops at Nw - 2, so no block is spent on that column)
+                if (xtail && X4 + MV == Nw - 1)
+                    out[eix<DIM>(Lw, Nw - 1, Jn, K)] =
+                        homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, Nw - 1, Jn, Kn);
+            }
         }
     }
     warp_or_commit(bad, flag);
@@ -354,7 +393,9 @@ ExtLay make_ext(int dim, int N, int z0, int nz) {
     ExtLay L{};
     L.N = N;
     L.Ne = N + 2;
-    L.Px = (L.Ne + 1) / 2 * 2;  // even pitch: 16-byte aligned rows for TMA
+    // pitch a multiple of 4 doubles: 32-byte aligned rows (TMA needs 16; the
+    // materialisation's 256-bit accesses start at data nodes 4m - 1)
+    L.Px = (L.Ne + 3) / 4 * 4;
     L.Nz = dim == 3 ? (nz < 0 ? N : nz) : 1;
     L.z0 = dim == 3 ? z0 : 0;
     L.plane = dim == 3 ? (long long)L.Px * L.Ne : (long long)L.Px;
