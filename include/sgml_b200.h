@@ -245,6 +245,34 @@ int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f
                const double* sigma_host_or_null, double a, const sgml_solver_cfg* cfg,
                const sgml_solver_opts* opts_or_null, double* u_host_out, sgml_report* rep);
 
+/* ---- post-solve fields (problems.hpp:100-148) ----------
+ * Dense device fields in, dense device fields out; the reference's bits.
+ * Vector fields are arrays of dim component fields (3 for curl). */
+/* axis_derivative (problems.cpp:74-97): central inside, one-sided 3-point on faces */
+int sgml_axis_derivative(const sgml_field* u, int axis, sgml_field* out);
+/* gradient (problems.cpp:391-396): out[c] for c < dim */
+int sgml_gradient(const sgml_field* u, sgml_field* const* out);
+/* curl (problems.cpp:376-389); SGML_EINVAL unless 3D */
+int sgml_curl(const sgml_field* const* psi, sgml_field* const* out);
+/* divergence (problems.cpp:398-405): v[c] for c < dim */
+int sgml_divergence(const sgml_field* const* v, sgml_field* out);
+/* deformation_velocity (problems.cpp:327-341): -grad u / (t f_raw + raw_integral);
+ * SGML_EINVAL on a zero denominator */
+int sgml_deformation_velocity(const sgml_field* u, const sgml_field* f_raw, double raw_integral, double t,
+                              sgml_field* const* out);
+/* move_nodes (problems.cpp:343-372): node positions after `steps` Euler steps,
+ * as coordinate fields pos[0..dim-1] (pos[2] optional in 2D: zeros) */
+int sgml_move_nodes(const sgml_field* u, const sgml_field* f_raw, double raw_integral, double t, int steps,
+                    sgml_field* const* pos);
+/* sample_vector (problems.cpp:407-413) of nv component fields at host points
+ * (3 doubles each) into host out (3 doubles each, unused components 0) */
+int sgml_sample_vector(const sgml_field* const* v, int nv, const double* points, int count, double* out);
+/* integrate_streamline (problems.cpp:415-455) for nseeds host seeds: points
+ * [seed][max_steps + 1][3], counts[seed] points used, stops[seed] =
+ * 0 max_steps, 1 left_domain, 2 stagnation (StreamlineStop order) */
+int sgml_integrate_streamlines(const sgml_field* const* v, const double* seeds, int nseeds, double step,
+                               int max_steps, double* points, int* counts, int* stops);
+
 #ifdef __cplusplus
 }
 #endif

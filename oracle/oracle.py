@@ -105,6 +105,13 @@ def _load_c():
         getattr(lib, fn).argtypes = [G, _D]
     lib.og_fill_capacitor_sigma.argtypes = [G, C.c_double, _D]
     lib.og_lcg_fill.argtypes = [_D, C.c_uint64, C.c_uint64]
+    lib.og_axis_derivative.argtypes = [G, _D, C.c_int, _D]
+    for fn in ("og_gradient", "og_curl", "og_divergence"):
+        getattr(lib, fn).argtypes = [G, _D, _D]
+    lib.og_deformation_velocity.argtypes = [G, _D, _D, C.c_double, C.c_double, _D]
+    lib.og_move_nodes.argtypes = [G, _D, _D, C.c_double, C.c_double, C.c_int, _D]
+    lib.og_sample_vector.argtypes = [G, _D, C.c_int, _D, _D]
+    lib.og_integrate_streamline.argtypes = [G, _D, _D, C.c_double, C.c_int, _D, C.POINTER(C.c_int)]
     return lib
 
 
@@ -130,6 +137,13 @@ def _load_ref():
     lib.ref_solve.argtypes = [G, B, _D, _D, C.c_double, C.c_int, C.c_double, C.c_int, C.c_double,
                               _D, C.POINTER(Report)]
     lib.ref_problem_fields.argtypes = [C.c_char_p, C.c_int, _D, _D, C.POINTER(C.c_int), _D, _D]
+    for fn in ("ref_gradient", "ref_curl", "ref_divergence"):
+        getattr(lib, fn).argtypes = [G, _D, _D]
+    lib.ref_deformation_velocity.argtypes = [G, _D, _D, C.c_double, C.c_double, _D]
+    lib.ref_move_nodes.argtypes = [G, _D, _D, C.c_double, C.c_double, C.c_int, _D]
+    lib.ref_sample_vector.argtypes = [G, _D, _D, _D]
+    lib.ref_integrate_streamline.argtypes = [G, _D, _D, C.c_double, C.c_int, _D, C.POINTER(C.c_int)]
+    lib.ref_deformation_setup.argtypes = [_D, C.c_int, C.c_double, C.c_int, _D, _D, _D]
     return lib
 
 
@@ -347,3 +361,94 @@ def build_schedule(n: int, n_r: int):
     if c < 0:
         raise ValueError("build_schedule: n and n_r must be >= 1")
     return [(k[i], lv[i], cn[i]) for i in range(c)]
+
+
+# ------------------------------------------------- post-solve fields ----
+# problems.cpp:40-97, 327-455.  Vector fields: (ncomp, total) arrays.
+# impl "c" = the restatement, "ref" = the reference build (oracle/_ref).
+
+def _lib(impl):
+    lib = c_lib() if impl == "c" else ref_lib()
+    if lib is None:
+        raise RuntimeError("reference build unavailable")
+    return lib, ("og_" if impl == "c" else "ref_")
+
+
+def axis_derivative(g: Grid, u, axis: int):
+    out = np.zeros(g.total)
+    c_lib().og_axis_derivative(C.byref(g), _ptr(u), axis, _ptr(out))
+    return out
+
+
+def gradient(g: Grid, u, impl: str = "c"):
+    lib, pre = _lib(impl)
+    out = np.zeros((g.dim, g.total))
+    getattr(lib, pre + "gradient")(C.byref(g), _ptr(u), _ptr(out))
+    return out
+
+
+def curl(g: Grid, psi, impl: str = "c"):
+    lib, pre = _lib(impl)
+    psi = np.ascontiguousarray(psi, np.float64)
+    out = np.zeros((3, g.total))
+    getattr(lib, pre + "curl")(C.byref(g), _ptr(psi), _ptr(out))
+    return out
+
+
+def divergence(g: Grid, v, impl: str = "c"):
+    lib, pre = _lib(impl)
+    v = np.ascontiguousarray(v[:g.dim], np.float64)
+    out = np.zeros(g.total)
+    getattr(lib, pre + "divergence")(C.byref(g), _ptr(v), _ptr(out))
+    return out
+
+
+def deformation_velocity(g: Grid, u, f_raw, raw_integral: float, t: float, impl: str = "c"):
+    """(status, velocity (dim, total)); status 1 = zero denominator (invalid_argument)."""
+    lib, pre = _lib(impl)
+    out = np.zeros((g.dim, g.total))
+    st = getattr(lib, pre + "deformation_velocity")(C.byref(g), _ptr(u), _ptr(f_raw), raw_integral, t, _ptr(out))
+    return st, out
+
+
+def move_nodes(g: Grid, u, f_raw, raw_integral: float, t: float, steps: int, impl: str = "c"):
+    """(status, positions (total, 3))."""
+    lib, pre = _lib(impl)
+    pos = np.zeros((g.total, 3))
+    st = getattr(lib, pre + "move_nodes")(C.byref(g), _ptr(u), _ptr(f_raw), raw_integral, t, steps, _ptr(pos))
+    return st, pos
+
+
+def sample_vector(g: Grid, v, pt, impl: str = "c"):
+    v = np.ascontiguousarray(v[:g.dim], np.float64)
+    p = np.ascontiguousarray(pt, np.float64)
+    out = np.zeros(3)
+    if impl == "c":
+        c_lib().og_sample_vector(C.byref(g), _ptr(v), g.dim, _ptr(p), _ptr(out))
+    else:
+        ref_lib().ref_sample_vector(C.byref(g), _ptr(v), _ptr(p), _ptr(out))
+    return out
+
+
+def integrate_streamline(g: Grid, v, seed, step: float, max_steps: int, impl: str = "c"):
+    """(points (count, 3), stop) with stop 0 max_steps, 1 left_domain, 2 stagnation."""
+    lib, pre = _lib(impl)
+    v = np.ascontiguousarray(v[:g.dim], np.float64)
+    sd = np.ascontiguousarray(seed, np.float64)
+    pts = np.zeros((max_steps + 1, 3))
+    stop = C.c_int(0)
+    cnt = getattr(lib, pre + "integrate_streamline")(C.byref(g), _ptr(v), _ptr(sd), step, max_steps, _ptr(pts),
+                                                     C.byref(stop))
+    return pts[:cnt].copy(), stop.value
+
+
+def ref_deformation_setup(points, a: float, n: int):
+    """deformation_problem of the reference for a closed curve: (grid, f_raw, f, raw_integral)."""
+    pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    dim = 3 if np.any(pts[:, 2] != 0.0) else 2
+    g = make_grid(dim, n)
+    f_raw = np.zeros(g.total)
+    f = np.zeros(g.total)
+    ri = C.c_double(0.0)
+    ref_lib().ref_deformation_setup(_ptr(pts), pts.shape[0], a, n, _ptr(f_raw), _ptr(f), C.byref(ri))
+    return g, f_raw, f, ri.value

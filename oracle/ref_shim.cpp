@@ -203,4 +203,90 @@ int ref_problem_fields(const char* name, int n, double* f_out, double* sigma_out
     return p.sigma.size() ? 3 : 2;
 }
 
+// ---- post-solve fields (problems.hpp:100-148), component-major vectors ----
+
+namespace {
+R::VectorField to_vector(const R::Grid& g, const double* v, int nc) {
+    R::VectorField f(g);
+    for (int c = 0; c < nc; ++c) std::memcpy(f.comp[c].data(), v + (size_t)c * g.total, g.total * sizeof(double));
+    return f;
+}
+void from_vector(const R::VectorField& f, int nc, double* out) {
+    for (int c = 0; c < nc; ++c) std::memcpy(out + (size_t)c * f.comp[c].size(), f.comp[c].data(),
+                                             f.comp[c].size() * sizeof(double));
+}
+}  // namespace
+
+void ref_gradient(const og_grid* g, const double* u, double* out) {
+    const R::Grid gr = grid_of(g);
+    from_vector(R::gradient(to_field(gr, u)), g->dim, out);
+}
+
+void ref_curl(const og_grid* g, const double* psi, double* out) {
+    const R::Grid gr = grid_of(g);
+    from_vector(R::curl(to_vector(gr, psi, 3)), 3, out);
+}
+
+void ref_divergence(const og_grid* g, const double* v, double* out) {
+    const R::Grid gr = grid_of(g);
+    from_field(R::divergence(to_vector(gr, v, g->dim)), out);
+}
+
+int ref_deformation_velocity(const og_grid* g, const double* u, const double* f_raw, double raw_integral,
+                             double t, double* out) {
+    const R::Grid gr = grid_of(g);
+    try {
+        from_vector(R::deformation_velocity(to_field(gr, u), to_field(gr, f_raw), raw_integral, t), g->dim, out);
+    } catch (const std::invalid_argument&) {
+        return 1;
+    }
+    return 0;
+}
+
+int ref_move_nodes(const og_grid* g, const double* u, const double* f_raw, double raw_integral, double t,
+                   int steps, double* pos) {
+    const R::Grid gr = grid_of(g);
+    try {
+        const std::vector<R::Point> pts =
+            R::move_nodes(to_field(gr, u), to_field(gr, f_raw), raw_integral, t, steps);
+        for (size_t p = 0; p < pts.size(); ++p)
+            for (int c = 0; c < 3; ++c) pos[3 * p + c] = pts[p][c];
+    } catch (const std::invalid_argument&) {
+        return 1;
+    }
+    return 0;
+}
+
+void ref_sample_vector(const og_grid* g, const double* v, const double* pt, double* out) {
+    const R::Grid gr = grid_of(g);
+    const R::Point s = R::sample_vector(to_vector(gr, v, g->dim), {pt[0], pt[1], pt[2]});
+    for (int c = 0; c < 3; ++c) out[c] = s[c];
+}
+
+int ref_integrate_streamline(const og_grid* g, const double* v, const double* seed, double step, int max_steps,
+                             double* pts, int* stop) {
+    const R::Grid gr = grid_of(g);
+    const R::Streamline line =
+        R::integrate_streamline(to_vector(gr, v, g->dim), {seed[0], seed[1], seed[2]}, step, max_steps);
+    for (size_t q = 0; q < line.points.size(); ++q)
+        for (int c = 0; c < 3; ++c) pts[3 * q + c] = line.points[q][c];
+    *stop = line.stop == R::StreamlineStop::max_steps ? 0 : (line.stop == R::StreamlineStop::left_domain ? 1 : 2);
+    return (int)line.points.size();
+}
+
+// deformation_problem (problems.cpp:302-325) for a closed curve given as
+// xyz triples: the raw deposited source, the projected source and the raw
+// integral; returns the grid dimension
+int ref_deformation_setup(const double* pts, int npts, double a, int n, double* f_raw, double* f,
+                          double* raw_integral) {
+    R::Curve c;
+    c.closed = true;
+    for (int q = 0; q < npts; ++q) c.points.push_back({pts[3 * q], pts[3 * q + 1], pts[3 * q + 2]});
+    const R::DeformationSetup s = R::deformation_problem(c, a, n);
+    std::memcpy(f_raw, s.f_raw.data(), s.f_raw.size() * sizeof(double));
+    std::memcpy(f, s.problem.f.data(), s.problem.f.size() * sizeof(double));
+    *raw_integral = s.raw_integral;
+    return s.problem.grid.dim;
+}
+
 }  // extern "C"

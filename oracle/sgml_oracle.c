@@ -725,3 +725,193 @@ void og_lcg_fill(double* f, uint64_t total, uint64_t seed) {
         f[p] = (double)(x >> 11) / (double)(1ull << 53) * 2.0 - 1.0;
     }
 }
+
+/* ======================================================================
+ * Post-solve fields (problems.cpp:40-97, 327-455)
+ * ====================================================================== */
+
+/* problems.cpp:74-97: central differences inside, one-sided three-point
+ * stencils on the two faces; inv2h = 1.0 / (2.0 * h) */
+void og_axis_derivative(const og_grid* g, const double* u, int axis, double* out) {
+    const int N = g->N;
+    const ptrdiff_t s = axis == 0 ? 1 : (axis == 1 ? (ptrdiff_t)N : (ptrdiff_t)N * N);
+    const double inv2h = 1.0 / (2.0 * g->h);
+    for (uint64_t p = 0; p < g->total; ++p) {
+        const int i = (int)(p % (uint64_t)N), j = (int)((p / (uint64_t)N) % (uint64_t)N),
+                  k = (int)(p / ((uint64_t)N * (uint64_t)N));
+        const int c = axis == 0 ? i : (axis == 1 ? j : k);
+        double v;
+        if (c == 0)
+            v = (-3.0 * u[p] + 4.0 * u[p + s] - u[p + 2 * s]) * inv2h;
+        else if (c == N - 1)
+            v = (3.0 * u[p] - 4.0 * u[p - s] + u[p - 2 * s]) * inv2h;
+        else
+            v = (u[p + s] - u[p - s]) * inv2h;
+        out[p] = v;
+    }
+}
+
+/* problems.cpp:391-396 */
+void og_gradient(const og_grid* g, const double* u, double* out) {
+    for (int c = 0; c < g->dim; ++c) og_axis_derivative(g, u, c, out + (size_t)c * g->total);
+}
+
+/* problems.cpp:376-389 */
+void og_curl(const og_grid* g, const double* psi, double* out) {
+    const uint64_t T = g->total;
+    double* d = (double*)malloc(6 * T * sizeof(double));
+    double *dzy = d, *dyz = d + T, *dxz = d + 2 * T, *dzx = d + 3 * T, *dyx = d + 4 * T, *dxy = d + 5 * T;
+    og_axis_derivative(g, psi + 2 * T, 1, dzy);
+    og_axis_derivative(g, psi + 1 * T, 2, dyz);
+    og_axis_derivative(g, psi + 0 * T, 2, dxz);
+    og_axis_derivative(g, psi + 2 * T, 0, dzx);
+    og_axis_derivative(g, psi + 1 * T, 0, dyx);
+    og_axis_derivative(g, psi + 0 * T, 1, dxy);
+    for (uint64_t p = 0; p < T; ++p) {
+        out[p] = dzy[p] - dyz[p];
+        out[T + p] = dxz[p] - dzx[p];
+        out[2 * T + p] = dyx[p] - dxy[p];
+    }
+    free(d);
+}
+
+/* problems.cpp:398-405: d = 0; d += d_c v_c for c < dim */
+void og_divergence(const og_grid* g, const double* v, double* out) {
+    const uint64_t T = g->total;
+    double* dc = (double*)malloc(T * sizeof(double));
+    for (uint64_t p = 0; p < T; ++p) out[p] = 0.0;
+    for (int c = 0; c < g->dim; ++c) {
+        og_axis_derivative(g, v + (size_t)c * T, c, dc);
+        for (uint64_t p = 0; p < T; ++p) out[p] += dc[p];
+    }
+    free(dc);
+}
+
+/* problems.cpp:327-341 */
+int og_deformation_velocity(const og_grid* g, const double* u, const double* f_raw, double raw_integral,
+                            double t, double* out) {
+    og_gradient(g, u, out);
+    for (int c = 0; c < g->dim; ++c) {
+        double* comp = out + (size_t)c * g->total;
+        for (uint64_t p = 0; p < g->total; ++p) {
+            const double den = t * f_raw[p] + raw_integral;
+            if (den == 0.0) return OG_INVALID;
+            comp[p] = -comp[p] / den;
+        }
+    }
+    return OG_OK;
+}
+
+/* std::clamp for doubles */
+static double og_clampd(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+/* problems.cpp:40-67 */
+double og_sample_scalar(const og_grid* g, const double* f, const double* pt) {
+    const int N = g->N;
+    int idx[3] = {0, 0, 0};
+    double frac[3] = {0.0, 0.0, 0.0};
+    for (int c = 0; c < g->dim; ++c) {
+        const double x = og_clampd(pt[c], 0.0, 1.0) / g->h;
+        int i0 = (int)floor(x);
+        i0 = i0 < 0 ? 0 : (N - 2 < i0 ? N - 2 : i0);
+        idx[c] = i0;
+        frac[c] = x - i0;
+    }
+    const double wx[2] = {1.0 - frac[0], frac[0]};
+    const double wy[2] = {1.0 - frac[1], frac[1]};
+    double acc = 0.0;
+    if (g->dim == 2) {
+        for (int b = 0; b < 2; ++b)
+            for (int a = 0; a < 2; ++a)
+                acc += wx[a] * wy[b] * f[(size_t)(idx[0] + a) + (size_t)N * (size_t)(idx[1] + b)];
+    } else {
+        const double wz[2] = {1.0 - frac[2], frac[2]};
+        for (int c = 0; c < 2; ++c)
+            for (int b = 0; b < 2; ++b)
+                for (int a = 0; a < 2; ++a)
+                    acc += wx[a] * wy[b] * wz[c] *
+                           f[(size_t)(idx[0] + a) + (size_t)N * ((size_t)(idx[1] + b) + (size_t)N * (size_t)(idx[2] + c))];
+    }
+    return acc;
+}
+
+/* problems.cpp:407-413 */
+void og_sample_vector(const og_grid* g, const double* v, int nv, const double* pt, double* out) {
+    out[0] = out[1] = out[2] = 0.0;
+    for (int c = 0; c < nv; ++c) out[c] = og_sample_scalar(g, v + (size_t)c * g->total, pt);
+}
+
+/* problems.cpp:343-372 */
+int og_move_nodes(const og_grid* g, const double* u, const double* f_raw, double raw_integral, double t,
+                  int steps, double* pos) {
+    if (steps < 1) return OG_INVALID;
+    const uint64_t T = g->total;
+    const int N = g->N;
+    double* grad = (double*)malloc((size_t)g->dim * T * sizeof(double));
+    og_gradient(g, u, grad);
+    for (uint64_t p = 0; p < T; ++p) {
+        const int i = (int)(p % (uint64_t)N), j = (int)((p / (uint64_t)N) % (uint64_t)N),
+                  k = (int)(p / ((uint64_t)N * (uint64_t)N));
+        pos[3 * p] = i * g->h;
+        pos[3 * p + 1] = j * g->h;
+        pos[3 * p + 2] = g->dim == 3 ? k * g->h : 0.0;
+    }
+    const double dt = t / steps;
+    for (int s = 0; s < steps; ++s) {
+        const double tau = s * dt;
+        for (uint64_t p = 0; p < T; ++p) {
+            double* x = pos + 3 * p;
+            const double den = tau * og_sample_scalar(g, f_raw, x) + raw_integral;
+            if (den == 0.0) continue;
+            for (int c = 0; c < g->dim; ++c) {
+                const double gc = og_sample_scalar(g, grad + (size_t)c * T, x);
+                x[c] = og_clampd(x[c] - dt * gc / den, 0.0, 1.0);
+            }
+        }
+    }
+    free(grad);
+    return OG_OK;
+}
+
+static int og_inside_unit(const double* p, int dim) {
+    for (int c = 0; c < dim; ++c)
+        if (!(p[c] >= 0.0 && p[c] <= 1.0)) return 0;
+    return 1;
+}
+
+static double og_norm3(const double* a) { return sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]); }
+
+/* problems.cpp:415-455 */
+int og_integrate_streamline(const og_grid* g, const double* v, const double* seed, double step, int max_steps,
+                            double* pts, int* stop) {
+    int cnt = 0;
+    double p[3] = {seed[0], seed[1], seed[2]};
+#define OG_PUSH(q) do { pts[3 * cnt] = (q)[0]; pts[3 * cnt + 1] = (q)[1]; pts[3 * cnt + 2] = (q)[2]; ++cnt; } while (0)
+    OG_PUSH(p);
+    *stop = 0;
+    if (!og_inside_unit(p, g->dim)) {
+        *stop = 1;
+        return cnt;
+    }
+    for (int s = 0; s < max_steps; ++s) {
+        double k1[3], k2[3], k3[3], k4[3], q[3], nx[3];
+        og_sample_vector(g, v, g->dim, p, k1);
+        if (og_norm3(k1) < 1e-12) { *stop = 2; return cnt; }
+        for (int c = 0; c < 3; ++c) q[c] = p[c] + 0.5 * step * k1[c];
+        if (!og_inside_unit(q, g->dim)) { *stop = 1; return cnt; }
+        og_sample_vector(g, v, g->dim, q, k2);
+        for (int c = 0; c < 3; ++c) q[c] = p[c] + 0.5 * step * k2[c];
+        if (!og_inside_unit(q, g->dim)) { *stop = 1; return cnt; }
+        og_sample_vector(g, v, g->dim, q, k3);
+        for (int c = 0; c < 3; ++c) q[c] = p[c] + step * k3[c];
+        if (!og_inside_unit(q, g->dim)) { *stop = 1; return cnt; }
+        og_sample_vector(g, v, g->dim, q, k4);
+        for (int c = 0; c < 3; ++c) nx[c] = p[c];
+        for (int c = 0; c < 3; ++c) nx[c] += step / 6.0 * (k1[c] + 2.0 * k2[c] + 2.0 * k3[c] + k4[c]);
+        if (!og_inside_unit(nx, g->dim)) { *stop = 1; return cnt; }
+        for (int c = 0; c < 3; ++c) p[c] = nx[c];
+        OG_PUSH(p);
+    }
+#undef OG_PUSH
+    return cnt;
+}

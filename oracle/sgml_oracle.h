@@ -121,6 +121,23 @@ void og_fill_sinsin2d(const og_grid* g, double* f);
 void og_fill_capacitor_sigma(const og_grid* g, double sign, double* sigma);
 void og_lcg_fill(double* f, uint64_t total, uint64_t seed);
 
+/* post-solve fields (problems.cpp:40-97, 327-455).  Vector fields are
+ * component-major: comp c at v + c * total.  Points are xyz triples. */
+void og_axis_derivative(const og_grid* g, const double* u, int axis, double* out);
+void og_gradient(const og_grid* g, const double* u, double* out);            /* dim comps */
+void og_curl(const og_grid* g, const double* psi, double* out);             /* 3D, 3 comps */
+void og_divergence(const og_grid* g, const double* v, double* out);         /* dim comps in */
+int og_deformation_velocity(const og_grid* g, const double* u, const double* f_raw, double raw_integral,
+                            double t, double* out);                           /* OG_INVALID on den == 0 */
+int og_move_nodes(const og_grid* g, const double* u, const double* f_raw, double raw_integral, double t,
+                  int steps, double* pos);                                    /* total xyz triples */
+double og_sample_scalar(const og_grid* g, const double* f, const double* p);
+void og_sample_vector(const og_grid* g, const double* v, int nv, const double* p, double* out);
+/* returns the number of points written (<= max_steps + 1); *stop = 0 max_steps,
+ * 1 left_domain, 2 stagnation */
+int og_integrate_streamline(const og_grid* g, const double* v, const double* seed, double step, int max_steps,
+                            double* pts, int* stop);
+
 #ifdef __cplusplus
 }
 #endif

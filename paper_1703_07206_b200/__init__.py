@@ -8,5 +8,6 @@ C-ABI.  There is no CPU fallback.
 from ._capi import LIB_PATH, SgmlError, device_count, header_symbols, kernel_error  # noqa: F401
 from .api import *  # noqa: F401,F403
 from .api import Work  # noqa: F401
+from .problems import *  # noqa: F401,F403
 
 __version__ = "0.1.0"

@@ -115,6 +115,15 @@ _SIGNATURES = {
     "sgml_ctx_clique": ([_P, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     "sgml_slab_plan": ([C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                         C.POINTER(C.c_int)], C.c_int),
+    "sgml_axis_derivative": ([_P, C.c_int, _P], C.c_int),
+    "sgml_gradient": ([_P, C.POINTER(_P)], C.c_int),
+    "sgml_curl": ([C.POINTER(_P), C.POINTER(_P)], C.c_int),
+    "sgml_divergence": ([C.POINTER(_P), _P], C.c_int),
+    "sgml_deformation_velocity": ([_P, _P, C.c_double, C.c_double, C.POINTER(_P)], C.c_int),
+    "sgml_move_nodes": ([_P, _P, C.c_double, C.c_double, C.c_int, C.POINTER(_P)], C.c_int),
+    "sgml_sample_vector": ([C.POINTER(_P), C.c_int, _D, C.c_int, _D], C.c_int),
+    "sgml_integrate_streamlines": ([C.POINTER(_P), _D, C.c_int, C.c_double, C.c_int, _D,
+                                    C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     "sgml_host_alloc": ([C.c_uint64, C.POINTER(_P)], C.c_int),
     "sgml_host_free": ([_P], C.c_int),
 }

@@ -54,6 +54,22 @@ double slot_to_double(unsigned long long bits) {
     return d;
 }
 
+
+// RAII device scratch (post-solve temporaries)
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(size_t bytes) { SGML_CUDA(cudaMalloc(&p, bytes ? bytes : 1)); }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    double* d() const { return static_cast<double*>(p); }
+    int* i() const { return static_cast<int*>(p); }
+};
+
+double inv2h_of(const sgml_grid& g) { return 1.0 / (2.0 * g.h); }  // problems.cpp:80
+
 }  // namespace
 
 extern "C" {
@@ -627,6 +643,174 @@ int sgml_host_alloc(uint64_t bytes, void** out) {
 int sgml_host_free(void* p) {
     return guarded([&] {
         if (p) SGML_CUDA(cudaFreeHost(p));
+    });
+}
+
+// ---- post-solve fields (problems.hpp:100-148) --------------------------------
+
+int sgml_axis_derivative(const sgml_field* u, int axis, sgml_field* out) {
+    return guarded([&] {
+        same_grid(u, out, "axis_derivative: grid mismatch");
+        require(axis >= 0 && axis < u->grid.dim, SGML_EINVAL, "axis_derivative: axis out of range");
+        activate(u->ctx);
+        const sgml_grid& g = u->grid;
+        launch_axis_derivative(g.dim, u->d, out->d, g.N, axis, inv2h_of(g), u->ctx->stream);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaStreamSynchronize(u->ctx->stream));
+    });
+}
+
+int sgml_gradient(const sgml_field* u, sgml_field* const* out) {
+    return guarded([&] {
+        require(u && out, SGML_EINVAL, "gradient: null argument");
+        const sgml_grid& g = u->grid;
+        double* o[3] = {nullptr, nullptr, nullptr};
+        for (int c = 0; c < g.dim; ++c) {
+            same_grid(u, out[c], "gradient: grid mismatch");
+            o[c] = out[c]->d;
+        }
+        activate(u->ctx);
+        launch_gradient(g.dim, u->d, o, g.N, inv2h_of(g), nullptr, 0.0, 0.0, nullptr, u->ctx->stream);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaStreamSynchronize(u->ctx->stream));
+    });
+}
+
+int sgml_curl(const sgml_field* const* psi, sgml_field* const* out) {
+    return guarded([&] {
+        require(psi && out && psi[0], SGML_EINVAL, "curl: null argument");
+        const sgml_grid& g = psi[0]->grid;
+        require(g.dim == 3, SGML_EINVAL, "curl: defined for 3D fields");
+        const double* p[3];
+        double* o[3];
+        for (int c = 0; c < 3; ++c) {
+            same_grid(psi[0], psi[c], "curl: grid mismatch");
+            same_grid(psi[0], out[c], "curl: grid mismatch");
+            p[c] = psi[c]->d;
+            o[c] = out[c]->d;
+        }
+        activate(psi[0]->ctx);
+        launch_curl(p, o, g.N, inv2h_of(g), psi[0]->ctx->stream);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaStreamSynchronize(psi[0]->ctx->stream));
+    });
+}
+
+int sgml_divergence(const sgml_field* const* v, sgml_field* out) {
+    return guarded([&] {
+        require(v && out && v[0], SGML_EINVAL, "divergence: null argument");
+        const sgml_grid& g = out->grid;
+        const double* p[3] = {nullptr, nullptr, nullptr};
+        for (int c = 0; c < g.dim; ++c) {
+            same_grid(out, v[c], "divergence: grid mismatch");
+            p[c] = v[c]->d;
+        }
+        activate(out->ctx);
+        launch_divergence(g.dim, p, out->d, g.N, inv2h_of(g), out->ctx->stream);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaStreamSynchronize(out->ctx->stream));
+    });
+}
+
+int sgml_deformation_velocity(const sgml_field* u, const sgml_field* f_raw, double raw_integral, double t,
+                              sgml_field* const* out) {
+    return guarded([&] {
+        require(u && f_raw && out, SGML_EINVAL, "deformation_velocity: null argument");
+        same_grid(u, f_raw, "deformation_velocity: grid mismatch");
+        const sgml_grid& g = u->grid;
+        double* o[3] = {nullptr, nullptr, nullptr};
+        for (int c = 0; c < g.dim; ++c) {
+            same_grid(u, out[c], "deformation_velocity: grid mismatch");
+            o[c] = out[c]->d;
+        }
+        sgml_ctx* ctx = u->ctx;
+        activate(ctx);
+        const cudaStream_t s = ctx->stream;
+        SGML_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), s));
+        launch_gradient(g.dim, u->d, o, g.N, inv2h_of(g), f_raw->d, raw_integral, t, ctx->d_flags, s);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+        if (ctx->h_flags[0]) fail(SGML_EINVAL, "deformation_velocity: zero denominator");
+    });
+}
+
+int sgml_move_nodes(const sgml_field* u, const sgml_field* f_raw, double raw_integral, double t, int steps,
+                    sgml_field* const* pos) {
+    return guarded([&] {
+        require(u && f_raw && pos, SGML_EINVAL, "move_nodes: null argument");
+        if (steps < 1) fail(SGML_EINVAL, "move_nodes: steps must be >= 1");
+        same_grid(u, f_raw, "move_nodes: grid mismatch");
+        const sgml_grid& g = u->grid;
+        double* o[3] = {nullptr, nullptr, nullptr};
+        for (int c = 0; c < 3; ++c) {
+            if (c >= g.dim && !pos[c]) continue;
+            same_grid(u, pos[c], "move_nodes: grid mismatch");
+            o[c] = pos[c]->d;
+        }
+        sgml_ctx* ctx = u->ctx;
+        activate(ctx);
+        const cudaStream_t s = ctx->stream;
+        // grad(u) on the full grid first (problems.cpp:347)
+        DevBuf gb((size_t)g.dim * g.total * sizeof(double));
+        double* gr[3] = {gb.d(), gb.d() + g.total, g.dim == 3 ? gb.d() + 2 * g.total : nullptr};
+        launch_gradient(g.dim, u->d, gr, g.N, inv2h_of(g), nullptr, 0.0, 0.0, nullptr, s);
+        if (g.dim == 2 && o[2]) SGML_CUDA(cudaMemsetAsync(o[2], 0, g.total * sizeof(double), s));
+        launch_move_nodes(g.dim, gr, f_raw->d, raw_integral, g.N, g.h, t, steps, o, s);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int sgml_sample_vector(const sgml_field* const* v, int nv, const double* points, int count, double* out) {
+    return guarded([&] {
+        require(v && v[0] && points && out && count >= 0, SGML_EINVAL, "sample_vector: bad argument");
+        require(nv >= 1 && nv <= 3, SGML_EINVAL, "sample_vector: 1..3 components");
+        const sgml_grid& g = v[0]->grid;
+        const double* p[3] = {nullptr, nullptr, nullptr};
+        for (int c = 0; c < nv; ++c) {
+            same_grid(v[0], v[c], "sample_vector: grid mismatch");
+            p[c] = v[c]->d;
+        }
+        if (count == 0) return;
+        sgml_ctx* ctx = v[0]->ctx;
+        activate(ctx);
+        const cudaStream_t s = ctx->stream;
+        DevBuf pin((size_t)count * 3 * sizeof(double)), po((size_t)count * 3 * sizeof(double));
+        SGML_CUDA(cudaMemcpyAsync(pin.p, points, (size_t)count * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        launch_sample_points(g.dim, p, nv, g.N, g.h, pin.d(), count, po.d(), s);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaMemcpyAsync(out, po.p, (size_t)count * 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int sgml_integrate_streamlines(const sgml_field* const* v, const double* seeds, int nseeds, double step,
+                               int max_steps, double* points, int* counts, int* stops) {
+    return guarded([&] {
+        require(v && v[0] && seeds && points && counts && stops, SGML_EINVAL, "integrate_streamline: null argument");
+        if (!(step > 0.0)) fail(SGML_EINVAL, "integrate_streamline: step must be positive");
+        require(nseeds >= 0 && max_steps >= 0, SGML_EINVAL, "integrate_streamline: bad sizes");
+        const sgml_grid& g = v[0]->grid;
+        const double* p[3] = {nullptr, nullptr, nullptr};
+        for (int c = 0; c < g.dim; ++c) {
+            same_grid(v[0], v[c], "integrate_streamline: grid mismatch");
+            p[c] = v[c]->d;
+        }
+        if (nseeds == 0) return;
+        sgml_ctx* ctx = v[0]->ctx;
+        activate(ctx);
+        const cudaStream_t s = ctx->stream;
+        const size_t npts = (size_t)nseeds * (size_t)(max_steps + 1) * 3;
+        DevBuf sd((size_t)nseeds * 3 * sizeof(double)), pts(npts * sizeof(double)),
+            ci((size_t)nseeds * sizeof(int)), si((size_t)nseeds * sizeof(int));
+        SGML_CUDA(cudaMemcpyAsync(sd.p, seeds, (size_t)nseeds * 3 * sizeof(double), cudaMemcpyHostToDevice, s));
+        launch_streamlines(g.dim, p, g.N, g.h, sd.d(), nseeds, step, max_steps, pts.d(), ci.i(), si.i(), s);
+        SGML_CUDA(cudaGetLastError());
+        SGML_CUDA(cudaMemcpyAsync(points, pts.p, npts * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaMemcpyAsync(counts, ci.p, (size_t)nseeds * sizeof(int), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaMemcpyAsync(stops, si.p, (size_t)nseeds * sizeof(int), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
     });
 }
 

@@ -115,4 +115,23 @@ void launch_pyramid_ext(int dim, const double* in, const ExtLay& Lin, double* ou
 void launch_scatter_ext(int dim, const double* dense, double* ext, const ExtLay& L, cudaStream_t s);
 void launch_gather_ext(int dim, const double* ext, const ExtLay& L, double* dense, cudaStream_t s);
 
+// ---- post-solve fields (fields.cu; dense x-fastest layout) ----------------
+// axis_derivative (problems.cpp:74-97)
+void launch_axis_derivative(int dim, const double* u, double* d, int N, int axis, double inv2h, cudaStream_t s);
+// gradient (problems.cpp:391-396); with f_raw, deformation_velocity's
+// -g / (t f_raw + raw_integral) (problems.cpp:327-341), flag[0] on a zero denominator
+void launch_gradient(int dim, const double* u, double* const* g, int N, double inv2h, const double* f_raw,
+                     double raw_integral, double t, int* flag, cudaStream_t s);
+void launch_curl(const double* const* psi, double* const* v, int N, double inv2h, cudaStream_t s);
+void launch_divergence(int dim, const double* const* v, double* d, int N, double inv2h, cudaStream_t s);
+// move_nodes (problems.cpp:343-372) from the gradient fields g
+void launch_move_nodes(int dim, const double* const* g, const double* f_raw, double raw_integral, int N, double h,
+                       double t, int steps, double* const* pos, cudaStream_t s);
+// integrate_streamline (problems.cpp:415-455), one thread per seed
+void launch_streamlines(int dim, const double* const* v, int N, double h, const double* seeds, int nseeds,
+                        double step, int max_steps, double* pts, int* counts, int* stops, cudaStream_t s);
+// sample_vector (problems.cpp:407-413) at device points (3 doubles each)
+void launch_sample_points(int dim, const double* const* v, int nv, int N, double h, const double* pts, int count,
+                          double* out, cudaStream_t s);
+
 }  // namespace sgmlb

@@ -76,11 +76,11 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
         // rows / plane of this warp clear of the y / z faces by two nodes (no
         // Dirichlet node, no mirror ghost; warp-uniform)
         const bool rows_in = (DIM == 2 || (Kg >= 2 && Kg <= Nw - 3)) && s0 >= 2 && node_j(ncopy - 1) <= Nw - 3;
-        // interior fast path of a lane: also clear of the x faces; frel = 1.
+        // fast path (warp-uniform): rows / plane clear of the y / z faces,
+        // frel = 1; the x faces are handled inline (lanes at the row ends).
         // The level-(w+1) nodes (even x at even rows / planes; both copies
         // have the row parity of s0 when D is even) take ufine, loaded up front
-        const bool inner = rows_in && frel == 1 && X4 >= 2 && X4 + MV <= Nw - 2 &&
-                           (!ufine || (D & 1) == 0);
+        const bool inner = rows_in && frel == 1 && (!ufine || (D & 1) == 0);
         const bool rowfine = inner && ufine && ((s0 | Kg) & 1) == 0;
         double uf[NC][2];
 #pragma unroll
@@ -209,20 +209,45 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
         }
         // final values (Dirichlet faces, ufine nodes) and the checks
         if (inner) {
+            // lane holding node 0, 1, Nw - 2 or Nw - 1: x-face values and mirrors
+            const bool xedge = X4 < 2 || X4 + MV > Nw - 2;
+            const double vx0 = homogeneous ? 0.0 : bc.val[0], vx1 = homogeneous ? 0.0 : bc.val[1];
 #pragma unroll
             for (int cp = 0; cp < NC; ++cp) {
                 if (cp >= ncopy) break;
                 double* po = out + (int)eix<DIM>(Lw, X4, node_j(cp), K);
+                double v[MV];
+#pragma unroll
+                for (int k = 0; k < MV; ++k) v[k] = (rowfine && (k & 1) == 0) ? uf[cp][k >> 1] : val[cp][k];
+                if (xedge) {
+#pragma unroll
+                    for (int k = 0; k < MV; ++k) {
+                        const int I = X4 + k;
+                        if (I == 0 && !bc.neu[0]) v[k] = vx0;
+                        if (I == Nw - 1 && !bc.neu[1]) v[k] = vx1;
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < MV; ++k) {
-                    double value = val[cp][k];
-                    if (rowfine && (k & 1) == 0) value = uf[cp][k >> 1];
-                    const unsigned hi = (unsigned)__double2hiint(value) & 0x7fffffffu;
+                    if (k >= nv) break;
+                    const unsigned hi = (unsigned)__double2hiint(v[k]) & 0x7fffffffu;
                     bad |= hi >= 0x7ff00000u;
-                    const unsigned key = hi | min((unsigned)__double2loint(value), 1u);
+                    const unsigned key = hi | min((unsigned)__double2loint(v[k]), 1u);
                     tiny |= key - 1u < 0x035fffffu;
-                    po[k] = value;
+                    po[k] = v[k];
                 }
+                if (xedge) {
+#pragma unroll
+                    for (int k = 0; k < MV; ++k) {
+                        if (k >= nv) break;
+                        const int I = X4 + k;
+                        if (I == 1) po[k - 2] = v[k];       // even mirror: ghost -1
+                        if (I == Nw - 2) po[k + 2] = v[k];  // ghost Nw (both when Nw == 3)
+                    }
+                }
+                // Dirichlet x-high face: the last group also writes node Nw - 1 (the
+                // grid stops at Nw - 2, so no block is spent on that column)
+                if (xtail && X4 + MV == Nw - 1) po[MV] = vx1;
             }
         } else {
 #pragma unroll

@@ -18,6 +18,7 @@
 #include "../../include/sgml/cycle.hpp"
 #include "../../include/sgml/grid.hpp"
 #include "../../include/sgml/kernels.hpp"
+#include "../../include/sgml/problems.hpp"
 #include "../../include/sgml_b200.h"
 
 namespace sgml {
@@ -352,6 +353,105 @@ double l1_error(const Field& v_h, const ExactSolution& exact) {
     }
     if (den == 0.0) throw std::invalid_argument("l1_error: exact solution is identically zero");
     return num / den;
+}
+
+// ---- problems.hpp (post-solve fields, problems.cpp:327-455) -----------------
+
+namespace {
+
+// device copies of the dim (or 3) components of a host vector field
+struct DevVec {
+    std::vector<std::unique_ptr<Dev>> c;
+    std::vector<sgml_field*> h;
+    DevVec(const VectorField& v, int n) {
+        for (int k = 0; k < n; ++k) {
+            c.push_back(std::make_unique<Dev>(v.comp[k]));
+            h.push_back(c.back()->f);
+        }
+    }
+    DevVec(const Grid& g, int n) {
+        for (int k = 0; k < n; ++k) {
+            c.push_back(std::make_unique<Dev>(g));
+            h.push_back(c.back()->f);
+        }
+    }
+    void to(VectorField& v, int n) const {
+        for (int k = 0; k < n; ++k) c[k]->to(v.comp[k]);
+    }
+};
+
+}  // namespace
+
+VectorField gradient(const Field& u) {
+    const Grid& g = u.grid();
+    Dev du(u);
+    DevVec out(g, g.dim);
+    check(sgml_gradient(du.f, out.h.data()));
+    VectorField v(g);
+    out.to(v, g.dim);
+    return v;
+}
+
+VectorField curl(const VectorField& psi) {
+    if (psi.dim != 3) throw std::invalid_argument("curl: defined for 3D fields");
+    const Grid& g = psi.grid();
+    DevVec in(psi, 3), out(g, 3);
+    check(sgml_curl(in.h.data(), out.h.data()));
+    VectorField v(g);
+    out.to(v, 3);
+    return v;
+}
+
+Field divergence(const VectorField& v) {
+    const Grid& g = v.grid();
+    DevVec in(v, v.dim);
+    Dev out(g);
+    check(sgml_divergence(in.h.data(), out.f));
+    Field d(g);
+    out.to(d);
+    return d;
+}
+
+VectorField deformation_velocity(const Field& u, const Field& f_raw, double raw_integral, double t) {
+    const Grid& g = u.grid();
+    Dev du(u), df(f_raw);
+    DevVec out(g, g.dim);
+    check(sgml_deformation_velocity(du.f, df.f, raw_integral, t, out.h.data()));
+    VectorField v(g);
+    out.to(v, g.dim);
+    return v;
+}
+
+std::vector<Point> move_nodes(const Field& u, const Field& f_raw, double raw_integral, double t, int steps) {
+    if (steps < 1) throw std::invalid_argument("move_nodes: steps must be >= 1");
+    const Grid& g = u.grid();
+    Dev du(u), df(f_raw);
+    DevVec pos(g, 3);
+    check(sgml_move_nodes(du.f, df.f, raw_integral, t, steps, pos.h.data()));
+    VectorField p(g);
+    pos.to(p, 3);
+    std::vector<Point> out(g.total);
+    for (std::size_t q = 0; q < g.total; ++q) out[q] = {p.comp[0][q], p.comp[1][q], p.comp[2][q]};
+    return out;
+}
+
+Point sample_vector(const VectorField& v, const Point& p) {
+    DevVec in(v, v.dim);
+    Point out{0.0, 0.0, 0.0};
+    check(sgml_sample_vector(in.h.data(), v.dim, p.data(), 1, out.data()));
+    return out;
+}
+
+Streamline integrate_streamline(const VectorField& v, const Point& seed, double step, int max_steps) {
+    if (!(step > 0.0)) throw std::invalid_argument("integrate_streamline: step must be positive");
+    DevVec in(v, v.dim);
+    std::vector<double> pts(3 * (static_cast<std::size_t>(max_steps > 0 ? max_steps : 0) + 1));
+    int count = 0, stop = 0;
+    check(sgml_integrate_streamlines(in.h.data(), seed.data(), 1, step, max_steps, pts.data(), &count, &stop));
+    Streamline line;
+    for (int q = 0; q < count; ++q) line.points.push_back({pts[3 * q], pts[3 * q + 1], pts[3 * q + 2]});
+    line.stop = static_cast<StreamlineStop>(stop);
+    return line;
 }
 
 }  // namespace sgml

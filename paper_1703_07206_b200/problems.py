@@ -1,0 +1,134 @@
+"""Post-solve fields of the reference's experiments (problems.hpp:100-148)
+on the device: difference fields, deformation velocity, node motion and RK4
+streamlines.  Each call runs the sm_100a kernels of csrc/fields.cu through
+the C-ABI; results are the reference's bits (problems.cpp:40-97, 327-455).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+from ._capi import check, lib
+from .api import Field, Grid
+
+__all__ = ["VectorField", "StreamlineStop", "Streamline", "axis_derivative", "gradient", "curl", "divergence",
+           "deformation_velocity", "move_nodes", "sample_vector", "integrate_streamline",
+           "integrate_streamlines"]
+
+
+def _handles(fields: Sequence[Optional[Field]]):
+    arr = (C.c_void_p * len(fields))(*[f.handle.value if f is not None else None for f in fields])
+    return arr
+
+
+class VectorField:
+    """problems.hpp:31-39: three component fields, comp[2] unused in 2D."""
+
+    def __init__(self, grid: Grid, comps: Optional[Sequence[Field]] = None, ctx=None):
+        self.grid = grid
+        self.dim = grid.dim
+        if comps is None:
+            comps = [Field(grid, ctx=ctx) for _ in range(3)]
+        self.comp = list(comps)
+
+    @classmethod
+    def from_numpy(cls, grid: Grid, arrays, ctx=None) -> "VectorField":
+        comps = [Field.from_numpy(grid, a, ctx=ctx) for a in arrays]
+        while len(comps) < 3:
+            comps.append(Field(grid, ctx=ctx))
+        return cls(grid, comps)
+
+    def numpy(self) -> np.ndarray:
+        return np.stack([c.numpy() for c in self.comp])
+
+
+class StreamlineStop(enum.IntEnum):
+    """problems.hpp:139"""
+    max_steps = 0
+    left_domain = 1
+    stagnation = 2
+
+
+@dataclass
+class Streamline:
+    points: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    stop: StreamlineStop = StreamlineStop.max_steps
+
+
+def axis_derivative(u: Field, axis: int) -> Field:
+    """problems.cpp:74-97"""
+    out = Field(u.grid, ctx=u.ctx)
+    check(lib().sgml_axis_derivative(u.handle, int(axis), out.handle))
+    return out
+
+
+def gradient(u: Field) -> VectorField:
+    """problems.cpp:391-396"""
+    v = VectorField(u.grid, ctx=u.ctx)
+    check(lib().sgml_gradient(u.handle, _handles(v.comp)))
+    return v
+
+
+def curl(psi: VectorField) -> VectorField:
+    """problems.cpp:376-389 (3D only: ValueError otherwise)"""
+    v = VectorField(psi.grid, ctx=psi.comp[0].ctx)
+    check(lib().sgml_curl(_handles(psi.comp), _handles(v.comp)))
+    return v
+
+
+def divergence(v: VectorField) -> Field:
+    """problems.cpp:398-405"""
+    out = Field(v.grid, ctx=v.comp[0].ctx)
+    check(lib().sgml_divergence(_handles(v.comp), out.handle))
+    return out
+
+
+def deformation_velocity(u: Field, f_raw: Field, raw_integral: float, t: float) -> VectorField:
+    """problems.cpp:327-341 (ValueError on a zero denominator)"""
+    v = VectorField(u.grid, ctx=u.ctx)
+    check(lib().sgml_deformation_velocity(u.handle, f_raw.handle, float(raw_integral), float(t),
+                                          _handles(v.comp)))
+    return v
+
+
+def move_nodes(u: Field, f_raw: Field, raw_integral: float, t: float, steps: int) -> VectorField:
+    """problems.cpp:343-372: node positions as coordinate fields (x, y, z)."""
+    pos = VectorField(u.grid, ctx=u.ctx)
+    check(lib().sgml_move_nodes(u.handle, f_raw.handle, float(raw_integral), float(t), int(steps),
+                                _handles(pos.comp)))
+    return pos
+
+
+def sample_vector(v: VectorField, points) -> np.ndarray:
+    """problems.cpp:407-413 at one point (3,) or many (m, 3)."""
+    p = np.ascontiguousarray(points, np.float64)
+    one = p.ndim == 1
+    p = p.reshape(-1, 3)
+    out = np.zeros_like(p)
+    check(lib().sgml_sample_vector(_handles(v.comp), v.dim, p.ctypes.data_as(_capi._D), p.shape[0],
+                                   out.ctypes.data_as(_capi._D)))
+    return out[0] if one else out
+
+
+def integrate_streamlines(v: VectorField, seeds, step: float, max_steps: int) -> list:
+    """problems.cpp:415-455 for several seeds (one device thread each)."""
+    sd = np.ascontiguousarray(seeds, np.float64).reshape(-1, 3)
+    m = sd.shape[0]
+    pts = np.zeros((m, max_steps + 1, 3))
+    counts = np.zeros(m, np.int32)
+    stops = np.zeros(m, np.int32)
+    check(lib().sgml_integrate_streamlines(_handles(v.comp), sd.ctypes.data_as(_capi._D), m, float(step),
+                                           int(max_steps), pts.ctypes.data_as(_capi._D),
+                                           counts.ctypes.data_as(C.POINTER(C.c_int)),
+                                           stops.ctypes.data_as(C.POINTER(C.c_int))))
+    return [Streamline(pts[s, :counts[s]].copy(), StreamlineStop(int(stops[s]))) for s in range(m)]
+
+
+def integrate_streamline(v: VectorField, seed, step: float, max_steps: int) -> Streamline:
+    """problems.cpp:415-455"""
+    return integrate_streamlines(v, [seed], step, max_steps)[0]

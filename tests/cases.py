@@ -145,3 +145,27 @@ SOLVE_CASES = [
     ("capacitor_high", 3), ("capacitor_low", 4), ("neumann2d_a", 4), ("neumann2d", 5),
     ("mixed2d", 5), ("mixed3d_a", 3), ("sigma3d_dirichlet", 3), ("zero_source_dirichlet1", 3),
 ]
+
+
+# ------------------------------------------------- post-solve fields ----
+# problems.cpp:40-97, 327-455 on deterministic inputs (tests/golden, parity)
+
+FIELD_GRIDS = [(2, 3), (2, 5), (3, 3), (3, 4)]
+
+
+def field_inputs(dim: int, n: int) -> dict:
+    g = O.make_grid(dim, n)
+    T = g.total
+    u = O.lcg(g, 101 + dim)
+    psi = np.stack([O.lcg(g, 111 + c) for c in range(3)])
+    v = np.stack([O.lcg(g, 121 + c) for c in range(dim)])
+    f_raw = np.abs(O.lcg(g, 131)) + 0.25
+    # a smooth swirl (streamlines that run for many steps) plus a random field
+    x = (np.arange(T) % g.N) * g.h
+    y = ((np.arange(T) // g.N) % g.N) * g.h
+    swirl = [-(y - 0.5), x - 0.5] + ([0.1 * np.ones(T)] if dim == 3 else [])
+    seeds = np.array([[0.7, 0.5, 0.5], [0.31, 0.62, 0.44], [0.5, 0.5, 0.5], [1.2, 0.5, 0.5]])
+    if dim == 2:
+        seeds[:, 2] = 0.0
+    return {"g": g, "u": u, "psi": psi, "v": v, "f_raw": f_raw, "swirl": np.stack(swirl),
+            "seeds": seeds, "raw_integral": 1.5, "t": 0.35, "steps": 6, "step": 0.02, "max_steps": 120}

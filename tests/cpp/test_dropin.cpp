@@ -13,6 +13,7 @@
 #include "sgml/cycle.hpp"
 #include "sgml/grid.hpp"
 #include "sgml/kernels.hpp"
+#include "sgml/problems.hpp"
 
 extern "C" {
 #include "sgml_oracle.h"
@@ -264,6 +265,55 @@ static void test_driver_edges() {
     EXPECT(throws<std::invalid_argument>([&] { restrict_sigma_levels(neg, 3); }));
 }
 
+// problems_tests.cpp:165-309 through the drop-in header, bitwise against the oracle
+static void test_post_solve_fields() {
+    const Grid g = make_grid(3, 4);
+    og_grid og = og_of(g);
+    VectorField psi(g);
+    std::vector<double> flat(3 * g.total);
+    for (int c = 0; c < 3; ++c) {
+        og_lcg_fill(psi.comp[c].data(), g.total, 500 + c);
+        std::memcpy(flat.data() + c * g.total, psi.comp[c].data(), g.total * sizeof(double));
+    }
+    const VectorField v = curl(psi);
+    std::vector<double> want(3 * g.total);
+    og_curl(&og, flat.data(), want.data());
+    for (int c = 0; c < 3; ++c)
+        EXPECT(same_bits(v.comp[c], std::vector<double>(want.begin() + c * g.total, want.begin() + (c + 1) * g.total)));
+    const Field d = divergence(v);
+    std::vector<double> vflat(3 * g.total), dwant(g.total);
+    for (int c = 0; c < 3; ++c) std::memcpy(vflat.data() + c * g.total, v.comp[c].data(), g.total * sizeof(double));
+    og_divergence(&og, vflat.data(), dwant.data());
+    EXPECT(same_bits(d, dwant));
+    const VectorField gr = gradient(psi.comp[0]);
+    std::vector<double> gwant(3 * g.total);
+    og_gradient(&og, psi.comp[0].data(), gwant.data());
+    EXPECT(same_bits(gr.comp[1], std::vector<double>(gwant.begin() + g.total, gwant.begin() + 2 * g.total)));
+    EXPECT(throws<std::invalid_argument>([&] { curl(VectorField(make_grid(2, 3))); }));
+
+    // deformation velocity and node motion (problems_tests.cpp:165-189)
+    const Grid g2 = make_grid(2, 3);
+    Field u(g2), f_raw(g2);
+    for (std::size_t p = 0; p < u.size(); ++p) u[p] = 2.0 * u.node_of(p).i * g2.h;
+    const VectorField dv = deformation_velocity(u, f_raw, 4.0, 0.7);
+    EXPECT(std::abs(dv.comp[0].at(3, 3) + 0.5) <= 1e-13);
+    EXPECT(throws<std::invalid_argument>([&] { deformation_velocity(u, f_raw, 0.0, 0.0); }));
+    const std::vector<Point> pos = move_nodes(Field(g2), f_raw, 1.0, 0.5, 10);
+    EXPECT(pos.size() == g2.total && pos[7][0] == 7 * g2.h);
+    EXPECT(throws<std::invalid_argument>([&] { move_nodes(u, f_raw, 1.0, 0.5, 0); }));
+
+    // streamline contract (problems_tests.cpp:281-309)
+    VectorField drift(g2);
+    drift.comp[0].fill(1.0);
+    const Streamline out = integrate_streamline(drift, {0.75, 0.5, 0.0}, 0.1, 100);
+    EXPECT(out.stop == StreamlineStop::left_domain && out.points.size() >= 2);
+    EXPECT(std::abs(out.points[1][0] - 0.85) <= 1e-13);
+    const Streamline stall = integrate_streamline(VectorField(g2), {0.5, 0.5, 0.0}, 0.1, 100);
+    EXPECT(stall.stop == StreamlineStop::stagnation && stall.points.size() == 1);
+    const Point s = sample_vector(drift, {0.317, 0.682, 0.0});
+    EXPECT(s[0] == 1.0 && s[1] == 0.0 && s[2] == 0.0);
+}
+
 int main() {
     const std::vector<std::pair<const char*, void (*)()>> tests = {
         {"schedule", test_schedule},
@@ -271,6 +321,7 @@ int main() {
         {"capacitor_bitwise", test_capacitor_bitwise},
         {"kernels", test_kernels},
         {"driver_edges", test_driver_edges},
+        {"post_solve_fields", test_post_solve_fields},
     };
     for (const auto& [name, fn] : tests) {
         const int before = failures;

@@ -41,7 +41,7 @@ def main() -> None:
     O.build(with_ref=True)
     if O.ref_lib() is None:
         raise SystemExit("reference build unavailable")
-    out = {"relax": {}, "restriction": {}, "residual": {}, "solve": {}, "schedule": {}}
+    out = {"relax": {}, "restriction": {}, "residual": {}, "solve": {}, "schedule": {}, "fields": {}}
     arrays = {}
 
     for case in K.relax_cases(full=False):
@@ -94,11 +94,31 @@ def main() -> None:
         for n_r in (1, 2, 3, 8):
             out["schedule"][key(n, n_r)] = int(O.ref_lib().ref_closed_form_work_units(n, n_r))
 
+    for dim, n in K.FIELD_GRIDS:
+        d = K.field_inputs(dim, n)
+        g = d["g"]
+        rec = {"gradient": digest(O.gradient(g, d["u"], impl="ref")),
+               "divergence": digest(O.divergence(g, d["v"], impl="ref"))}
+        if dim == 3:
+            rec["curl"] = digest(O.curl(g, d["psi"], impl="ref"))
+        st, vel = O.deformation_velocity(g, d["u"], d["f_raw"], d["raw_integral"], d["t"], impl="ref")
+        rec["deformation_velocity"] = [st, digest(vel)]
+        st, pos = O.move_nodes(g, 0.01 * d["u"], d["f_raw"], d["raw_integral"], d["t"], d["steps"], impl="ref")
+        rec["move_nodes"] = [st, digest(pos)]
+        lines = []
+        for field in ("swirl", "v"):
+            for seed in d["seeds"]:
+                pts, stop = O.integrate_streamline(g, d[field], seed, d["step"], d["max_steps"], impl="ref")
+                lines.append([field, len(pts), stop, digest(pts)])
+        rec["streamlines"] = lines
+        rec["sample"] = [digest(O.sample_vector(g, d["v"], p, impl="ref")) for p in d["seeds"]]
+        out["fields"][key(dim, n)] = rec
+
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, indent=0, sort_keys=True)
     np.savez_compressed(os.path.join(HERE, "arrays.npz"), **arrays)
     print("relax", len(out["relax"]), "restriction", len(out["restriction"]), "residual",
-          len(out["residual"]), "solve", len(out["solve"]), "arrays", len(arrays))
+          len(out["residual"]), "solve", len(out["solve"]), "fields", len(out["fields"]), "arrays", len(arrays))
 
 
 if __name__ == "__main__":

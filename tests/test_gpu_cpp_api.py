@@ -18,4 +18,4 @@ def test_cpp_dropin_api():
     out = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert out.stdout.count("PASS") == 5
+    assert out.stdout.count("PASS") == 6

@@ -1,0 +1,126 @@
+"""GPU parity of the post-solve operators (csrc/fields.cu) against the
+pinned C restatement (tests/test_oracle_fields.py): bit-identical fp64,
+-0.0 folded into +0.0."""
+import math
+
+import numpy as np
+import pytest
+
+import cases as K
+from cases import O
+import paper_1703_07206_b200 as S
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    assert S.device_count() >= 1, "no CUDA device: GPU tests must run on the B200 box"
+    S.default_context()
+
+
+def sgrid(g):
+    return S.make_grid(g.dim, g.n)
+
+
+def dev(g, a):
+    return S.Field.from_numpy(sgrid(g), a)
+
+
+def vdev(g, arrays):
+    return S.VectorField.from_numpy(sgrid(g), arrays)
+
+
+GRIDS = K.FIELD_GRIDS + [(2, 7), (3, 6)]
+
+
+@pytest.mark.parametrize("dim,n", GRIDS)
+def test_difference_fields_bitwise(dim, n):
+    d = K.field_inputs(dim, n)
+    g = d["g"]
+    u = dev(g, d["u"])
+    for axis in range(dim):
+        assert K.bits_equal(S.axis_derivative(u, axis).numpy(), O.axis_derivative(g, d["u"], axis))
+    grad = S.gradient(u).numpy()
+    assert K.bits_equal(grad[:dim], O.gradient(g, d["u"]))
+    assert K.bits_equal(S.divergence(vdev(g, d["v"])).numpy(), O.divergence(g, d["v"]))
+    if dim == 3:
+        assert K.bits_equal(S.curl(vdev(g, d["psi"])).numpy(), O.curl(g, d["psi"]))
+    else:
+        with pytest.raises(ValueError):
+            S.curl(vdev(g, d["psi"][:2]))
+
+
+@pytest.mark.parametrize("dim,n", GRIDS)
+def test_deformation_velocity_and_move_nodes_bitwise(dim, n):
+    d = K.field_inputs(dim, n)
+    g = d["g"]
+    st, vel = O.deformation_velocity(g, d["u"], d["f_raw"], d["raw_integral"], d["t"])
+    assert st == 0
+    got = S.deformation_velocity(dev(g, d["u"]), dev(g, d["f_raw"]), d["raw_integral"], d["t"]).numpy()
+    assert K.bits_equal(got[:dim], vel)
+    u = 0.01 * d["u"]
+    st, pos = O.move_nodes(g, u, d["f_raw"], d["raw_integral"], d["t"], d["steps"])
+    got = S.move_nodes(dev(g, u), dev(g, d["f_raw"]), d["raw_integral"], d["t"], d["steps"]).numpy()
+    assert K.bits_equal(got.T, pos)
+
+
+def test_field_errors_follow_the_reference():
+    g = O.make_grid(2, 3)
+    x = (np.arange(g.total) % g.N) * g.h
+    u, z = dev(g, 2.0 * x), dev(g, np.zeros(g.total))
+    with pytest.raises(ValueError):  # problems.cpp:334-335
+        S.deformation_velocity(u, z, 0.0, 0.0)
+    with pytest.raises(ValueError):  # problems.cpp:345
+        S.move_nodes(u, z, 1.0, 0.5, 0)
+    with pytest.raises(ValueError):  # problems.cpp:417
+        S.integrate_streamline(S.gradient(u), [0.5, 0.5, 0.0], 0.0, 10)
+
+
+@pytest.mark.parametrize("dim,n", GRIDS)
+def test_streamlines_and_samples_bitwise(dim, n):
+    d = K.field_inputs(dim, n)
+    g = d["g"]
+    for name in ("swirl", "v"):
+        v = vdev(g, d[name])
+        lines = S.integrate_streamlines(v, d["seeds"], d["step"], d["max_steps"])
+        for seed, line in zip(d["seeds"], lines):
+            pts, stop = O.integrate_streamline(g, d[name], seed, d["step"], d["max_steps"])
+            assert int(line.stop) == stop
+            assert K.bits_equal(line.points, pts)
+        got = S.sample_vector(v, d["seeds"])
+        want = np.stack([O.sample_vector(g, d[name], p) for p in d["seeds"]])
+        assert K.bits_equal(got, want)
+
+
+def test_rk4_orbit_closes_on_device():
+    # acceptance_main.cpp:287-309
+    g = O.make_grid(2, 5)
+    T = np.arange(g.total)
+    x, y = (T % g.N) * g.h, ((T // g.N) % g.N) * g.h
+    om = 2.0 * 3.14159265358979323846 / 6.0
+    rot = np.stack([-om * (y - 0.5), om * (x - 0.5)])
+    line = S.integrate_streamline(vdev(g, rot), [0.75, 0.5, 0.0], 1e-3, 6000)
+    pts, stop = O.integrate_streamline(g, rot, [0.75, 0.5, 0.0], 1e-3, 6000)
+    assert line.stop == S.StreamlineStop.max_steps and len(line.points) == 6001
+    assert K.bits_equal(line.points, pts)
+    assert math.hypot(line.points[-1][0] - 0.75, line.points[-1][1] - 0.5) <= 1e-6
+
+
+def test_div_curl_of_solved_potentials():
+    # acceptance_main.cpp:270-286 at a small size: psi from three device
+    # solves of the knotted-vortex problem, div(curl psi) ~ 0 inside
+    if O.ref_lib() is None:
+        pytest.skip("trifoil sources come from the reference build (oracle/_ref)")
+    comps = []
+    for c in "xyz":
+        g, b, f, s, a = O.ref_problem("trifoil_" + c, 4)
+        res = S.solve(S.ProblemSpec(sgrid(g), f, bc=S.BoundarySpec([S.FaceBc(S.BcKind(b.kind[i]), b.value[i])
+                                                                    for i in range(6)])),
+                      S.SolverConfig(tol=1e-10, max_cycles=60))
+        assert res.report.converged
+        comps.append(res.u)
+    psi = vdev(g, comps)
+    div = S.divergence(S.curl(psi)).numpy().reshape(g.N, g.N, g.N)
+    assert np.max(np.abs(div[1:-1, 1:-1, 1:-1])) <= 1e-13
+    assert K.bits_equal(S.curl(psi).numpy(), O.curl(g, np.stack(comps)))

@@ -3,17 +3,19 @@
 // (proj/tools/sgml_main.cpp:84-94 convergence, :166-178 capacitor,
 // :184-221 bench) plus `poisson3d`, the benchmark problem.
 //
-// The problems are built on the host with the reference's closed forms
-// (problems.cpp:160-193, 500-521) so the inputs are the reference's bits;
-// every solve and every timed cycle runs on the device through the drop-in
-// C++ API (include/sgml/*.hpp -> libsgml_b200.so).  Outputs use the
-// reference's file formats (io.cpp:35-120: %.17g, report.csv, trace.csv,
-// legacy ASCII VTK, bench.csv).  Exit codes as the reference: 0 success,
-// 2 reported non-convergence, 1 input errors.
+// plus deform (:100-125) and trifoil (:131-164).
 //
-// Not here (off the solve path): deform (curve deposition,
-// node motion) and trifoil (vortex-filament sources, curl, streamlines),
-// and the gradient output F.vtk of capacitor.
+// The problems are built on the host with the reference's closed forms and
+// curve deposition (problems.cpp:160-193, 217-300, 302-325, 374-398,
+// 500-521) so the inputs are the reference's bits (the libm calls stay on
+// the host); every solve, every timed cycle and every post-solve field
+// (gradient, curl, node motion, streamlines) runs on the device through the
+// drop-in C++ API (include/sgml/*.hpp -> libsgml_b200.so).  Outputs use the
+// reference's file formats (io.cpp:35-178: %.17g, report.csv, trace.csv,
+// legacy ASCII VTK, points CSV, bench.csv).  Exit codes as the reference:
+// 0 success, 2 reported non-convergence, 1 input errors.
+#include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -25,8 +27,13 @@
 #include <stdexcept>
 #include <string>
 
+#include <sstream>
+#include <vector>
+
 #include "sgml/cycle.hpp"
 #include "sgml/grid.hpp"
+#include "sgml/kernels.hpp"
+#include "sgml/problems.hpp"
 
 namespace {
 
@@ -40,6 +47,12 @@ struct RunConfig {
     double safety = 0.9;
     std::string mode = "high";
     std::string out = ".";
+    double a = 0.1;
+    double r = 0.14;
+    std::string curve_path;
+    std::string seeds_path;
+    double t = 0.0;  // 0 = per-command default
+    int steps = 0;   // 0 = per-command default
 };
 
 std::string fmt(double x) {
@@ -122,6 +135,231 @@ sgml::ProblemSpec capacitor(int n, const std::string& mode) {
     return p;
 }
 
+
+// ---- curves and singular sources (problems.cpp:100-140, 217-300) ----------
+
+struct Curve {
+    std::vector<sgml::Point> points;
+    std::vector<sgml::Point> payload;  // empty or one vector per point
+    bool closed = false;
+};
+
+sgml::Point sub(const sgml::Point& a, const sgml::Point& b) { return {a[0] - b[0], a[1] - b[1], a[2] - b[2]}; }
+sgml::Point add_scaled(const sgml::Point& a, double s, const sgml::Point& b) {
+    return {a[0] + s * b[0], a[1] + s * b[1], a[2] + s * b[2]};
+}
+double norm(const sgml::Point& a) { return std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]); }
+
+// uniform resampling at spacing ~h, unit tangents when payload is requested
+Curve resample_curve(const Curve& curve, double h) {
+    const std::size_t m_in = curve.points.size();
+    if (m_in < 2) throw std::invalid_argument("resample_curve: need at least 2 points");
+    if (!(h > 0.0)) throw std::invalid_argument("resample_curve: spacing must be positive");
+    const std::size_t segs = curve.closed ? m_in : m_in - 1;
+    std::vector<double> cum(segs + 1, 0.0);
+    for (std::size_t s = 0; s < segs; ++s)
+        cum[s + 1] = cum[s] + norm(sub(curve.points[(s + 1) % m_in], curve.points[s]));
+    const double length = cum[segs];
+    if (!(length > 0.0)) throw std::invalid_argument("resample_curve: curve has zero length");
+    const std::size_t m = static_cast<std::size_t>(std::max<long long>(1, std::llround(length / h)));
+    const double ds = length / static_cast<double>(m);
+    const std::size_t count = curve.closed ? m : m + 1;
+    Curve out;
+    out.closed = curve.closed;
+    std::size_t seg = 0;
+    for (std::size_t i = 0; i < count; ++i) {
+        const double s = std::min(static_cast<double>(i) * ds, length);
+        while (seg + 1 < segs && cum[seg + 1] < s) ++seg;
+        const double seg_len = cum[seg + 1] - cum[seg];
+        const double t = seg_len > 0.0 ? (s - cum[seg]) / seg_len : 0.0;
+        const sgml::Point& a = curve.points[seg % m_in];
+        const sgml::Point& b = curve.points[(seg + 1) % m_in];
+        out.points.push_back(add_scaled(a, t, sub(b, a)));
+    }
+    if (!curve.payload.empty()) {
+        const std::size_t mo = out.points.size();
+        out.payload.resize(mo);
+        for (std::size_t i = 0; i < mo; ++i) {
+            sgml::Point d;
+            if (curve.closed) d = sub(out.points[(i + 1) % mo], out.points[(i + mo - 1) % mo]);
+            else if (i == 0) d = sub(out.points[1], out.points[0]);
+            else if (i == mo - 1) d = sub(out.points[mo - 1], out.points[mo - 2]);
+            else d = sub(out.points[i + 1], out.points[i - 1]);
+            const double len = norm(d);
+            if (!(len > 0.0)) throw std::invalid_argument("resample_curve: degenerate tangent");
+            out.payload[i] = {d[0] / len, d[1] / len, d[2] / len};
+        }
+    }
+    return out;
+}
+
+// half the two adjacent chord lengths per sample
+std::vector<double> arc_elements(const Curve& curve) {
+    const std::size_t m = curve.points.size();
+    std::vector<double> ds(m, 0.0);
+    const std::size_t segs = curve.closed ? m : m - 1;
+    for (std::size_t s = 0; s < segs; ++s) {
+        const double len = norm(sub(curve.points[(s + 1) % m], curve.points[s]));
+        ds[s] += 0.5 * len;
+        ds[(s + 1) % m] += 0.5 * len;
+    }
+    return ds;
+}
+
+// tensor-hat scatter of one point mass, weights scaled by 1 / h^dim
+template <typename Deposit>
+void scatter_mass(const sgml::Point& p, const sgml::Grid& g, Deposit&& into) {
+    int idx[3] = {0, 0, 0};
+    double frac[3] = {0.0, 0.0, 0.0};
+    for (int c = 0; c < g.dim; ++c) {
+        const double x = p[c];
+        if (!(x >= 0.0 && x <= 1.0)) throw std::invalid_argument("deposit_delta: curve sample outside the unit domain");
+        int i0 = static_cast<int>(std::floor(x / g.h));
+        i0 = std::clamp(i0, 0, g.N - 2);
+        idx[c] = i0;
+        frac[c] = x / g.h - i0;
+    }
+    const double inv_hd = g.dim == 2 ? 1.0 / (g.h * g.h) : 1.0 / (g.h * g.h * g.h);
+    const double wx[2] = {1.0 - frac[0], frac[0]};
+    const double wy[2] = {1.0 - frac[1], frac[1]};
+    if (g.dim == 2) {
+        for (int b = 0; b < 2; ++b)
+            for (int a = 0; a < 2; ++a) into(idx[0] + a, idx[1] + b, 0, wx[a] * wy[b] * inv_hd);
+    } else {
+        const double wz[2] = {1.0 - frac[2], frac[2]};
+        for (int c = 0; c < 2; ++c)
+            for (int b = 0; b < 2; ++b)
+                for (int a = 0; a < 2; ++a) into(idx[0] + a, idx[1] + b, idx[2] + c, wx[a] * wy[b] * wz[c] * inv_hd);
+    }
+}
+
+bool inside_unit(const sgml::Point& p, int dim) {
+    for (int c = 0; c < dim; ++c)
+        if (!(p[c] >= 0.0 && p[c] <= 1.0)) return false;
+    return true;
+}
+
+sgml::Field deposit_delta(const Curve& curve, const sgml::Grid& grid, double strength) {
+    if (curve.points.size() < 2) throw std::invalid_argument("deposit_delta: need at least 2 points");
+    sgml::Field f(grid);
+    const std::vector<double> ds = arc_elements(curve);
+    for (std::size_t i = 0; i < curve.points.size(); ++i) {
+        const double mass = strength * ds[i];
+        scatter_mass(curve.points[i], grid, [&](int a, int b, int c, double w) { f.at(a, b, c) += mass * w; });
+    }
+    return f;
+}
+
+sgml::VectorField deposit_delta_vector(const Curve& curve, const sgml::Grid& grid) {
+    if (curve.payload.size() != curve.points.size())
+        throw std::invalid_argument("deposit_delta_vector: curve carries no payload");
+    sgml::VectorField f(grid);
+    const std::vector<double> ds = arc_elements(curve);
+    for (std::size_t i = 0; i < curve.points.size(); ++i) {
+        const sgml::Point& pay = curve.payload[i];
+        scatter_mass(curve.points[i], grid, [&](int a, int b, int c, double w) {
+            for (int comp = 0; comp < 3; ++comp) f.comp[comp].at(a, b, c) += pay[comp] * ds[i] * w;
+        });
+    }
+    return f;
+}
+
+// all-Neumann potential attracting nodes toward a closed curve (problems.cpp:302-325)
+struct DeformationSetup {
+    sgml::ProblemSpec problem;
+    sgml::Field f_raw;
+    double raw_integral = 0.0;
+};
+
+DeformationSetup deformation_problem(const Curve& curve, double a, int n) {
+    int dim = 2;
+    for (const sgml::Point& p : curve.points)
+        if (p[2] != 0.0) dim = 3;
+    const sgml::Grid grid = sgml::make_grid(dim, n);
+    DeformationSetup setup;
+    const Curve rs = resample_curve(curve, grid.h);
+    setup.f_raw = deposit_delta(rs, grid, 1.0);
+    setup.raw_integral = sgml::trapezoid_mean(setup.f_raw);
+    setup.problem.grid = grid;
+    setup.problem.a = a;
+    setup.problem.bc = sgml::BoundarySpec::all_neumann();
+    setup.problem.f = setup.f_raw;
+    sgml::zero_mean_projection(setup.problem.f);
+    return setup;
+}
+
+// knotted vortex filament (problems.cpp:374-398): laplacian psi_c = -omega_c
+struct TrifoilSetup {
+    std::array<sgml::ProblemSpec, 3> psi;
+};
+
+TrifoilSetup trifoil_problem(int n, double r) {
+    if (!(r > 0.0)) throw std::invalid_argument("trifoil_problem: r must be positive");
+    const sgml::Grid grid = sgml::make_grid(3, n);
+    Curve raw;
+    raw.closed = true;
+    const int samples = 512;
+    raw.payload.resize(samples);
+    for (int s = 0; s < samples; ++s) {
+        const double t = 2.0 * kPi * s / samples;
+        raw.points.push_back({0.5 + r * (std::sin(t) + 2.0 * std::sin(2.0 * t)),
+                              0.5 + r * (std::cos(t) - 2.0 * std::cos(2.0 * t)), 0.5 - r * std::sin(3.0 * t)});
+    }
+    for (const sgml::Point& p : raw.points)
+        if (!inside_unit(p, 3))
+            throw std::invalid_argument("trifoil_problem: curve leaves the unit domain (max extent 3r)");
+    const Curve curve = resample_curve(raw, grid.h);
+    const sgml::VectorField omega = deposit_delta_vector(curve, grid);
+    TrifoilSetup setup;
+    for (int c = 0; c < 3; ++c) {
+        sgml::ProblemSpec& prob = setup.psi[c];
+        prob.grid = grid;
+        prob.bc = sgml::BoundarySpec::all_dirichlet(0.0);
+        prob.f = omega.comp[c];
+        for (std::size_t p = 0; p < prob.f.size(); ++p) prob.f[p] = -prob.f[p];
+    }
+    return setup;
+}
+
+// io.cpp:126-166: x,y[,z] rows, optional non-numeric header line
+std::vector<sgml::Point> read_points_csv(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw std::runtime_error("cannot open: " + path);
+    std::vector<sgml::Point> pts;
+    std::string line;
+    std::size_t lineno = 0;
+    while (std::getline(in, line)) {
+        ++lineno;
+        while (!line.empty() && (line.back() == '\r' || line.back() == ' ')) line.pop_back();
+        if (line.empty()) continue;
+        std::istringstream row(line);
+        sgml::Point p{0.0, 0.0, 0.0};
+        std::string cell;
+        std::size_t col = 0;
+        bool numeric = true, first_cell_numeric = true;
+        while (std::getline(row, cell, ',')) {
+            if (col >= 3) { numeric = false; break; }
+            try {
+                std::size_t used = 0;
+                p[col] = std::stod(cell, &used);
+                while (used < cell.size() && std::isspace(static_cast<unsigned char>(cell[used]))) ++used;
+                if (used != cell.size()) numeric = false;
+            } catch (const std::exception&) {
+                numeric = false;
+            }
+            if (!numeric) {
+                if (col == 0) first_cell_numeric = false;
+                break;
+            }
+            ++col;
+        }
+        if (lineno == 1 && !first_cell_numeric) continue;
+        if (!numeric || col < 2) throw std::runtime_error(path + ": malformed row " + std::to_string(lineno));
+        pts.push_back(p);
+    }
+    return pts;
+}
+
 // ---- outputs (io.cpp formats) ---------------------------------------------
 
 std::ofstream open_out(const std::string& path) {
@@ -158,6 +396,32 @@ void write_vtk(const sgml::Field& f, const std::string& path, const std::string&
     for (std::size_t p = 0; p < f.size(); ++p) out << fmt(f[p]) << '\n';
 }
 
+void vtk_header(std::ofstream& out, const sgml::Grid& g, const std::string& name) {
+    out << "# vtk DataFile Version 3.0\n" << name << "\nASCII\nDATASET STRUCTURED_POINTS\n"
+        << "DIMENSIONS " << g.N << ' ' << g.N << ' ' << (g.dim == 3 ? g.N : 1) << '\n'
+        << "ORIGIN 0 0 0\n"
+        << "SPACING " << fmt(g.h) << ' ' << fmt(g.h) << ' ' << (g.dim == 3 ? fmt(g.h) : std::string("1")) << '\n'
+        << "POINT_DATA " << g.total << '\n';
+}
+
+void write_vector_vtk(const sgml::VectorField& v, const std::string& path, const std::string& name) {
+    std::ofstream out = open_out(path);
+    vtk_header(out, v.grid(), name);
+    out << "VECTORS " << name << " double\n";
+    for (std::size_t p = 0; p < v.comp[0].size(); ++p)
+        out << fmt(v.comp[0][p]) << ' ' << fmt(v.comp[1][p]) << ' ' << fmt(v.comp[2][p]) << '\n';
+}
+
+void write_points_csv(const std::vector<sgml::Point>& pts, int dim, const std::string& path) {
+    std::ofstream out = open_out(path);
+    out << (dim == 3 ? "x,y,z\n" : "x,y\n");
+    for (const sgml::Point& p : pts) {
+        out << fmt(p[0]) << ',' << fmt(p[1]);
+        if (dim == 3) out << ',' << fmt(p[2]);
+        out << '\n';
+    }
+}
+
 void summary(const char* label, const sgml::SolveReport& rep) {
     if (rep.rows.empty()) {
         std::cout << label << ": no cycles recorded\n";
@@ -183,6 +447,74 @@ int solve_and_write(const char* label, const sgml::ProblemSpec& prob, const RunC
     summary(label, res.report);
     std::cout << label << ": solve " << fmt(secs) << " s wall (H2D, device solve, D2H)\n";
     return res.report.converged ? 0 : 2;
+}
+
+// capacitor (sgml_main.cpp:166-178): the solve plus the force field F = grad u
+int cmd_capacitor(const RunConfig& cfg, bool vtk) {
+    std::filesystem::create_directories(cfg.out);
+    const sgml::SolveResult res = sgml::solve(capacitor(cfg.n, cfg.mode), solver_config(cfg));
+    write_report(res.report, join(cfg.out, "report.csv"));
+    write_trace(res.report, join(cfg.out, "trace.csv"));
+    if (vtk) {
+        write_vtk(res.u, join(cfg.out, "u.vtk"), "u");
+        write_vector_vtk(sgml::gradient(res.u), join(cfg.out, "F.vtk"), "F");
+    }
+    summary("capacitor", res.report);
+    return res.report.converged ? 0 : 2;
+}
+
+// deform (sgml_main.cpp:100-125): potential of a closed curve, then node motion
+int cmd_deform(const RunConfig& cfg, bool vtk) {
+    if (cfg.curve_path.empty()) throw std::invalid_argument("deform: --curve PATH is required");
+    std::filesystem::create_directories(cfg.out);
+    Curve curve;
+    curve.points = read_points_csv(cfg.curve_path);
+    curve.closed = true;
+    const DeformationSetup setup = deformation_problem(curve, cfg.a, cfg.n);
+    const sgml::SolveResult res = sgml::solve(setup.problem, solver_config(cfg));
+    write_report(res.report, join(cfg.out, "report.csv"));
+    write_trace(res.report, join(cfg.out, "trace.csv"));
+    if (vtk) write_vtk(res.u, join(cfg.out, "u.vtk"), "u");
+    const double horizon = cfg.t > 0.0 ? cfg.t : 1.0;
+    const int steps = cfg.steps > 0 ? cfg.steps : 50;
+    const std::vector<sgml::Point> nodes = sgml::move_nodes(res.u, setup.f_raw, setup.raw_integral, horizon, steps);
+    write_points_csv(nodes, setup.problem.grid.dim, join(cfg.out, "nodes.csv"));
+    summary("deform", res.report);
+    return res.report.converged ? 0 : 2;
+}
+
+// trifoil (sgml_main.cpp:131-164): three potential solves, v = curl psi, streamlines
+int cmd_trifoil(const RunConfig& cfg, bool vtk) {
+    std::filesystem::create_directories(cfg.out);
+    const TrifoilSetup setup = trifoil_problem(cfg.n, cfg.r);
+    sgml::VectorField psi(setup.psi[0].grid);
+    bool converged = true;
+    const char* report_names[3] = {"report.csv", "report_psi_y.csv", "report_psi_z.csv"};
+    const char* trace_names[3] = {"trace.csv", "trace_psi_y.csv", "trace_psi_z.csv"};
+    const char* labels[3] = {"psi_x", "psi_y", "psi_z"};
+    for (int c = 0; c < 3; ++c) {
+        const sgml::SolveResult res = sgml::solve(setup.psi[c], solver_config(cfg));
+        write_report(res.report, join(cfg.out, report_names[c]));
+        write_trace(res.report, join(cfg.out, trace_names[c]));
+        summary(labels[c], res.report);
+        converged = converged && res.report.converged;
+        psi.comp[c] = res.u;
+    }
+    const sgml::VectorField v = sgml::curl(psi);
+    if (vtk) {
+        write_vector_vtk(psi, join(cfg.out, "psi.vtk"), "psi");
+        write_vector_vtk(v, join(cfg.out, "v.vtk"), "velocity");
+    }
+    std::vector<sgml::Point> seeds;
+    if (!cfg.seeds_path.empty()) seeds = read_points_csv(cfg.seeds_path);
+    else seeds = {{0.5, 0.5, 0.5}, {0.35, 0.5, 0.5}};
+    const double step = cfg.t > 0.0 ? cfg.t : 0.01;
+    const int max_steps = cfg.steps > 0 ? cfg.steps : 2000;
+    for (std::size_t s = 0; s < seeds.size(); ++s) {
+        const sgml::Streamline line = sgml::integrate_streamline(v, seeds[s], step, max_steps);
+        write_points_csv(line.points, 3, join(cfg.out, "streamline_" + std::to_string(s) + ".csv"));
+    }
+    return converged ? 0 : 2;
 }
 
 // single-cycle sweep over n_lo..n (sgml_main.cpp:184-221): one cycle per
@@ -218,8 +550,10 @@ int cmd_bench(const RunConfig& cfg) {
 }
 
 void usage() {
-    std::cerr << "usage: sgml_b200 {convergence|poisson3d|capacitor|bench} [--n N] [--nr R] [--tol T]\n"
-                 "       [--max-cycles C] [--safety S] [--out DIR] [--mode high|low] [--no-vtk]\n";
+    std::cerr << "usage: sgml_b200 {convergence|poisson3d|capacitor|deform|trifoil|bench} [--n N] [--nr R]\n"
+                 "       [--tol T] [--max-cycles C] [--safety S] [--out DIR] [--mode high|low] [--no-vtk]\n"
+                 "       deform: --curve PATH [--a A] [--t T] [--steps S]; trifoil: [--r R] [--seeds PATH]\n"
+                 "       [--t STEP] [--steps S]\n";
 }
 
 }  // namespace
@@ -248,13 +582,21 @@ int main(int argc, char** argv) {
             else if (a == "--mode") cfg.mode = val();
             else if (a == "--threads") (void)val();  // (OpenMP knob of the reference CLI)
             else if (a == "--no-vtk") vtk = false;
+            else if (a == "--a") cfg.a = std::stod(val());
+            else if (a == "--r") cfg.r = std::stod(val());
+            else if (a == "--curve") cfg.curve_path = val();
+            else if (a == "--seeds") cfg.seeds_path = val();
+            else if (a == "--t") cfg.t = std::stod(val());
+            else if (a == "--steps") cfg.steps = std::stoi(val());
             else throw std::invalid_argument("unknown option " + a);
         }
         if (cfg.n_r < 1 || !(cfg.tol > 0.0) || cfg.max_cycles < 1)
             throw std::invalid_argument("--nr, --tol and --max-cycles must be positive");
         if (cmd == "convergence") return solve_and_write("convergence", poisson2d(cfg.n), cfg, vtk);
         if (cmd == "poisson3d") return solve_and_write("poisson3d", poisson3d(cfg.n), cfg, vtk);
-        if (cmd == "capacitor") return solve_and_write("capacitor", capacitor(cfg.n, cfg.mode), cfg, vtk);
+        if (cmd == "capacitor") return cmd_capacitor(cfg, vtk);
+        if (cmd == "deform") return cmd_deform(cfg, vtk);
+        if (cmd == "trifoil") return cmd_trifoil(cfg, vtk);
         if (cmd == "bench") return cmd_bench(cfg);
         usage();
         return 1;
