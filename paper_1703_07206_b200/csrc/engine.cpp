@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -229,6 +230,10 @@ sgml_solver::~sgml_solver() {
     dfree(Lg); dfree(Lscr); dfree(Lu); dfree(Lup); dfree(Ldu); dfree(Ldup);
     for (double* s : Lsig) dfree(s);
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
+    for (CycleGraph& G : graphs) {
+        if (G.exec) cudaGraphExecDestroy(G.exec);
+        for (cudaEvent_t e : G.events) cudaEventDestroy(e);
+    }
     if (tev0) cudaEventDestroy(tev0);
     if (tev1) cudaEventDestroy(tev1);
     if (d_chain) cudaFree(d_chain);
@@ -252,6 +257,12 @@ void sgml_solver::check_launch(int cls) {
 }
 
 cudaEvent_t sgml_solver::next_event() {
+    if (capturing) {  // events recorded inside a graph belong to it
+        cudaEvent_t e;
+        SGML_CUDA(cudaEventCreate(&e));
+        capturing->events.push_back(e);
+        return e;
+    }
     if (evused == evpool.size()) {
         cudaEvent_t e;
         SGML_CUDA(cudaEventCreate(&e));
@@ -263,9 +274,14 @@ cudaEvent_t sgml_solver::next_event() {
 void sgml_solver::harvest_spans() {
     for (const Span& sp : spans) {
         float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, sp.a, sp.b) == cudaSuccess) {
+        const cudaError_t e = cudaEventElapsedTime(&ms, sp.a, sp.b);
+        if (e == cudaSuccess) {
             cls_ms[sp.cls] += ms;
             cls_n[sp.cls] += 1;
+        } else {
+            static int reported = 0;
+            if (!reported++) std::fprintf(stderr, "sgml: span timing unavailable (%s)\n", cudaGetErrorString(e));
+            (void)cudaGetLastError();  // (not sticky: clear it)
         }
     }
     spans.clear();
@@ -692,6 +708,55 @@ void sgml_solver::cycle_dense(const double* src_dense, double* out_dense, bool h
     }
 }
 
+bool sgml_solver::use_graphs() const {
+    static const int off = std::getenv("SGML_NO_GRAPHS") ? 1 : 0;
+    return compact() && nrk == 1 && !off && debug_sync <= 0 && !diag_mode;
+}
+
+const double* sgml_solver::cycle_graph(bool homogeneous) {
+    CycleGraph& G = graphs[homogeneous ? 1 : 0];
+    const cudaStream_t s = ctx->stream;
+    if (G.exec && fstate == G.pre) {
+        SGML_CUDA(cudaGraphLaunch(G.exec, s));
+        fstate = G.post;
+        launches += G.nlaunch;
+        spans.insert(spans.end(), G.spans.begin(), G.spans.end());
+        return G.out;
+    }
+    if (G.exec) {
+        SGML_CUDA(cudaGraphExecDestroy(G.exec));
+        G.exec = nullptr;
+        for (cudaEvent_t e : G.events) cudaEventDestroy(e);
+        G.events.clear();
+    }
+    G.pre = fstate;
+    const uint64_t l0 = launches;
+    const size_t s0 = spans.size();
+    cudaGraph_t graph = nullptr;
+    SGML_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    capturing = &G;
+    const double* e = nullptr;
+    try {
+        e = cycle_compact(homogeneous);
+    } catch (...) {
+        capturing = nullptr;
+        cudaStreamEndCapture(s, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    capturing = nullptr;
+    SGML_CUDA(cudaStreamEndCapture(s, &graph));
+    const cudaError_t ie = cudaGraphInstantiate(&G.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    SGML_CUDA(ie);
+    G.post = fstate;
+    G.out = e;
+    G.nlaunch = launches - l0;
+    G.spans.assign(spans.begin() + (long)s0, spans.end());
+    SGML_CUDA(cudaGraphLaunch(G.exec, s));
+    return e;
+}
+
 const double* sgml_solver::cycle_compact(bool homogeneous) {
     const int dim = g.dim, n = g.n;
     const cudaStream_t s = ctx->stream;
@@ -1000,7 +1065,7 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
         }
         SGML_CUDA(cudaMemsetAsync(d_cycle, 0, (n_slots + 1) * sizeof(unsigned long long), s));
         reset_fail_flags();
-        const double* e = cycle(homogeneous);
+        const double* e = use_graphs() ? cycle_graph(homogeneous) : cycle(homogeneous);
         // kernel_error check before the recurrence touches u_tot and r
         if (nrk > 1) tp->allreduce_max_i32(d_flag, 1, s);
         SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -159,11 +159,30 @@ struct sgml_solver {
             return;
         }
         Span sp{cls, next_event(), next_event()};
-        cudaEventRecord(sp.a, ctx->stream);
+        // (inside a stream capture an external record makes a real record node)
+        const unsigned fl = capturing ? cudaEventRecordExternal : cudaEventRecordDefault;
+        cudaEventRecordWithFlags(sp.a, ctx->stream, fl);
         fn();
-        cudaEventRecord(sp.b, ctx->stream);
+        cudaEventRecordWithFlags(sp.b, ctx->stream, fl);
         spans.push_back(sp);
     }
+    // One cycle as a CUDA graph (single-GPU compact engine): the ~145
+    // launches of a cycle replay from the device's queue instead of the
+    // host's, so the coarse levels do not pay host launch latency.  A graph
+    // is valid for the face-state map it was captured from (the host-side
+    // bookkeeping of cycle_compact); a mismatch recaptures.
+    struct CycleGraph {
+        cudaGraphExec_t exec = nullptr;
+        std::unordered_map<const double*, int> pre, post;
+        const double* out = nullptr;
+        uint64_t nlaunch = 0;
+        std::vector<Span> spans;          // timing spans (graph-owned events)
+        std::vector<cudaEvent_t> events;
+    };
+    CycleGraph graphs[2];                 // by homogeneous
+    CycleGraph* capturing = nullptr;
+    bool use_graphs() const;
+    const double* cycle_graph(bool homogeneous);
     cudaEvent_t next_event();
     void harvest_spans();  // call after a stream synchronize
     // cycle.cpp:140-247 on a DENSE device source; the dense result goes to
