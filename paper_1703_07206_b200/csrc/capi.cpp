@@ -194,6 +194,7 @@ int sgml_ctx_destroy(sgml_ctx* ctx) {
         cudaFreeHost(ctx->h_slots);
         cudaFreeHost(ctx->h_flags);
         if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+        for (cudaEvent_t e : ctx->h_stage_events) cudaEventDestroy(e);
         delete ctx->cached;
         cudaStreamDestroy(ctx->stream);
         delete ctx;

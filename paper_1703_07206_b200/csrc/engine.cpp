@@ -124,8 +124,23 @@ double trapezoid_mean_host(sgml_ctx* ctx, const sgml_grid& g, const double* dfie
         SGML_CUDA(cudaMallocHost((void**)&ctx->h_stage, bytes));
         ctx->h_stage_bytes = bytes;
     }
-    SGML_CUDA(cudaMemcpyAsync(ctx->h_stage, dfield, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-    SGML_CUDA(cudaStreamSynchronize(ctx->stream));
+    // the copy streams in chunks; the (inherently serial) sum runs behind it
+    constexpr size_t kChunk = size_t(1) << 18;  // doubles (2 MB)
+    const size_t nchunks = (g.total + kChunk - 1) / kChunk;
+    while (ctx->h_stage_events.size() < std::min<size_t>(nchunks, 64)) {
+        cudaEvent_t e;
+        SGML_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->h_stage_events.push_back(e);
+    }
+    const size_t nev = ctx->h_stage_events.size();
+    const size_t per = (nchunks + nev - 1) / nev * kChunk;  // elements per event
+    for (size_t c0 = 0, q = 0; c0 < g.total; c0 += per, ++q) {
+        const size_t cnt = std::min(per, (size_t)g.total - c0);
+        SGML_CUDA(cudaMemcpyAsync(ctx->h_stage + c0, dfield + c0, cnt * sizeof(double), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+        SGML_CUDA(cudaEventRecord(ctx->h_stage_events[q], ctx->stream));
+    }
+    size_t ready = 0, next = 0;
     const double* f = ctx->h_stage;
     const int N = g.N;
     double sum = 0.0, comp = 0.0;
@@ -134,6 +149,10 @@ double trapezoid_mean_host(sgml_ctx* ctx, const sgml_grid& g, const double* dfie
     for (int k = 0; k < KMAX; ++k) {
         const double wk = (g.dim == 3 && (k == 0 || k == N - 1)) ? 0.5 : 1.0;
         for (int j = 0; j < N; ++j) {
+            while (ready < pos + (size_t)N) {  // this row has arrived
+                SGML_CUDA(cudaEventSynchronize(ctx->h_stage_events[next++]));
+                ready = std::min((size_t)g.total, ready + per);
+            }
             const bool jf = j == 0 || j == N - 1;
             for (int i = 0; i < N; ++i, ++pos) {
                 double w = 1.0;

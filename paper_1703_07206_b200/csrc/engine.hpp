@@ -27,6 +27,7 @@ struct sgml_ctx {
     int* h_flags = nullptr;
     double* h_stage = nullptr;              // pinned staging for host reductions
     size_t h_stage_bytes = 0;
+    std::vector<cudaEvent_t> h_stage_events;  // chunk arrival of the staging copy
     // sgml_solve's engine cache (one problem shape), see capi.cpp
     struct sgml_solver* cached = nullptr;
     std::string cached_key;
