@@ -75,10 +75,16 @@ typedef struct {
  * sgml_solver_cfg so the reference SolverConfig maps 1:1). */
 typedef struct {
     int engine;     /* 0 = level-compact B200 engine (default), 1 = literal full-grid passes */
-    int use_graph;  /* capture each cycle's launch sequence in a CUDA graph */
+    int use_graph;  /* 0 / 1: single-GPU compact solves replay each cycle from a CUDA graph
+                       (default); -1: launch eagerly */
     int timing;     /* record per-kernel-class device time in the report */
     int timing_classes; /* 0: every class; else a mask of (1 << SGML_CLASS_*) to time */
+    int stencil;    /* SGML_STENCIL_RADIAL (0, the reference's 9/27-point form) or
+                       SGML_STENCIL_COMPACT (1, 5/7-point, no
+                       reference counterpart, parity unpinned) */
 } sgml_solver_opts;
+
+enum { SGML_STENCIL_RADIAL = 0, SGML_STENCIL_COMPACT = 1 };
 
 /* cycle.hpp:81-89 */
 typedef struct {

@@ -105,6 +105,8 @@ def _load_c():
         getattr(lib, fn).argtypes = [G, _D]
     lib.og_fill_capacitor_sigma.argtypes = [G, C.c_double, _D]
     lib.og_lcg_fill.argtypes = [_D, C.c_uint64, C.c_uint64]
+    lib.og_set_stencil.argtypes = [C.c_int]
+    lib.og_get_stencil.restype = C.c_int
     lib.og_axis_derivative.argtypes = [G, _D, C.c_int, _D]
     for fn in ("og_gradient", "og_curl", "og_divergence"):
         getattr(lib, fn).argtypes = [G, _D, _D]
@@ -452,3 +454,23 @@ def ref_deformation_setup(points, a: float, n: int):
     ri = C.c_double(0.0)
     ref_lib().ref_deformation_setup(_ptr(pts), pts.shape[0], a, n, _ptr(f_raw), _ptr(f), C.byref(ri))
     return g, f_raw, f, ri.value
+
+
+# ------------------------------------------------------ stencil family ----
+
+class stencil:
+    """Context manager: run the C restatement with stencil family `mode`
+    (0 radial = the reference's, 1 compact 5/7-point, SURVEY.md 8a row a23,
+    parity unpinned)."""
+
+    def __init__(self, mode):
+        self.mode = 1 if mode in (1, "compact") else 0
+
+    def __enter__(self):
+        self.prev = c_lib().og_get_stencil()
+        c_lib().og_set_stencil(self.mode)
+        return self
+
+    def __exit__(self, *exc):
+        c_lib().og_set_stencil(self.prev)
+        return False

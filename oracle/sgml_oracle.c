@@ -69,32 +69,58 @@ static inline int mirror_index(int i, int N) {
 
 /* stencil.cpp:13-25: offsets in order r, q, p (skip the centre) */
 typedef struct { int p, q, r; double inv_l2; } og_off;
-static og_off OFF2[8], OFF3[26];
+static og_off OFF2[8], OFF3[26], CMP2[4], CMP3[6];
 static int offs_ready = 0;
+
+/* Stencil family.  0: the reference's radial 9/27-point form (stencil.cpp).
+ * 1: the compact 5/7-point form the north star names and the reference does
+ * not implement (parity UNPINNED, no reference): the
+ * axis offsets only, in the same r, q, p order, inv_l2 = 1, prefactor 1,
+ * step constant K = 1/(2d) (the Gershgorin bound, which reproduces the
+ * reference's K_2 = 1/3 and K_3 = 13/44 for the radial form); same sigma
+ * face average and ghosts. */
+static int og_stencil_mode = 0;
+void og_set_stencil(int mode) { og_stencil_mode = mode; }
+int og_get_stencil(void) { return og_stencil_mode; }
 
 static void build_offsets(void) {
     if (offs_ready) return;
-    int c2 = 0, c3 = 0;
+    int c2 = 0, c3 = 0, k2 = 0, k3 = 0;
     for (int r = -1; r <= 1; ++r)
         for (int q = -1; q <= 1; ++q)
             for (int p = -1; p <= 1; ++p) {
                 if (p == 0 && q == 0 && r == 0) continue;
-                const double l2 = (double)(p * p + q * q + r * r);
+                const int l2i = p * p + q * q + r * r;
+                const double l2 = (double)l2i;
                 OFF3[c3++] = (og_off){p, q, r, 1.0 / l2};
                 if (r == 0) OFF2[c2++] = (og_off){p, q, 0, 1.0 / l2};
+                if (l2i == 1) {
+                    CMP3[k3++] = (og_off){p, q, r, 1.0};
+                    if (r == 0) CMP2[k2++] = (og_off){p, q, 0, 1.0};
+                }
             }
     offs_ready = 1;
 }
 
 static inline const og_off* offsets(int dim, int* count) {
     build_offsets();
+    if (og_stencil_mode == 1) {
+        *count = dim == 2 ? 4 : 6;
+        return dim == 2 ? CMP2 : CMP3;
+    }
     *count = dim == 2 ? 8 : 26;
     return dim == 2 ? OFF2 : OFF3;
 }
 
-/* stencil.hpp:49,52 */
-static inline double prefactor(int dim) { return dim == 2 ? 0.5 : 3.0 / 13.0; }
-static inline double step_constant(int dim) { return dim == 2 ? 1.0 / 3.0 : 13.0 / 44.0; }
+/* stencil.hpp:49,52 (radial); compact: 1 and 1/(2d) */
+static inline double prefactor(int dim) {
+    if (og_stencil_mode == 1) return 1.0;
+    return dim == 2 ? 0.5 : 3.0 / 13.0;
+}
+static inline double step_constant(int dim) {
+    if (og_stencil_mode == 1) return dim == 2 ? 1.0 / 4.0 : 1.0 / 6.0;
+    return dim == 2 ? 1.0 / 3.0 : 13.0 / 44.0;
+}
 /* stencil.hpp:65 / kernels.cpp:22 */
 static const double AXW[3] = {0.25, 0.5, 0.25};
 

@@ -79,6 +79,12 @@ typedef struct {
 /* status codes shared with the product C-ABI */
 enum { OG_OK = 0, OG_INVALID = 1, OG_BADSTEP = 2, OG_NONFINITE = 3 };
 
+/* stencil family for every function below (test infrastructure switch):
+ * 0 = the reference's radial form (default), 1 = compact 5/7-point (SURVEY.md
+ * 8a row a23, parity unpinned: the reference has no such stencil) */
+void og_set_stencil(int mode);
+int og_get_stencil(void);
+
 int og_make_grid(int dim, int n, og_grid* out);
 int og_on_dirichlet(const og_bc* bc, int dim, int N, int i, int j, int k);
 double og_dirichlet_value(const og_bc* bc, int dim, int N, int i, int j, int k);

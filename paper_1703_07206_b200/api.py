@@ -470,13 +470,17 @@ class SolverConfig:
 class SolverOptions:
     """Engine switches with no reference counterpart."""
     engine: str = "compact"     # "compact" (B200 level-compact) or "literal" (reference-shaped)
-    use_graph: bool = False
+    use_graph: bool = True      # replay each cycle from a CUDA graph (single-GPU compact solves)
     timing: bool = False
     timing_classes: int = 0     # 0: time every kernel class; else a mask of 1 << class index
+    stencil: str = "radial"     # "radial" (the reference's) or "compact" 5/7-point (no reference)
 
     def to_c(self) -> _capi.SolverOpts:
-        return _capi.SolverOpts(0 if self.engine == "compact" else 1, int(self.use_graph),
-                                int(self.timing), int(self.timing_classes))
+        if self.stencil not in ("radial", "compact"):
+            raise ValueError("stencil must be 'radial' or 'compact'")
+        return _capi.SolverOpts(0 if self.engine == "compact" else 1, 1 if self.use_graph else -1,
+                                int(self.timing), int(self.timing_classes),
+                                0 if self.stencil == "radial" else 1)
 
 
 @dataclass

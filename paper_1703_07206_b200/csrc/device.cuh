@@ -132,7 +132,11 @@ struct RelaxConst {
     double denom1;     // 1.0 - dtau1*a (sigma == 1)
     int homogeneous;
     int has_a;
+    int compact;       // stencil family: 0 radial (the reference's), 1 compact 5/7-point
 };
+
+// compact 5/7-point family: only the axis offsets
+__device__ __forceinline__ bool stencil_skip(int compact, int l2) { return compact && l2 != 1; }
 
 // kernels.cpp:94-137 at a subset node whose stencil neighbours sit at
 // +-lam in the index space of `up` (lam = 2^v for full-grid fields, 1 for
@@ -157,6 +161,7 @@ __device__ __forceinline__ double relax_at(const double* __restrict__ up,
 #pragma unroll
                 for (int p = -1; p <= 1; ++p) {
                     if (p == 0 && q == 0 && r == 0) continue;
+                    if (stencil_skip(rc.compact, p * p + q * q + r * r)) continue;
                     const ptrdiff_t d = r * sz + q * sy + p * lam;
                     double sbar = 1.0;
                     if (SIG) {
@@ -173,6 +178,7 @@ __device__ __forceinline__ double relax_at(const double* __restrict__ up,
 #pragma unroll
                 for (int p = -1; p <= 1; ++p) {
                     if (p == 0 && q == 0 && r == 0) continue;
+                    if (stencil_skip(rc.compact, p * p + q * q + r * r)) continue;
                     const int ni = i + p * lam, nj = j + q * lam, nk = k + r * lam;
                     double sbar = 1.0;
                     if (SIG) {

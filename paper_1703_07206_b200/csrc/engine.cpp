@@ -88,13 +88,16 @@ int relax_count(int n, int n_r, int v1) {
 }
 
 // kernels.cpp:182-188 and the sigma == 1 step (see RelaxConst)
-RelaxConst relax_const(int dim, int level, double h, double a, double safety, bool homogeneous) {
+RelaxConst relax_const(int dim, int level, double h, double a, double safety, bool homogeneous, int compact) {
     RelaxConst rc{};
     const int lam = 1 << level;
     const double s = lam * h;
     rc.inv_s2 = 1.0 / (s * s);
-    rc.pref = dim == 2 ? 0.5 : 3.0 / 13.0;
-    rc.kdim = dim == 2 ? 1.0 / 3.0 : 13.0 / 44.0;
+    // stencil.hpp:49,52 for the radial form; the compact 5/7-point form
+    // has prefactor 1 and the Gershgorin step K = 1/(2d)
+    rc.pref = compact ? 1.0 : (dim == 2 ? 0.5 : 3.0 / 13.0);
+    rc.kdim = compact ? (dim == 2 ? 1.0 / 4.0 : 1.0 / 6.0) : (dim == 2 ? 1.0 / 3.0 : 13.0 / 44.0);
+    rc.compact = compact ? 1 : 0;
     rc.a = a;
     rc.safety = safety;
     const double smax = 1.0;
@@ -314,6 +317,8 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
     g = make_grid_or_throw(dim, n);
     if (!(cfg_.tol > 0.0)) fail(SGML_EINVAL, "solve: tol must be positive");
     if (cfg_.n_r < 1) fail(SGML_EINVAL, "solve: n_r must be >= 1");
+    if (opts_.stencil != SGML_STENCIL_RADIAL && opts_.stencil != SGML_STENCIL_COMPACT)
+        fail(SGML_EINVAL, "solver: unknown stencil family");
     bc_host = bcin;
     bc = to_dev(bcin);
     all_neumann = !any_dirichlet(bcin, dim);
@@ -585,7 +590,7 @@ void sgml_solver::load_sigma(const double* sigma_dense) {
         for (int m = 1; m < n; ++m) pyramid_step(S[m - 1], m - 1, S[m]);
         // per-node pseudo-time steps of the sigma relaxation, per level
         for (int m = 0; m < n; ++m) {
-            const RelaxConst rcm = relax_const(dim, m, g.h, a, cfg.safety, false);
+            const RelaxConst rcm = relax_const(dim, m, g.h, a, cfg.safety, false, opts.stencil);
             launch(SGML_CLASS_OTHER, [&] { launch_dtau_ext(dim, S[m], Lv[m], DT[m], rcm, s); });
         }
     } else {
@@ -679,7 +684,7 @@ void sgml_solver::residual(const double* e) {
     const int dim = g.dim;
     const cudaStream_t s = ctx->stream;
     unsigned long long* d_rmax = d_cycle + n_slots;
-    const RelaxConst rc0 = relax_const(dim, 0, g.h, a, cfg.safety, false);
+    const RelaxConst rc0 = relax_const(dim, 0, g.h, a, cfg.safety, false, opts.stencil);
     if (compact()) {
         // faces: r = 0 on Dirichlet nodes (kernels.cpp:351-358), u_tot += e
         // there (e holds 0 or the face value)
@@ -700,10 +705,10 @@ void sgml_solver::residual(const double* e) {
         halo(r, 0);  // the next cycle's pyramid reads r across the slab faces
     } else {
         const double inv_h2 = 1.0 / (g.h * g.h);
-        const double pref = dim == 2 ? 0.5 : 3.0 / 13.0;
+        const double pref = relax_const(dim, 0, g.h, a, cfg.safety, true, opts.stencil).pref;
         launch(SGML_CLASS_RESIDUAL, [&] {
             launch_residual(dim, has_sigma, r, e, utot, has_sigma ? Lsig[0] : nullptr, g.N, inv_h2, pref, a, bc,
-                            d_rmax, s);
+                            d_rmax, s, opts.stencil);
         });
     }
 }
@@ -729,7 +734,7 @@ void sgml_solver::cycle_dense(const double* src_dense, double* out_dense, bool h
 
 bool sgml_solver::use_graphs() const {
     static const int off = std::getenv("SGML_NO_GRAPHS") ? 1 : 0;
-    return compact() && nrk == 1 && !off && debug_sync <= 0 && !diag_mode;
+    return compact() && nrk == 1 && !off && opts.use_graph >= 0 && debug_sync <= 0 && !diag_mode;
 }
 
 const double* sgml_solver::cycle_graph(bool homogeneous) {
@@ -803,7 +808,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
     bool base_zero = true;      // state.u entered the cycle zeroed
 
     auto relax_level = [&](int v, double* in, int c, double* p0, double* p1) -> double* {
-        const RelaxConst rc = relax_const(dim, v, g.h, a, cfg.safety, homogeneous);
+        const RelaxConst rc = relax_const(dim, v, g.h, a, cfg.safety, homogeneous, opts.stencil);
         double* cur = in;
         for (int p = 1; p <= c; ++p) {
             double* out = cur == p0 ? p1 : p0;
@@ -954,7 +959,7 @@ const double* sgml_solver::cycle_literal(bool homogeneous) {
                 SGML_CUDA(cudaMemsetAsync(dup, 0, T * sizeof(double), s));
                 current = v;
             }
-            const RelaxConst rc = relax_const(dim, v, g.h, a, cfg.safety, homogeneous);
+            const RelaxConst rc = relax_const(dim, v, g.h, a, cfg.safety, homogeneous, opts.stencil);
             for (int p = 0; p < c; ++p) {
                 std::swap(u, up);
                 std::swap(du, dup);

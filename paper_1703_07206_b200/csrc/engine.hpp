@@ -58,7 +58,8 @@ BcDev to_dev(const sgml_bc& bc);
 bool any_dirichlet(const sgml_bc& bc, int dim);
 sgml_grid make_grid_or_throw(int dim, int n);
 int relax_count(int n, int n_r, int v1);
-RelaxConst relax_const(int dim, int level, double h, double a, double safety, bool homogeneous);
+RelaxConst relax_const(int dim, int level, double h, double a, double safety, bool homogeneous,
+                       int compact = 0);
 double* dalloc(size_t count);
 void dfree(double* p);
 

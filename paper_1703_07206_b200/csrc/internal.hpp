@@ -26,7 +26,7 @@ void launch_relax_literal(int dim, bool sig, double* u, double* du, const double
 // r = 0 on Dirichlet faces, u_tot += e (if non-null), max|r| (if non-null).
 void launch_residual(int dim, bool sig, double* r, const double* e, double* utot,
                      const double* sigma, int N, double inv_h2, double pref, double a,
-                     const BcDev& bc, unsigned long long* rmax_slot, cudaStream_t s);
+                     const BcDev& bc, unsigned long long* rmax_slot, cudaStream_t s, int compact = 0);
 void launch_max_abs(const double* f, uint64_t total, unsigned long long* slot, cudaStream_t s);
 void launch_sub_scalar(double* f, uint64_t total, double v, cudaStream_t s);
 void launch_add_into(double* dst, const double* src, uint64_t total, cudaStream_t s);

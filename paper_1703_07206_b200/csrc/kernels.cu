@@ -143,7 +143,7 @@ template <int DIM, bool SIG>
 __global__ void __launch_bounds__(BX* BY)
     k_residual(double* __restrict__ r, const double* __restrict__ e, double* __restrict__ utot,
                const double* __restrict__ sig, int N, double inv_h2, double pref, double a,
-               int has_a, BcDev bc, unsigned long long* rmax_slot) {
+               int has_a, BcDev bc, unsigned long long* rmax_slot, int compact) {
     const int i = blockIdx.x * BX + threadIdx.x, j = blockIdx.y * BY + threadIdx.y, k = blockIdx.z;
     double mx = 0.0;
     if (i < N && j < N) {
@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(BX* BY)
 #pragma unroll
                     for (int p = -1; p <= 1; ++p) {
                         if (p == 0 && q == 0 && rr == 0) continue;
+                        if (stencil_skip(compact, p * p + q * q + rr * rr)) continue;
                         const ptrdiff_t d = rr * sz + q * sy + p;
                         const double sbar = SIG ? 0.5 * (sig[pos + d] + sc) : 1.0;
                         acc = stencil_term<SIG>(acc, sbar, e[pos + d], ec, p * p + q * q + rr * rr);
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(BX* BY)
 #pragma unroll
                     for (int p = -1; p <= 1; ++p) {
                         if (p == 0 && q == 0 && rr == 0) continue;
+                        if (stencil_skip(compact, p * p + q * q + rr * rr)) continue;
                         const int ni = i + p, nj = j + q, nk = k + rr;
                         const double sbar = SIG ? 0.5 * (mirror(sig, N, ni, nj, nk) + sc) : 1.0;
                         acc = stencil_term<SIG>(acc, sbar, ghost(e, N, bc, ni, nj, nk), ec,
@@ -268,15 +270,15 @@ void launch_relax_literal(int dim, bool sig, double* u, double* du, const double
 
 void launch_residual(int dim, bool sig, double* r, const double* e, double* utot,
                      const double* sigma, int N, double inv_h2, double pref, double a,
-                     const BcDev& bc, unsigned long long* rmax_slot, cudaStream_t s) {
+                     const BcDev& bc, unsigned long long* rmax_slot, cudaStream_t s, int compact) {
     const dim3 gr = grid_for(dim, N), bl(BX, BY);
     const int has_a = a != 0.0;
     if (dim == 2) {
-        if (sig) k_residual<2, true><<<gr, bl, 0, s>>>(r, e, utot, sigma, N, inv_h2, pref, a, has_a, bc, rmax_slot);
-        else k_residual<2, false><<<gr, bl, 0, s>>>(r, e, utot, sigma, N, inv_h2, pref, a, has_a, bc, rmax_slot);
+        if (sig) k_residual<2, true><<<gr, bl, 0, s>>>(r, e, utot, sigma, N, inv_h2, pref, a, has_a, bc, rmax_slot, compact);
+        else k_residual<2, false><<<gr, bl, 0, s>>>(r, e, utot, sigma, N, inv_h2, pref, a, has_a, bc, rmax_slot, compact);
     } else {
-        if (sig) k_residual<3, true><<<gr, bl, 0, s>>>(r, e, utot, sigma, N, inv_h2, pref, a, has_a, bc, rmax_slot);
-        else k_residual<3, false><<<gr, bl, 0, s>>>(r, e, utot, sigma, N, inv_h2, pref, a, has_a, bc, rmax_slot);
+        if (sig) k_residual<3, true><<<gr, bl, 0, s>>>(r, e, utot, sigma, N, inv_h2, pref, a, has_a, bc, rmax_slot, compact);
+        else k_residual<3, false><<<gr, bl, 0, s>>>(r, e, utot, sigma, N, inv_h2, pref, a, has_a, bc, rmax_slot, compact);
     }
 }
 

@@ -381,8 +381,9 @@ __global__ void __launch_bounds__(128) k_sample_ext(const double* __restrict__ i
 }
 
 // Per-node pseudo-time step of the sigma relaxation (kernels.cpp:132-136):
-// dtau = (safety K) / (inv_s2 smax) with smax = max over the 2^d... 26 (8)
-// neighbours of sbar = 0.5 (sigma_n + sigma_c).  It depends on sigma only,
+// dtau = (safety K) / (inv_s2 smax) with smax = max over the 26 (8)
+// neighbours (compact stencil: the 6 (4) axis neighbours) of
+// sbar = 0.5 (sigma_n + sigma_c).  It depends on sigma only,
 // so it is evaluated once per solve and level; the max is order-free and
 // sbar's sum commutes, so this is the relaxation pass's own value bit for bit.
 template <int DIM>
@@ -402,6 +403,7 @@ __global__ void __launch_bounds__(128) k_dtau_ext(const double* __restrict__ sig
 #pragma unroll
             for (int p = -1; p <= 1; ++p) {
                 if (r == 0 && q == 0 && p == 0) continue;
+                if (stencil_skip(rc.compact, r * r + q * q + p * p)) continue;
                 const double sbar = 0.5 * (sig[c + r * sz + q * sy + p] + sc);
                 smax = smax < sbar ? sbar : smax;
             }

@@ -98,7 +98,9 @@ using NodeD = double[Tile<DIM>::RT][Tile<DIM>::XP];
 //              (kernels.cpp:407-415; r is 0 on Dirichlet faces).
 // Range: data nodes [lo.x, hi.x] x [lo.y, hi.y] x [lo.z, hi.z] (2D: x, y),
 // z indices local to the array (z-slabs).
-template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO>
+// CMP: the compact 5/7-point stencil family (axis offsets only, SURVEY.md 8a
+// row a23); the constants (prefactor, step) come in rc.
+template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO, bool CMP>
 __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) : 4)
     k_relax_tma(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_g,
                 const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_t,
@@ -248,7 +250,8 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
             for (int p = -1; p <= 1; ++p) {
                 if (dr == 0 && q == 0 && p == 0) continue;
                 const int l2 = dr * dr + q * q + p * p;
-                const bool first = dr == -1 && q == (DIM == 3 ? -1 : 0) && p == -1;
+                if (CMP && l2 != 1) continue;
+                const bool first = dr == -1 && (CMP ? (q == 0 && p == 0) : (q == (DIM == 3 ? -1 : 0) && p == -1));
                 const bool fuse = !SIG && fm && l2 == 2 && !first;
 #pragma unroll
                 for (int a = 0; a < RT; ++a)
@@ -317,6 +320,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
 #pragma unroll
                     for (int p = -1; p <= 1; ++p) {
                         if (!(q > 0 || (q == 0 && p > 0))) continue;
+                        if (CMP && q * q + p * p != 1) continue;
                         const int aq = DIM == 3 ? a + q : a, bp = b + p;
                         if (!inside(aq, bp)) continue;
                         const int wc = DIM == 3 ? a + 1 : 0, wn = DIM == 3 ? aq + 1 : 0;
@@ -498,19 +502,31 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
     }
 }
 
-template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO>
-void launch_t(dim3 grid, dim3 block, cudaStream_t s, const TmaSet& tm, double* uo, double* duo,
+template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO, bool CMP>
+void launch_k(dim3 grid, dim3 block, cudaStream_t s, const TmaSet& tm, double* uo, double* duo,
               const ExtLay& L, int3 lo, int3 hi, int zb, const RelaxConst& rc,
               unsigned long long* slot, int* flag, int pass_slot) {
     const int bytes = (int)sizeof(TRing<DIM, SIG, MODE>);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_relax_tma<DIM, SIG, HAS_A, MODE, DUO>,
+        cudaFuncSetAttribute(k_relax_tma<DIM, SIG, HAS_A, MODE, DUO, CMP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         configured = true;
     }
-    k_relax_tma<DIM, SIG, HAS_A, MODE, DUO><<<grid, block, bytes, s>>>(tm.u, tm.g, tm.s, tm.t, uo, duo, L, lo,
-                                                                       hi, zb, rc, slot, flag, pass_slot);
+    k_relax_tma<DIM, SIG, HAS_A, MODE, DUO, CMP><<<grid, block, bytes, s>>>(tm.u, tm.g, tm.s, tm.t, uo, duo, L,
+                                                                            lo, hi, zb, rc, slot, flag, pass_slot);
+}
+
+template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO>
+void launch_t(dim3 grid, dim3 block, cudaStream_t s, const TmaSet& tm, double* uo, double* duo,
+              const ExtLay& L, int3 lo, int3 hi, int zb, const RelaxConst& rc,
+              unsigned long long* slot, int* flag, int pass_slot) {
+    if (rc.compact)
+        launch_k<DIM, SIG, HAS_A, MODE, DUO, true>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag,
+                                                   pass_slot);
+    else
+        launch_k<DIM, SIG, HAS_A, MODE, DUO, false>(grid, block, s, tm, uo, duo, L, lo, hi, zb, rc, slot, flag,
+                                                    pass_slot);
 }
 
 template <int DIM, int MODE, bool DUO>
