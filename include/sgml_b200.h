@@ -279,6 +279,22 @@ int sgml_sample_vector(const sgml_field* const* v, int nv, const double* points,
 int sgml_integrate_streamlines(const sgml_field* const* v, const double* seeds, int nseeds, double step,
                                int max_steps, double* points, int* counts, int* stops);
 
+/* ---- problem builders --------------------------------
+ * The reference's sources / coefficients assembled on the device, bit for bit
+ * (the libm calls run on the host over their few distinct arguments; curve
+ * deposits are summed on the host in the reference's sample order and
+ * scattered).  Fields must be allocated on the target grid. */
+int sgml_build_poisson2d_source(sgml_field* f);              /* problems.cpp:160-176 */
+int sgml_build_poisson3d_source(sgml_field* f);              /* problems.cpp:178-193 */
+int sgml_build_sinsin2d_source(sgml_field* f);               /* BASELINE configs[0]: -2 pi^2 sin sin */
+int sgml_build_capacitor_sigma(sgml_field* sigma, int high); /* problems.cpp:500-521 (high: -, low: +) */
+/* problems.cpp:374-398: the three psi sources -omega_c of trifoil_problem(n, r) */
+int sgml_build_trifoil_sources(sgml_field* const* f3, double r);
+/* problems.cpp:302-325 for a closed curve (xyz triples; z != 0 anywhere makes
+ * it 3D): f_raw, the zero-mean source f and the raw trapezoid integral */
+int sgml_build_deformation_sources(const double* points, int npts, sgml_field* f, sgml_field* f_raw,
+                                   double* raw_integral);
+
 #ifdef __cplusplus
 }
 #endif

@@ -124,6 +124,12 @@ _SIGNATURES = {
     "sgml_sample_vector": ([C.POINTER(_P), C.c_int, _D, C.c_int, _D], C.c_int),
     "sgml_integrate_streamlines": ([C.POINTER(_P), _D, C.c_int, C.c_double, C.c_int, _D,
                                     C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+    "sgml_build_poisson2d_source": ([_P], C.c_int),
+    "sgml_build_poisson3d_source": ([_P], C.c_int),
+    "sgml_build_sinsin2d_source": ([_P], C.c_int),
+    "sgml_build_capacitor_sigma": ([_P, C.c_int], C.c_int),
+    "sgml_build_trifoil_sources": ([C.POINTER(_P), C.c_double], C.c_int),
+    "sgml_build_deformation_sources": ([_D, C.c_int, _P, _P, _D], C.c_int),
     "sgml_host_alloc": ([C.c_uint64, C.POINTER(_P)], C.c_int),
     "sgml_host_free": ([_P], C.c_int),
 }

@@ -311,9 +311,8 @@ int sgml_field_fill(sgml_field* f, double value) {
     return guarded([&] {
         require(f != nullptr, SGML_EINVAL, "field_fill: null field");
         activate(f->ctx);
-        std::vector<double> h(f->grid.total, value);
-        SGML_CUDA(cudaMemcpyAsync(f->d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice,
-                                  f->ctx->stream));
+        launch_fill(f->d, f->grid.total, value, f->ctx->stream);
+        SGML_CUDA(cudaGetLastError());
         SGML_CUDA(cudaStreamSynchronize(f->ctx->stream));
     });
 }

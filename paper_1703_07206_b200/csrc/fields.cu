@@ -341,3 +341,80 @@ void launch_sample_points(int dim, const double* const* v, int nv, int N, double
 }
 
 }  // namespace sgmlb
+
+// ---------------------------------------------------------------------------
+// Problem builders on the device.  The reference's
+// closed forms call libm (sin, tanh) per node, which a device cannot
+// reproduce bit for bit; but their arguments take few distinct values: sin
+// depends on one coordinate (N values per axis), the capacitor's tanh on
+// r^2 = m h^2 with the integer m = di^2 + dj^2 + dk^2 (every step of
+// sq(i h - 0.5) + ... is exact for dyadic h).  The host evaluates those
+// values with the host libm (the reference's bits), the device assembles
+// the field with the reference's arithmetic order.
+// ---------------------------------------------------------------------------
+
+namespace sgmlb {
+namespace {
+
+// problems.cpp:178-193: f = (-3 pi pi) ((s_i s_j) s_k), s_t = sin(pi t h)
+__global__ void __launch_bounds__(128) k_fill_poisson3d(double* __restrict__ f, int N,
+                                                        const double* __restrict__ s, double scale) {
+    const Node n = node_here<3>(N);
+    if (!n.ok) return;
+    f[n.p] = scale * ((s[n.i] * s[n.j]) * s[n.k]);
+}
+
+// C1 config (oracle og_fill_sinsin2d): f = ((-2 pi pi) s_i) s_j
+__global__ void __launch_bounds__(128) k_fill_sinsin2d(double* __restrict__ f, int N,
+                                                       const double* __restrict__ s, double scale) {
+    const Node n = node_here<2>(N);
+    if (!n.ok) return;
+    f[n.p] = (scale * s[n.i]) * s[n.j];
+}
+
+// problems.cpp:160-176: f = -(P''(x) P(y) + P(x) P''(y)), P(t) = t^2 - t^4
+__global__ void __launch_bounds__(128) k_fill_poisson2d(double* __restrict__ f, int N, double h) {
+    const Node n = node_here<2>(N);
+    if (!n.ok) return;
+    const double x = n.i * h, y = n.j * h;
+    const double px = x * x - x * x * x * x, py = y * y - y * y * y * y;
+    const double dx = 2.0 - 12.0 * x * x, dy = 2.0 - 12.0 * y * y;
+    f[n.p] = -(dx * py + px * dy);
+}
+
+// problems.cpp:509-515: sigma = table[m], m = di^2 + dj^2 + dk^2, d = i - (N-1)/2
+__global__ void __launch_bounds__(128) k_fill_radial(double* __restrict__ f, int N,
+                                                     const double* __restrict__ table) {
+    const Node n = node_here<3>(N);
+    if (!n.ok) return;
+    const int c = (N - 1) / 2;
+    const int di = n.i - c, dj = n.j - c, dk = n.k - c;
+    f[n.p] = table[di * di + dj * dj + dk * dk];
+}
+
+// sparse contributions (unique nodes) into a zeroed field
+__global__ void k_scatter_pairs(double* __restrict__ f, const unsigned long long* __restrict__ idx,
+                                const double* __restrict__ val, int count) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < count) f[idx[q]] = val[q];
+}
+
+}  // namespace
+
+void launch_fill_poisson3d(double* f, int N, const double* s, double scale, cudaStream_t st) {
+    k_fill_poisson3d<<<node_grid(3, N), dim3(32, 4), 0, st>>>(f, N, s, scale);
+}
+void launch_fill_sinsin2d(double* f, int N, const double* s, double scale, cudaStream_t st) {
+    k_fill_sinsin2d<<<node_grid(2, N), dim3(32, 4), 0, st>>>(f, N, s, scale);
+}
+void launch_fill_poisson2d(double* f, int N, double h, cudaStream_t st) {
+    k_fill_poisson2d<<<node_grid(2, N), dim3(32, 4), 0, st>>>(f, N, h);
+}
+void launch_fill_radial(double* f, int N, const double* table, cudaStream_t st) {
+    k_fill_radial<<<node_grid(3, N), dim3(32, 4), 0, st>>>(f, N, table);
+}
+void launch_scatter_pairs(double* f, const unsigned long long* idx, const double* val, int count, cudaStream_t st) {
+    if (count > 0) k_scatter_pairs<<<(count + 255) / 256, 256, 0, st>>>(f, idx, val, count);
+}
+
+}  // namespace sgmlb

@@ -28,6 +28,7 @@ void launch_residual(int dim, bool sig, double* r, const double* e, double* utot
                      const double* sigma, int N, double inv_h2, double pref, double a,
                      const BcDev& bc, unsigned long long* rmax_slot, cudaStream_t s, int compact = 0);
 void launch_max_abs(const double* f, uint64_t total, unsigned long long* slot, cudaStream_t s);
+void launch_fill(double* f, uint64_t total, double v, cudaStream_t s);
 void launch_sub_scalar(double* f, uint64_t total, double v, cudaStream_t s);
 void launch_add_into(double* dst, const double* src, uint64_t total, cudaStream_t s);
 void launch_apply_boundary(int dim, double* u, int N, const BcDev& bc, bool homogeneous,
@@ -133,5 +134,12 @@ void launch_streamlines(int dim, const double* const* v, int N, double h, const 
 // sample_vector (problems.cpp:407-413) at device points (3 doubles each)
 void launch_sample_points(int dim, const double* const* v, int nv, int N, double h, const double* pts, int count,
                           double* out, cudaStream_t s);
+
+// ---- problem builders (fields.cu; host-evaluated libm tables) -------------
+void launch_fill_poisson3d(double* f, int N, const double* s, double scale, cudaStream_t st);
+void launch_fill_sinsin2d(double* f, int N, const double* s, double scale, cudaStream_t st);
+void launch_fill_poisson2d(double* f, int N, double h, cudaStream_t st);
+void launch_fill_radial(double* f, int N, const double* table, cudaStream_t st);
+void launch_scatter_pairs(double* f, const unsigned long long* idx, const double* val, int count, cudaStream_t st);
 
 }  // namespace sgmlb

@@ -204,6 +204,11 @@ __global__ void k_max_abs(const double* __restrict__ f, uint64_t total, unsigned
     block_max_commit(m, slot);
 }
 
+__global__ void k_fill(double* __restrict__ f, uint64_t total, double v) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < total; p += (uint64_t)gridDim.x * blockDim.x)
+        f[p] = v;
+}
+
 __global__ void k_sub_scalar(double* __restrict__ f, uint64_t total, double v) {
     for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < total;
          p += (uint64_t)gridDim.x * blockDim.x)
@@ -284,6 +289,10 @@ void launch_residual(int dim, bool sig, double* r, const double* e, double* utot
 
 void launch_max_abs(const double* f, uint64_t total, unsigned long long* slot, cudaStream_t s) {
     k_max_abs<<<flat_blocks(total), 256, 0, s>>>(f, total, slot);
+}
+
+void launch_fill(double* f, uint64_t total, double v, cudaStream_t s) {
+    k_fill<<<flat_blocks(total), 256, 0, s>>>(f, total, v);
 }
 
 void launch_sub_scalar(double* f, uint64_t total, double v, cudaStream_t s) {

@@ -18,7 +18,8 @@ from .api import Field, Grid
 
 __all__ = ["VectorField", "StreamlineStop", "Streamline", "axis_derivative", "gradient", "curl", "divergence",
            "deformation_velocity", "move_nodes", "sample_vector", "integrate_streamline",
-           "integrate_streamlines"]
+           "integrate_streamlines", "poisson2d_source", "poisson3d_source", "sinsin2d_source",
+           "capacitor_sigma", "trifoil_sources", "deformation_sources"]
 
 
 def _handles(fields: Sequence[Optional[Field]]):
@@ -132,3 +133,55 @@ def integrate_streamlines(v: VectorField, seeds, step: float, max_steps: int) ->
 def integrate_streamline(v: VectorField, seed, step: float, max_steps: int) -> Streamline:
     """problems.cpp:415-455"""
     return integrate_streamlines(v, [seed], step, max_steps)[0]
+
+
+# ---- problem builders on the device (SURVEY.md 8f rank 2) -------------------
+# The reference's sources / coefficients (problems.cpp) as device fields, bit
+# for bit: libm runs on the host over the few distinct arguments, the device
+# assembles the dense field.
+
+def poisson2d_source(grid: Grid, ctx=None) -> Field:
+    """problems.cpp:160-176"""
+    f = Field(grid, ctx=ctx)
+    check(lib().sgml_build_poisson2d_source(f.handle))
+    return f
+
+
+def poisson3d_source(grid: Grid, ctx=None) -> Field:
+    """problems.cpp:178-193"""
+    f = Field(grid, ctx=ctx)
+    check(lib().sgml_build_poisson3d_source(f.handle))
+    return f
+
+
+def sinsin2d_source(grid: Grid, ctx=None) -> Field:
+    """BASELINE.json configs[0]: f = -2 pi^2 sin(pi x) sin(pi y)"""
+    f = Field(grid, ctx=ctx)
+    check(lib().sgml_build_sinsin2d_source(f.handle))
+    return f
+
+
+def capacitor_sigma(grid: Grid, mode: str = "high", ctx=None) -> Field:
+    """problems.cpp:500-521 ("high": strongly conducting sphere, "low": weakly)"""
+    if mode not in ("high", "low"):
+        raise ValueError('capacitor_problem: mode must be "high" or "low"')
+    s = Field(grid, ctx=ctx)
+    check(lib().sgml_build_capacitor_sigma(s.handle, 1 if mode == "high" else 0))
+    return s
+
+
+def trifoil_sources(grid: Grid, r: float = 0.14, ctx=None) -> list:
+    """problems.cpp:374-398: the sources -omega_c of the three psi problems."""
+    fs = [Field(grid, ctx=ctx) for _ in range(3)]
+    check(lib().sgml_build_trifoil_sources(_handles(fs), float(r)))
+    return fs
+
+
+def deformation_sources(points, grid: Grid, ctx=None):
+    """problems.cpp:302-325 for a closed curve: (f, f_raw, raw_integral)."""
+    pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    f, f_raw = Field(grid, ctx=ctx), Field(grid, ctx=ctx)
+    ri = C.c_double(0.0)
+    check(lib().sgml_build_deformation_sources(pts.ctypes.data_as(_capi._D), pts.shape[0], f.handle, f_raw.handle,
+                                               C.byref(ri)))
+    return f, f_raw, ri.value

@@ -124,3 +124,35 @@ def test_div_curl_of_solved_potentials():
     div = S.divergence(S.curl(psi)).numpy().reshape(g.N, g.N, g.N)
     assert np.max(np.abs(div[1:-1, 1:-1, 1:-1])) <= 1e-13
     assert K.bits_equal(S.curl(psi).numpy(), O.curl(g, np.stack(comps)))
+
+
+# ---- problem builders on the device ------------------
+
+@pytest.mark.parametrize("n", [3, 5, 8])
+def test_device_builders_match_the_reference_bits(n):
+    g3 = O.make_grid(3, n)
+    assert K.bits_equal(S.poisson3d_source(sgrid(g3)).numpy(), O.fill("poisson3d", g3))
+    for mode, sign in (("high", -1.0), ("low", 1.0)):
+        assert K.bits_equal(S.capacitor_sigma(sgrid(g3), mode).numpy(), O.fill("capacitor_sigma", g3, sign))
+    g2 = O.make_grid(2, n + 2)
+    assert K.bits_equal(S.poisson2d_source(sgrid(g2)).numpy(), O.fill("poisson2d", g2))
+    assert K.bits_equal(S.sinsin2d_source(sgrid(g2)).numpy(), O.fill("sinsin2d", g2))
+
+
+@pytest.mark.parametrize("n", [3, 5, 7])
+def test_device_curve_sources_match_the_reference(n):
+    if O.ref_lib() is None:
+        pytest.skip("curve sources are compared with the reference build (oracle/_ref)")
+    g = O.make_grid(3, n)
+    fs = S.trifoil_sources(sgrid(g), 0.14)
+    for c, name in enumerate("xyz"):
+        _, _, f, _, _ = O.ref_problem("trifoil_" + name, n)
+        got = fs[c].numpy()
+        assert np.array_equal(got.view(np.int64), f.view(np.int64))  # incl. the -0.0 of the negation
+    t = 2.0 * 3.14159265358979323846 * np.arange(32) / 32.0
+    pts = np.stack([0.5 + 0.25 * np.cos(t), 0.5 + 0.25 * np.sin(t), np.zeros(32)], axis=1)
+    g2 = O.make_grid(2, n + 3)
+    f, f_raw, ri = S.deformation_sources(pts, sgrid(g2))
+    gr, f_raw_ref, f_ref, ri_ref = O.ref_deformation_setup(pts, 0.1, n + 3)
+    assert ri == ri_ref
+    assert K.bits_equal(f_raw.numpy(), f_raw_ref) and K.bits_equal(f.numpy(), f_ref)
