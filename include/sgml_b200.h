@@ -295,6 +295,12 @@ int sgml_build_trifoil_sources(sgml_field* const* f3, double r);
 int sgml_build_deformation_sources(const double* points, int npts, sgml_field* f, sgml_field* f_raw,
                                    double* raw_integral);
 
+/* ---- output (io.cpp:14-64) ------------------------------
+ * The reference's legacy ASCII VTK files ("%.17g"), byte for byte, streamed
+ * from the device in chunks and formatted on all host threads. */
+int sgml_write_field_vtk(const sgml_field* f, const char* path, const char* name);
+int sgml_write_vector_vtk(const sgml_field* const* v3, const char* path, const char* name); /* v3[2] may be NULL */
+
 #ifdef __cplusplus
 }
 #endif

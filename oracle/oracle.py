@@ -146,6 +146,8 @@ def _load_ref():
     lib.ref_sample_vector.argtypes = [G, _D, _D, _D]
     lib.ref_integrate_streamline.argtypes = [G, _D, _D, C.c_double, C.c_int, _D, C.POINTER(C.c_int)]
     lib.ref_deformation_setup.argtypes = [_D, C.c_int, C.c_double, C.c_int, _D, _D, _D]
+    lib.ref_write_field_vtk.argtypes = [G, _D, C.c_char_p, C.c_char_p]
+    lib.ref_write_vector_vtk.argtypes = [G, _D, C.c_char_p, C.c_char_p]
     return lib
 
 

@@ -12,6 +12,7 @@
 
 #include "sgml/cycle.hpp"
 #include "sgml/kernels.hpp"
+#include "sgml/io.hpp"
 #include "sgml/problems.hpp"
 
 extern "C" {
@@ -287,6 +288,17 @@ int ref_deformation_setup(const double* pts, int npts, double a, int n, double* 
     std::memcpy(f, s.problem.f.data(), s.problem.f.size() * sizeof(double));
     *raw_integral = s.raw_integral;
     return s.problem.grid.dim;
+}
+
+// io.cpp:45-64 (byte reference for the streamed writers)
+void ref_write_field_vtk(const og_grid* g, const double* f, const char* path, const char* name) {
+    R::write_field_vtk(to_field(grid_of(g), f), path, name);
+}
+void ref_write_vector_vtk(const og_grid* g, const double* v, const char* path, const char* name) {
+    const R::Grid gr = grid_of(g);
+    R::VectorField vf(gr);
+    for (int c = 0; c < g->dim; ++c) std::memcpy(vf.comp[c].data(), v + (size_t)c * g->total, g->total * sizeof(double));
+    R::write_vector_vtk(vf, path, name);
 }
 
 }  // extern "C"

@@ -19,7 +19,7 @@ from .api import Field, Grid
 __all__ = ["VectorField", "StreamlineStop", "Streamline", "axis_derivative", "gradient", "curl", "divergence",
            "deformation_velocity", "move_nodes", "sample_vector", "integrate_streamline",
            "integrate_streamlines", "poisson2d_source", "poisson3d_source", "sinsin2d_source",
-           "capacitor_sigma", "trifoil_sources", "deformation_sources"]
+           "capacitor_sigma", "trifoil_sources", "deformation_sources", "write_field_vtk", "write_vector_vtk"]
 
 
 def _handles(fields: Sequence[Optional[Field]]):
@@ -185,3 +185,16 @@ def deformation_sources(points, grid: Grid, ctx=None):
     check(lib().sgml_build_deformation_sources(pts.ctypes.data_as(_capi._D), pts.shape[0], f.handle, f_raw.handle,
                                                C.byref(ri)))
     return f, f_raw, ri.value
+
+
+# ---- output (io.cpp:14-64): streamed from the device ------------------------
+
+def write_field_vtk(f: Field, path: str, name: str) -> None:
+    """io.cpp:45-53, byte for byte."""
+    check(lib().sgml_write_field_vtk(f.handle, str(path).encode(), name.encode()))
+
+
+def write_vector_vtk(v: VectorField, path: str, name: str) -> None:
+    """io.cpp:55-64, byte for byte (the third component of a 2D field is written as 0)."""
+    comps = list(v.comp[:3]) if v.dim == 3 else [v.comp[0], v.comp[1], None]
+    check(lib().sgml_write_vector_vtk(_handles(comps), str(path).encode(), name.encode()))

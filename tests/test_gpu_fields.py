@@ -156,3 +156,22 @@ def test_device_curve_sources_match_the_reference(n):
     gr, f_raw_ref, f_ref, ri_ref = O.ref_deformation_setup(pts, 0.1, n + 3)
     assert ri == ri_ref
     assert K.bits_equal(f_raw.numpy(), f_raw_ref) and K.bits_equal(f.numpy(), f_ref)
+
+
+# ---- streamed VTK output (io.cpp:14-64) ---------------
+
+@pytest.mark.parametrize("dim,n", [(2, 4), (3, 3), (3, 5)])
+def test_streamed_vtk_matches_the_reference_bytes(dim, n, tmp_path):
+    if O.ref_lib() is None:
+        pytest.skip("the byte reference is the reference's own writer (oracle/_ref)")
+    g = O.make_grid(dim, n)
+    rng = np.random.default_rng(n)
+    u = rng.standard_normal(g.total) * 10.0 ** rng.integers(-300, 300, g.total)
+    u[:5] = [0.0, -0.0, 1.0, 0.1, 1e-320]
+    S.write_field_vtk(dev(g, u), tmp_path / "a.vtk", "u")
+    O.ref_lib().ref_write_field_vtk(O.C.byref(g), O._ptr(u), str(tmp_path / "b.vtk").encode(), b"u")
+    assert (tmp_path / "a.vtk").read_bytes() == (tmp_path / "b.vtk").read_bytes()
+    v = np.ascontiguousarray(rng.standard_normal((dim, g.total)))
+    S.write_vector_vtk(vdev(g, v), tmp_path / "c.vtk", "velocity")
+    O.ref_lib().ref_write_vector_vtk(O.C.byref(g), O._ptr(v), str(tmp_path / "d.vtk").encode(), b"velocity")
+    assert (tmp_path / "c.vtk").read_bytes() == (tmp_path / "d.vtk").read_bytes()
