@@ -300,6 +300,9 @@ int sgml_build_deformation_sources(const double* points, int npts, sgml_field* f
  * from the device in chunks and formatted on all host threads. */
 int sgml_write_field_vtk(const sgml_field* f, const char* path, const char* name);
 int sgml_write_vector_vtk(const sgml_field* const* v3, const char* path, const char* name); /* v3[2] may be NULL */
+/* the same files from host arrays: ncomp 1 (SCALARS) or 3 (VECTORS; comps[2] may be NULL) */
+int sgml_write_vtk_host(const double* const* comps, int ncomp, const sgml_grid* g, const char* path,
+                        const char* name);
 
 #ifdef __cplusplus
 }

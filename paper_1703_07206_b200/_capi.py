@@ -132,6 +132,7 @@ _SIGNATURES = {
     "sgml_build_deformation_sources": ([_D, C.c_int, _P, _P, _D], C.c_int),
     "sgml_write_field_vtk": ([_P, C.c_char_p, C.c_char_p], C.c_int),
     "sgml_write_vector_vtk": ([C.POINTER(_P), C.c_char_p, C.c_char_p], C.c_int),
+    "sgml_write_vtk_host": ([C.POINTER(_D), C.c_int, C.POINTER(Grid), C.c_char_p, C.c_char_p], C.c_int),
     "sgml_host_alloc": ([C.c_uint64, C.POINTER(_P)], C.c_int),
     "sgml_host_free": ([_P], C.c_int),
 }

@@ -81,9 +81,43 @@ struct File {
     }
 };
 
+// format rows of host arrays in parallel blocks, written in order
+void format_block(const double* const* src, int ncomp, uint64_t lo, uint64_t hi, std::string& out) {
+    out.resize((size_t)(hi - lo) * (size_t)ncomp * 26);
+    char* p = out.data();
+    for (uint64_t i = lo; i < hi; ++i)
+        for (int c = 0; c < ncomp; ++c) {
+            p = fmt17(p, src[c] ? src[c][i] : 0.0);
+            *p++ = c + 1 < ncomp ? ' ' : '\n';
+        }
+    out.resize((size_t)(p - out.data()));
+}
+
+void format_rows(const double* const* comp, int ncomp, uint64_t total, File& out) {
+    const unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    constexpr uint64_t kChunk = uint64_t(1) << 22;
+    std::vector<std::string> text(nth);
+    for (uint64_t c0 = 0; c0 < total; c0 += kChunk) {
+        const uint64_t cnt = std::min(kChunk, total - c0);
+        const double* src[3] = {nullptr, nullptr, nullptr};
+        for (int c = 0; c < ncomp; ++c) src[c] = comp[c] ? comp[c] + c0 : nullptr;
+        auto work = [&](unsigned t) { format_block(src, ncomp, cnt * t / nth, cnt * (t + 1) / nth, text[t]); };
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < nth; ++t) pool.emplace_back(work, t);
+        work(0);
+        for (auto& th : pool) th.join();
+        for (unsigned t = 0; t < nth; ++t) out.put(text[t].data(), text[t].size());
+    }
+}
+
 // Stream ncomp device arrays (comp[c] == nullptr: zeros) as text rows of
-// ncomp values ("a\n" or "a b c\n").
+// ncomp values ("a\n" or "a b c\n"); ctx == nullptr: the arrays are host
+// memory (no copies).
 void stream_rows(sgml_ctx* ctx, const double* const* comp, int ncomp, uint64_t total, File& out) {
+    if (!ctx) {
+        format_rows(comp, ncomp, total, out);
+        return;
+    }
     const cudaStream_t s = ctx->stream;
     constexpr uint64_t kChunk = uint64_t(1) << 22;  // nodes per chunk
     const uint64_t per = std::min<uint64_t>(kChunk, std::max<uint64_t>(total, 1));
@@ -174,6 +208,22 @@ int sgml_write_vector_vtk(const sgml_field* const* v, const char* path, const ch
         out.put(head.data(), head.size());
         const double* comp[3] = {v[0]->d, v[1]->d, v[2] ? v[2]->d : nullptr};
         stream_rows(v[0]->ctx, comp, 3, v[0]->grid.total, out);
+        out.close();
+    });
+}
+
+// the same writers for host arrays (the command-line driver's fields)
+int sgml_write_vtk_host(const double* const* comps, int ncomp, const sgml_grid* g, const char* path,
+                        const char* name) {
+    return guarded([&] {
+        if (!comps || !comps[0] || !g || !path || !name || (ncomp != 1 && ncomp != 3))
+            fail(SGML_EINVAL, "write_vtk_host: bad argument");
+        File out(path);
+        std::string head = vtk_header(*g, name);
+        head += ncomp == 1 ? std::string("SCALARS ") + name + " double 1\nLOOKUP_TABLE default\n"
+                           : std::string("VECTORS ") + name + " double\n";
+        out.put(head.data(), head.size());
+        stream_rows(nullptr, comps, ncomp, g->total, out);
         out.close();
     });
 }

@@ -34,6 +34,7 @@
 #include "sgml/grid.hpp"
 #include "sgml/kernels.hpp"
 #include "sgml/problems.hpp"
+#include "sgml_b200.h"
 
 namespace {
 
@@ -385,31 +386,21 @@ void write_trace(const sgml::SolveReport& r, const std::string& path) {
 }
 
 void write_vtk(const sgml::Field& f, const std::string& path, const std::string& name) {
-    std::ofstream out = open_out(path);
+    // io.cpp:45-53, formatted on all host threads (libsgml_b200's writer)
     const sgml::Grid& g = f.grid();
-    out << "# vtk DataFile Version 3.0\n" << name << "\nASCII\nDATASET STRUCTURED_POINTS\n"
-        << "DIMENSIONS " << g.N << ' ' << g.N << ' ' << (g.dim == 3 ? g.N : 1) << '\n'
-        << "ORIGIN 0 0 0\n"
-        << "SPACING " << fmt(g.h) << ' ' << fmt(g.h) << ' ' << (g.dim == 3 ? fmt(g.h) : std::string("1")) << '\n'
-        << "POINT_DATA " << g.total << '\n'
-        << "SCALARS " << name << " double 1\nLOOKUP_TABLE default\n";
-    for (std::size_t p = 0; p < f.size(); ++p) out << fmt(f[p]) << '\n';
-}
-
-void vtk_header(std::ofstream& out, const sgml::Grid& g, const std::string& name) {
-    out << "# vtk DataFile Version 3.0\n" << name << "\nASCII\nDATASET STRUCTURED_POINTS\n"
-        << "DIMENSIONS " << g.N << ' ' << g.N << ' ' << (g.dim == 3 ? g.N : 1) << '\n'
-        << "ORIGIN 0 0 0\n"
-        << "SPACING " << fmt(g.h) << ' ' << fmt(g.h) << ' ' << (g.dim == 3 ? fmt(g.h) : std::string("1")) << '\n'
-        << "POINT_DATA " << g.total << '\n';
+    const sgml_grid cg{g.dim, g.n, g.N, 0, g.h, (uint64_t)g.total};
+    const double* comps[1] = {f.data()};
+    if (sgml_write_vtk_host(comps, 1, &cg, path.c_str(), name.c_str()) != SGML_OK)
+        throw std::runtime_error(sgml_last_error());
 }
 
 void write_vector_vtk(const sgml::VectorField& v, const std::string& path, const std::string& name) {
-    std::ofstream out = open_out(path);
-    vtk_header(out, v.grid(), name);
-    out << "VECTORS " << name << " double\n";
-    for (std::size_t p = 0; p < v.comp[0].size(); ++p)
-        out << fmt(v.comp[0][p]) << ' ' << fmt(v.comp[1][p]) << ' ' << fmt(v.comp[2][p]) << '\n';
+    // io.cpp:55-64
+    const sgml::Grid& g = v.grid();
+    const sgml_grid cg{g.dim, g.n, g.N, 0, g.h, (uint64_t)g.total};
+    const double* comps[3] = {v.comp[0].data(), v.comp[1].data(), v.comp[2].size() ? v.comp[2].data() : nullptr};
+    if (sgml_write_vtk_host(comps, 3, &cg, path.c_str(), name.c_str()) != SGML_OK)
+        throw std::runtime_error(sgml_last_error());
 }
 
 void write_points_csv(const std::vector<sgml::Point>& pts, int dim, const std::string& path) {
