@@ -149,7 +149,9 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
             double acc[NC][MV];
             // `st` is a literal at both call sites: the straddle selects vanish
             // from the common (same-cell) path
-            auto accumulate = [&](bool st) {
+            // `sk` (rowfine warps): the level-(w+1) nodes (even k) take ufine,
+            // so their chains are not evaluated
+            auto accumulate = [&](bool st, bool sk) {
 #pragma unroll
                 for (int r = 0; r < 2; ++r) {
                     if (r >= nr) break;
@@ -175,6 +177,7 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
                         // (r, q); a zero-weight p = 1 term adds +-0 (as the reference)
 #pragma unroll
                         for (int k = 0; k < MV; ++k) {
+                            if (sk && (k & 1) == 0) continue;
                             const double w0 = wzy * wx0[k], w1 = wzy * fx[k];
                             const int j = st ? (k >> 1) : 0;
 #pragma unroll
@@ -187,12 +190,18 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
                     }
                 }
             };
-            if (straddle) accumulate(true);
-            else accumulate(false);
+            if (rowfine) {
+                if (straddle) accumulate(true, true);
+                else accumulate(false, true);
+            } else {
+                if (straddle) accumulate(true, false);
+                else accumulate(false, false);
+            }
 #pragma unroll
             for (int cp = 0; cp < NC; ++cp)
 #pragma unroll
-                for (int k = 0; k < MV; ++k) val[cp][k] = val[cp][k] + acc[cp][k];
+                for (int k = 0; k < MV; ++k)
+                    if (!(rowfine && (k & 1) == 0)) val[cp][k] = val[cp][k] + acc[cp][k];
             if (DIAG) {
 #pragma unroll
                 for (int cp = 0; cp < NC; ++cp)
