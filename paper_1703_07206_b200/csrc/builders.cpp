@@ -19,33 +19,12 @@
 
 #include "engine.hpp"
 
-namespace sgmlb {
-const char* last_error_cstr();
-}
-
 using namespace sgmlb;
 
 namespace {
 
 constexpr double kPi = 0x1.921fb54442d18p+1;  // std::numbers::pi_v<double>
 using Point = std::array<double, 3>;
-
-template <typename F>
-int guarded(F&& fn) {
-    try {
-        fn();
-        return SGML_OK;
-    } catch (const Error& e) {
-        set_error(e.msg);
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        set_error("host allocation failed");
-        return SGML_ECUDA;
-    } catch (const std::exception& e) {
-        set_error(e.what());
-        return SGML_ELOGIC;
-    }
-}
 
 void need(bool ok, const char* msg) {
     if (!ok) fail(SGML_EINVAL, msg);

@@ -20,23 +20,6 @@ using namespace sgmlb;
 
 namespace {
 
-template <typename F>
-int guarded(F&& fn) {
-    try {
-        fn();
-        return SGML_OK;
-    } catch (const Error& e) {
-        set_error(e.msg);
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        set_error("host allocation failed");
-        return SGML_ECUDA;
-    } catch (const std::exception& e) {
-        set_error(e.what());
-        return SGML_ELOGIC;
-    }
-}
-
 void require(bool ok, int code, const char* msg) {
     if (!ok) fail(code, msg);
 }

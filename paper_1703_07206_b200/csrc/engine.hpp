@@ -8,6 +8,8 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <new>
+#include <stdexcept>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -50,6 +52,25 @@ struct Error {
     std::string msg;
 };
 void set_error(const std::string& msg);
+
+// C-ABI wrapper body: run fn, translate exceptions into sgml_status codes
+// (the message goes to sgml_last_error)
+template <typename F>
+int guarded(F&& fn) {
+    try {
+        fn();
+        return SGML_OK;
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return SGML_ECUDA;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return SGML_ELOGIC;
+    }
+}
 [[noreturn]] void fail(int code, const std::string& msg);
 void cuda_check(cudaError_t e, const char* what);
 #define SGML_CUDA(call) ::sgmlb::cuda_check((call), #call)

@@ -20,23 +20,6 @@ using namespace sgmlb;
 
 namespace {
 
-template <typename F>
-int guarded(F&& fn) {
-    try {
-        fn();
-        return SGML_OK;
-    } catch (const Error& e) {
-        set_error(e.msg);
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        set_error("host allocation failed");
-        return SGML_ECUDA;
-    } catch (const std::exception& e) {
-        set_error(e.what());
-        return SGML_ELOGIC;
-    }
-}
-
 // io.cpp:35-39 format_double: "%.17g"
 inline char* fmt17(char* p, double x) {
     return std::to_chars(p, p + 32, x, std::chars_format::general, 17).ptr;
