@@ -1092,8 +1092,10 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
         const double* e = use_graphs() ? cycle_graph(homogeneous) : cycle(homogeneous);
         // kernel_error check before the recurrence touches u_tot and r
         if (nrk > 1) tp->allreduce_max_i32(d_flag, 1, s);
-        SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaStreamSynchronize(s));
+        static const bool dbg_flags = std::getenv("SGML_DEBUG_FLAGS") != nullptr;
+        if (dbg_flags) std::fprintf(stderr, "sgml: cycle %d flags %d %d %d %d\n", cyc, h_flag[0], h_flag[1], h_flag[2], h_flag[3]);
         if (h_flag[0]) {
             // the reference throws at the first failing pass: the trace keeps
             // the samples of the passes before it, the cycle gets no row
