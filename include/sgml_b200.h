@@ -250,6 +250,14 @@ int sgml_solver_footprint(const sgml_solver* s, uint64_t* bytes);
 int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f_host,
                const double* sigma_host_or_null, double a, const sgml_solver_cfg* cfg,
                const sgml_solver_opts* opts_or_null, double* u_host_out, sgml_report* rep);
+/* `count` solves of one problem shape (one sigma, different sources) end to
+ * end, pipelined: solve k+1's source moves in and solve k-1's solution moves
+ * out on a copy stream while solve k runs.  f_hosts[k] / u_hosts[k] host
+ * buffers (pinned for full overlap), reps[k] one report each.  Results are
+ * those of count sgml_solve calls. */
+int sgml_solve_many(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, int count, const double* const* f_hosts,
+                    const double* sigma_host_or_null, double a, const sgml_solver_cfg* cfg,
+                    const sgml_solver_opts* opts_or_null, double* const* u_hosts, sgml_report* reps);
 
 /* ---- post-solve fields (problems.hpp:100-148) ----------
  * Dense device fields in, dense device fields out; the reference's bits.

@@ -107,6 +107,8 @@ _SIGNATURES = {
     "sgml_solver_footprint": ([_P, _U64P], C.c_int),
     "sgml_solve": ([_P, C.c_int, C.c_int, C.POINTER(Bc), _D, _D, C.c_double, C.POINTER(SolverCfg),
                     C.POINTER(SolverOpts), _D, C.POINTER(Report)], C.c_int),
+    "sgml_solve_many": ([_P, C.c_int, C.c_int, C.POINTER(Bc), C.c_int, C.POINTER(_D), _D, C.c_double,
+                         C.POINTER(SolverCfg), C.POINTER(SolverOpts), C.POINTER(_D), C.POINTER(Report)], C.c_int),
     "sgml_nccl_unique_id": ([C.c_char_p], C.c_int),
     "sgml_ctx_join_nccl": ([_P, C.c_int, C.c_int, C.c_char_p], C.c_int),
     "sgml_local_group_create": ([C.c_int, C.POINTER(_P)], C.c_int),

@@ -25,7 +25,7 @@ __all__ = [
     "max_abs", "trapezoid_mean", "zero_mean_projection", "apply_boundary", "ScheduleStep",
     "CycleSchedule", "build_schedule", "closed_form_work_units", "schedule_work_units",
     "SolverConfig", "SolverOptions", "DiagSample", "CycleRecord", "SolveReport", "ProblemSpec",
-    "SolveResult", "single_cycle", "solve", "Solver", "restrict_sigma_levels", "pure_neumann_pin",
+    "SolveResult", "single_cycle", "solve", "solve_many", "Solver", "restrict_sigma_levels", "pure_neumann_pin",
     "kernel_error", "LocalGroup", "nccl_unique_id", "slab_plan",
 ]
 
@@ -616,6 +616,39 @@ def solve(problem: ProblemSpec, config: SolverConfig = SolverConfig(),
                            C.byref(config.to_c()), C.byref(opts), u.ctypes.data_as(_capi._D),
                            C.byref(rb.c)))
     return SolveResult(u, rb.to_report())
+
+
+def solve_many(problems: Sequence[ProblemSpec], config: SolverConfig = SolverConfig(),
+               options: Optional[SolverOptions] = None, ctx: Optional[Context] = None,
+               out: Optional[Sequence[np.ndarray]] = None) -> list:
+    """Several solves of one problem shape (same grid, bc, a, sigma; different
+    sources) through ``sgml_solve_many``: transfers of neighbouring solves
+    overlap the device work.  Same results as one ``solve`` per problem.
+    ``out``: optional host arrays (pinned for full overlap) for the solutions."""
+    ctx = ctx or default_context()
+    if not problems:
+        return []
+    p0 = problems[0]
+    g = p0.grid
+    fs = [np.ascontiguousarray(p.f, np.float64).reshape(-1) for p in problems]
+    for p, f in zip(problems, fs):
+        if p.grid != g or f.size != g.total:
+            raise ValueError("solve_many: every problem must share the grid")
+    sig = None
+    if p0.sigma is not None:
+        sig = np.ascontiguousarray(p0.sigma, np.float64).reshape(-1)
+    us = list(out) if out is not None else [np.empty(g.total, np.float64) for _ in problems]
+    rbs = [_ReportBuffers() for _ in problems]
+    reps = (_capi.Report * len(problems))(*[rb.c for rb in rbs])
+    fptr = (_capi._D * len(problems))(*[f.ctypes.data_as(_capi._D) for f in fs])
+    uptr = (_capi._D * len(problems))(*[u.ctypes.data_as(_capi._D) for u in us])
+    opts = (options or SolverOptions()).to_c()
+    check(lib().sgml_solve_many(ctx.handle, g.dim, g.n, C.byref(p0.bc.to_c()), len(problems), fptr,
+                                None if sig is None else sig.ctypes.data_as(_capi._D), float(p0.a),
+                                C.byref(config.to_c()), C.byref(opts), uptr, reps))
+    for rb, rc in zip(rbs, reps):
+        rb.c = rc
+    return [SolveResult(u, rb.to_report()) for u, rb in zip(us, rbs)]
 
 
 class Solver:

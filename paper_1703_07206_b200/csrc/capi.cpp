@@ -561,6 +561,60 @@ int sgml_solver_footprint(const sgml_solver* s, uint64_t* bytes) {
     });
 }
 
+}  // extern "C"
+
+namespace {
+
+// sgml_solve's engine cache: one engine per context for the last problem
+// shape (grid, bc, a, cfg, opts, sigma present); sigma is (re)loaded when given.
+// Call with ctx->mu held.
+sgml_solver* cached_solver(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* sigma_host, double a,
+                           const sgml_solver_cfg* cfg, const sgml_solver_opts& o) {
+    const sgml_grid g = make_grid_or_throw(dim, n);
+    const cudaStream_t s = ctx->stream;
+    std::string key(reinterpret_cast<const char*>(&g), sizeof g);
+    key.append(reinterpret_cast<const char*>(bc), sizeof *bc);
+    key.append(reinterpret_cast<const char*>(&a), sizeof a);
+    key.append(reinterpret_cast<const char*>(cfg), sizeof *cfg);
+    key.append(reinterpret_cast<const char*>(&o), sizeof o);
+    key.push_back(sigma_host ? 's' : '-');
+    const size_t bytes = g.total * sizeof(double);
+    if (!ctx->cached || ctx->cached_key != key) {
+        delete ctx->cached;
+        ctx->cached = nullptr;
+        ctx->cached_key.clear();
+        double* sig = nullptr;
+        struct Guard {
+            double* p = nullptr;
+            ~Guard() { dfree(p); }
+        } sg;
+        if (sigma_host) {
+            sg.p = sig = dalloc(g.total);
+            SGML_CUDA(cudaMemcpyAsync(sig, sigma_host, bytes, cudaMemcpyHostToDevice, s));
+        }
+        auto sv = std::make_unique<sgml_solver>();
+        sv->build(ctx, dim, n, *bc, a, sig, *cfg, o);
+        sv->fin = sv->alloc(g.total);
+        ctx->cached = sv.release();
+        ctx->cached_key = key;
+    } else if (sigma_host) {
+        sgml_solver* sv = ctx->cached;
+        SGML_CUDA(cudaMemcpyAsync(sv->sigma_stage(), sigma_host, bytes, cudaMemcpyHostToDevice, s));
+        sv->load_sigma(sv->sigma_stage());
+    }
+    return ctx->cached;
+}
+
+void check_solve_args(const sgml_solver_cfg* cfg) {
+    // cycle.cpp:142-152 validation order: tol, n_r (finite source: in run)
+    require(cfg->tol > 0.0, SGML_EINVAL, "solve: tol must be positive");
+    require(cfg->n_r >= 1, SGML_EINVAL, "solve: n_r must be >= 1");
+}
+
+}  // namespace
+
+extern "C" {
+
 int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f_host,
                const double* sigma_host, double a, const sgml_solver_cfg* cfg,
                const sgml_solver_opts* opts, double* u_host_out, sgml_report* rep) {
@@ -569,49 +623,82 @@ int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f
         const sgml_grid g = make_grid_or_throw(dim, n);
         activate(ctx);
         const cudaStream_t s = ctx->stream;
-        // cycle.cpp:142-152 validation order: tol, n_r, finite source
-        require(cfg->tol > 0.0, SGML_EINVAL, "solve: tol must be positive");
-        require(cfg->n_r >= 1, SGML_EINVAL, "solve: n_r must be >= 1");
+        check_solve_args(cfg);
         sgml_solver_opts o{};
         if (opts) o = *opts;
         std::lock_guard<std::mutex> lock(ctx->mu);
-        // one cached engine per context: repeated solves of one problem shape
-        // reuse its device buffers (freed with the context)
-        std::string key(reinterpret_cast<const char*>(&g), sizeof g);
-        key.append(reinterpret_cast<const char*>(bc), sizeof *bc);
-        key.append(reinterpret_cast<const char*>(&a), sizeof a);
-        key.append(reinterpret_cast<const char*>(cfg), sizeof *cfg);
-        key.append(reinterpret_cast<const char*>(&o), sizeof o);
-        key.push_back(sigma_host ? 's' : '-');
+        sgml_solver* sv = cached_solver(ctx, dim, n, bc, sigma_host, a, cfg, o);
         const size_t bytes = g.total * sizeof(double);
-        if (!ctx->cached || ctx->cached_key != key) {
-            delete ctx->cached;
-            ctx->cached = nullptr;
-            ctx->cached_key.clear();
-            double* sig = nullptr;
-            struct Guard {
-                double* p = nullptr;
-                ~Guard() { dfree(p); }
-            } sg;
-            if (sigma_host) {
-                sg.p = sig = dalloc(g.total);
-                SGML_CUDA(cudaMemcpyAsync(sig, sigma_host, bytes, cudaMemcpyHostToDevice, s));
-            }
-            auto sv = std::make_unique<sgml_solver>();
-            sv->build(ctx, dim, n, *bc, a, sig, *cfg, o);
-            sv->fin = sv->alloc(g.total);
-            ctx->cached = sv.release();
-            ctx->cached_key = key;
-        } else if (sigma_host) {
-            sgml_solver* sv = ctx->cached;
-            SGML_CUDA(cudaMemcpyAsync(sv->sigma_stage(), sigma_host, bytes, cudaMemcpyHostToDevice, s));
-            sv->load_sigma(sv->sigma_stage());
-        }
-        sgml_solver* sv = ctx->cached;
         SGML_CUDA(cudaMemcpyAsync(sv->fin, f_host, bytes, cudaMemcpyHostToDevice, s));
         sv->run(sv->fin, nullptr, rep);
         if (u_host_out)
             SGML_CUDA(cudaMemcpyAsync(u_host_out, sv->result(), bytes, cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+int sgml_solve_many(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, int count, const double* const* f_hosts,
+                    const double* sigma_host, double a, const sgml_solver_cfg* cfg,
+                    const sgml_solver_opts* opts, double* const* u_hosts, sgml_report* reps) {
+    return guarded([&] {
+        require(ctx && bc && f_hosts && cfg && reps && count >= 0, SGML_EINVAL, "solve: null argument");
+        const sgml_grid g = make_grid_or_throw(dim, n);
+        activate(ctx);
+        const cudaStream_t s = ctx->stream;
+        check_solve_args(cfg);
+        sgml_solver_opts o{};
+        if (opts) o = *opts;
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        sgml_solver* sv = cached_solver(ctx, dim, n, bc, sigma_host, a, cfg, o);
+        if (count == 0) return;
+        const size_t bytes = g.total * sizeof(double);
+        // double-buffered staging: the copy stream moves solve k+1's source in
+        // and solve k-1's solution out while solve k runs
+        if (!sv->fin2) sv->fin2 = sv->alloc(g.total);
+        for (int b = 0; b < 2; ++b)
+            if (!sv->uout[b]) sv->uout[b] = sv->alloc(g.total);
+        cudaStream_t cs = nullptr;
+        cudaEvent_t in_ready[2] = {nullptr, nullptr}, out_ready[2] = {nullptr, nullptr}, out_done[2] = {nullptr, nullptr};
+        struct Cleanup {
+            cudaStream_t* cs;
+            cudaEvent_t* ev[3];
+            ~Cleanup() {
+                if (*cs) {
+                    cudaStreamSynchronize(*cs);
+                    cudaStreamDestroy(*cs);
+                }
+                for (auto* e : ev)
+                    for (int b = 0; b < 2; ++b)
+                        if (e[b]) cudaEventDestroy(e[b]);
+            }
+        } cleanup{&cs, {in_ready, out_ready, out_done}};
+        SGML_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            SGML_CUDA(cudaEventCreateWithFlags(&in_ready[b], cudaEventDisableTiming));
+            SGML_CUDA(cudaEventCreateWithFlags(&out_ready[b], cudaEventDisableTiming));
+            SGML_CUDA(cudaEventCreateWithFlags(&out_done[b], cudaEventDisableTiming));
+        }
+        double* fin[2] = {sv->fin, sv->fin2};
+        auto stage_in = [&](int k) {
+            SGML_CUDA(cudaMemcpyAsync(fin[k & 1], f_hosts[k], bytes, cudaMemcpyHostToDevice, cs));
+            SGML_CUDA(cudaEventRecord(in_ready[k & 1], cs));
+        };
+        stage_in(0);
+        for (int k = 0; k < count; ++k) {
+            const int b = k & 1;
+            // (solve k-1 finished reading fin[b ^ 1] before run returned)
+            if (k + 1 < count) stage_in(k + 1);
+            SGML_CUDA(cudaStreamWaitEvent(s, in_ready[b], 0));
+            if (k >= 2) SGML_CUDA(cudaStreamWaitEvent(s, out_done[b], 0));  // uout[b] drained
+            sv->run(fin[b], sv->uout[b], &reps[k]);
+            SGML_CUDA(cudaEventRecord(out_ready[b], s));
+            if (u_hosts && u_hosts[k]) {
+                SGML_CUDA(cudaStreamWaitEvent(cs, out_ready[b], 0));
+                SGML_CUDA(cudaMemcpyAsync(u_hosts[k], sv->uout[b], bytes, cudaMemcpyDeviceToHost, cs));
+            }
+            SGML_CUDA(cudaEventRecord(out_done[b], cs));
+        }
+        SGML_CUDA(cudaStreamSynchronize(cs));
         SGML_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -244,6 +244,7 @@ double* sgml_solver::alloc(size_t count) {
 sgml_solver::~sgml_solver() {
     if (ctx) cudaSetDevice(ctx->device);
     dfree(r); dfree(utot); dfree(A); dfree(B); dfree(fin); dfree(dense);
+    dfree(fin2); dfree(uout[0]); dfree(uout[1]);
     for (size_t m = 1; m < P.size(); ++m) dfree(P[m]);
     for (double* s : S) dfree(s);
     for (double* d : DT) dfree(d);

@@ -114,6 +114,8 @@ struct sgml_solver {
     double* A = nullptr;
     double* B = nullptr;
     double* fin = nullptr;     // dense staging for host-buffer solves (sgml_solve)
+    double* fin2 = nullptr;    // second source / two result buffers (sgml_solve_many pipeline)
+    double* uout[2] = {nullptr, nullptr};
     double* dense = nullptr;   // dense scratch / result (compact engine)
     // level arrays of the compact engine (index = level), extended layout
     std::vector<int> Nl;

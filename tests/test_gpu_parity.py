@@ -350,3 +350,21 @@ def test_solve_twice_with_nonzero_dirichlet_values():
     for name, n in (("capacitor_high", 3), ("capacitor_low", 3), ("sigma3d_dirichlet", 3)):
         for _ in range(2):
             check_solve(name, n)
+
+
+@pytest.mark.parametrize("name,n", [("poisson3d", 4), ("capacitor_high", 3), ("sinsin2d", 5)])
+def test_solve_many_equals_single_solves(name, n):
+    # sgml_solve_many pipelines the transfers of neighbouring solves; each
+    # result must be the single solve's, bit for bit
+    g, b, f, s, a = K.solve_problem(name, n)
+    scales = [1.0, -0.5, 3.0] if not np.all(f == 0) else [1.0]
+    probs = [S.ProblemSpec(sgrid(g), f * c, bc=sbc_of(b), sigma=s, a=a) for c in scales]
+    cfg = S.SolverConfig(tol=1e-10, max_cycles=40)
+    many = S.solve_many(probs, cfg)
+    for p, m in zip(probs, many):
+        one = S.solve(p, cfg)
+        assert [(r.cycle, r.work_units, r.residual, r.diag_min) for r in m.report.rows] == \
+            [(r.cycle, r.work_units, r.residual, r.diag_min) for r in one.report.rows]
+        assert [(t.cycle, t.pass_, t.level, t.value) for t in m.report.trace] == \
+            [(t.cycle, t.pass_, t.level, t.value) for t in one.report.trace]
+        assert np.array_equal(m.u.view(np.int64), one.u.view(np.int64))
