@@ -870,7 +870,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                     const ChainEntry* ch = chain_at();
                     launch(SGML_CLASS_MATERIALIZE, [&] {
                         launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lv[v + 1],
-                                            v + 1, ch, count, v1, bc, homogeneous, flag, diag_mode, s);
+                                            v + 1, ch, count, bc, homogeneous, flag, diag_mode, s);
                     });
                     fstate[other] = face_want(homogeneous);
                     halo(other, 0);
@@ -888,7 +888,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                 int wb;
                 base_src(v, bp, bl, wb);
                 launch(SGML_CLASS_MATERIALIZE, [&] {
-                    launch_materialize4(dim, in, Lv[v], v, bp, bl, wb, base_zero, ufinal, Lf, 1, ch, count, v1,
+                    launch_materialize4(dim, in, Lv[v], v, bp, bl, wb, base_zero, ufinal, Lf, 1, ch, count,
                                         bc, homogeneous, flag, diag_mode, s);
                 });
                 fstate[in] = face_want(homogeneous);
@@ -907,7 +907,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
             const ChainEntry* ch = chain_at();
             const ExtLay Lf = n > 1 ? Lv[1] : Lv[0];
             launch(SGML_CLASS_MATERIALIZE, [&] {
-                launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lf, 1, ch, count, v1,
+                launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lf, 1, ch, count,
                                     bc, homogeneous, flag, diag_mode, s);
             });
             fstate[other] = face_want(homogeneous);

@@ -101,7 +101,7 @@ void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc
 // at an interpolated node (flag[4] <- min entry fslot; failure re-runs only)
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
                          const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
-                         int frel, const ChainEntry* chain, int nchain, int maxl, const BcDev& bc,
+                         int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
                          bool homogeneous, int* flag, bool diag, cudaStream_t s);
 // per-node pseudo-time step of the sigma relaxation at every node of a level
 // array (own planes), from the level's sigma (with ghosts / halos)

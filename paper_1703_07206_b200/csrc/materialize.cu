@@ -444,12 +444,12 @@ uint64_t ext_size(int dim, const ExtLay& L) {
 
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
                          const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
-                         int frel, const ChainEntry* chain, int nchain, int maxl, const BcDev& bc,
+                         int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
                          bool homogeneous, int* flag, bool diag, cudaStream_t s) {
     const int Nw = Lw.N;
-    // two copies (y and y + (Nw-1)/2): measured faster than four, whose 16
-    // nodes per thread cost occupancy (maxl is kept for that variant)
-    (void)maxl;
+    // two copies (y and y + (Nw-1)/2): measured faster than one (occupancy
+    // does not pay for the lost weight sharing) and than four (16 nodes per
+    // thread cost occupancy)
     constexpr int NC = 2;
     // Dirichlet x-high face (Nw - 1 a multiple of MV): threads cover x < Nw - 1
     // and the last group writes the face node (xtail)
