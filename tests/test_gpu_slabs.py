@@ -22,7 +22,7 @@ def sbc_of(b):
     return S.BoundarySpec([S.FaceBc(S.BcKind(b.kind[f]), b.value[f]) for f in range(6)])
 
 
-def solve_clique(name, n, nranks, n_r=2, max_cycles=40):
+def solve_clique(name, n, nranks, n_r=2, max_cycles=40, stencil="radial"):
     g, b, f, s, a = K.solve_problem(name, n)
     group = S.LocalGroup(nranks)
     out, err = [None] * nranks, [None] * nranks
@@ -34,7 +34,7 @@ def solve_clique(name, n, nranks, n_r=2, max_cycles=40):
             assert ctx.clique() == (nranks, r)
             prob = S.ProblemSpec(sgrid(g), f, bc=sbc_of(b), sigma=s, a=a)
             out[r] = S.solve(prob, S.SolverConfig(n_r=n_r, tol=1e-10, max_cycles=max_cycles, safety=0.9),
-                             ctx=ctx)
+                             S.SolverOptions(stencil=stencil), ctx=ctx)
         except Exception as exc:  # surfaced below
             err[r] = exc
 
@@ -47,7 +47,8 @@ def solve_clique(name, n, nranks, n_r=2, max_cycles=40):
     for e in err:
         if e is not None:
             raise e
-    ref = O.solve(g, b, f, s, a, n_r=n_r, tol=1e-10, max_cycles=max_cycles)
+    with O.stencil(stencil):
+        ref = O.solve(g, b, f, s, a, n_r=n_r, tol=1e-10, max_cycles=max_cycles)
     return out, ref
 
 
@@ -86,3 +87,12 @@ def test_slab_plan_rejects_bad_cliques():
         S.slab_plan(4, 3, 0)        # not a power of two
     with pytest.raises(ValueError):
         S.slab_plan(3, 8, 0)        # fewer than 2 planes per rank
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("name,n", [("poisson3d", 5), ("capacitor_high", 4)])
+def test_slab_solve_compact_stencil(name, n):
+    # the 5/7-point family through the decomposition
+    out, ref = solve_clique(name, n, 2, max_cycles=80, stencil="compact")
+    for res in out:
+        check_same(res, ref)
