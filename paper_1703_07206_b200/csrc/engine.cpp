@@ -253,6 +253,12 @@ sgml_solver::~sgml_solver() {
     dfree(Lg); dfree(Lscr); dfree(Lu); dfree(Lup); dfree(Ldu); dfree(Ldup);
     for (double* s : Lsig) dfree(s);
     for (cudaEvent_t e : evpool) cudaEventDestroy(e);
+    if (hx_stream) {
+        cudaStreamSynchronize(hx_stream);
+        cudaStreamDestroy(hx_stream);
+        cudaEventDestroy(hx_ready);
+        cudaEventDestroy(hx_done);
+    }
     for (CycleGraph& G : graphs) {
         if (G.exec) cudaGraphExecDestroy(G.exec);
         for (cudaEvent_t e : G.events) cudaEventDestroy(e);
@@ -525,6 +531,19 @@ void sgml_solver::own_planes(int v, int p, int& kb, int& cnt) const {
 void sgml_solver::halo(double* a, int v) {
     if (!dist(v)) return;
     tp->halo(a, Lv[v].plane, Lv[v].Nz, d_flag, ctx->stream);
+}
+
+// relaxation passes of z-slab levels overlap their halo exchange with the
+// interior planes (SGML_NO_HALO_OVERLAP=1: exchange after the whole pass)
+bool sgml_solver::overlap_halos(int v) {
+    static const bool off = std::getenv("SGML_NO_HALO_OVERLAP") != nullptr;
+    if (off || !dist(v) || rng[v].hi[2] - rng[v].lo[2] < 2) return false;
+    if (!hx_stream) {
+        SGML_CUDA(cudaStreamCreateWithFlags(&hx_stream, cudaStreamNonBlocking));
+        SGML_CUDA(cudaEventCreateWithFlags(&hx_ready, cudaEventDisableTiming));
+        SGML_CUDA(cudaEventCreateWithFlags(&hx_done, cudaEventDisableTiming));
+    }
+    return true;
 }
 
 // a replicated level array whose planes were produced rank by rank (own
@@ -828,12 +847,35 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
             tm.g = gmap(gsrc(v));
             tm.s = has_sigma ? umap(S[v]) : tm.u;
             tm.t = has_sigma ? gmap(DT[v]) : tm.g;
-            launch(v == 0 ? SGML_CLASS_RELAX0 : SGML_CLASS_RELAX_COARSE, [&] {
-                launch_relax_tma(dim, has_sigma, tm, out, duo, Lv[v], rng[v], rc, diag + slot, flag, slot, s);
-            });
+            auto relax_range = [&](const NodeRange& rg) {
+                launch(v == 0 ? SGML_CLASS_RELAX0 : SGML_CLASS_RELAX_COARSE, [&] {
+                    launch_relax_tma(dim, has_sigma, tm, out, duo, Lv[v], rg, rc, diag + slot, flag, slot, s);
+                });
+            };
+            if (overlap_halos(v)) {
+                // z-slab level: the two planes the neighbours need first, their
+                // halo exchange on the transfer stream while the interior planes
+                // are relaxed (all three launches share the pass's diag slot)
+                NodeRange b0 = rng[v], b1 = rng[v], mid = rng[v];
+                b0.hi[2] = b0.lo[2];
+                b1.lo[2] = b1.hi[2];
+                mid.lo[2] += 1;
+                mid.hi[2] -= 1;
+                relax_range(b0);
+                relax_range(b1);
+                SGML_CUDA(cudaEventRecord(hx_ready, s));
+                SGML_CUDA(cudaStreamWaitEvent(hx_stream, hx_ready, 0));
+                tp->halo(out, Lv[v].plane, Lv[v].Nz, d_flag, hx_stream);
+                if (duo) tp->halo(duo, Lv[v].plane, Lv[v].Nz, d_flag, hx_stream);
+                SGML_CUDA(cudaEventRecord(hx_done, hx_stream));
+                relax_range(mid);
+                SGML_CUDA(cudaStreamWaitEvent(s, hx_done, 0));
+            } else {
+                relax_range(rng[v]);
+                halo(out, v);  // z-slab levels: the next consumer reads across the slab faces
+                if (duo) halo(duo, v);
+            }
             ++slot;
-            halo(out, v);  // z-slab levels: the next consumer reads across the slab faces
-            if (duo) halo(duo, v);
             cur = out;
             first = false;
         }

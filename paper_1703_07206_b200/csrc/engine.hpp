@@ -242,7 +242,10 @@ struct sgml_solver {
     bool dist(int v) const { return nrk > 1 && v < vrep; }
     double* BS = nullptr;      // base sampled on level vrep (replicated), for replicated targets
     bool bs_valid = false;
-    void halo(double* a, int v);                          // after a producer at a z-slab level
+    void halo(double* a, int v);
+    bool overlap_halos(int v);
+    cudaStream_t hx_stream = nullptr;  // halo transfers overlapped with interior planes
+    cudaEvent_t hx_ready = nullptr, hx_done = nullptr;                          // after a producer at a z-slab level
     void gather_level(double* a, int v);                  // replicated level: own planes -> all
     void own_planes(int v, int p, int& kb, int& cnt) const;  // rank p's planes of level v
     void refresh_bs(const double* base);
