@@ -827,6 +827,24 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
     double* other = B;
     bool base_zero = true;      // state.u entered the cycle zeroed
 
+    // a materialisation into a z-slab level array and its halo exchange: the
+    // two own boundary planes first, their exchange overlapping the rest
+    auto mat_halo = [&](double* dst, int w, auto&& mat) {
+        if (dim == 3 && overlap_halos(w) && Lv[w].Nz >= 3) {
+            const int nz = Lv[w].Nz;
+            mat(0, 1);
+            mat(nz - 1, nz);
+            SGML_CUDA(cudaEventRecord(hx_ready, s));
+            SGML_CUDA(cudaStreamWaitEvent(hx_stream, hx_ready, 0));
+            tp->halo(dst, Lv[w].plane, nz, d_flag, hx_stream);
+            SGML_CUDA(cudaEventRecord(hx_done, hx_stream));
+            mat(1, nz - 1);
+            SGML_CUDA(cudaStreamWaitEvent(s, hx_done, 0));
+        } else {
+            mat(0, -1);
+            halo(dst, w);
+        }
+    };
     auto relax_level = [&](int v, double* in, int c, double* p0, double* p1) -> double* {
         const RelaxConst rc = relax_const(dim, v, g.h, a, cfg.safety, homogeneous, opts.stencil);
         double* cur = in;
@@ -910,12 +928,13 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                 if (count + (c - 1) > kMaxChain) {
                     // fold the pending increments into a full-grid base
                     const ChainEntry* ch = chain_at();
-                    launch(SGML_CLASS_MATERIALIZE, [&] {
-                        launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lv[v + 1],
-                                            v + 1, ch, count, bc, homogeneous, flag, diag_mode, s);
+                    mat_halo(other, 0, [&](int kb, int ke) {
+                        launch(SGML_CLASS_MATERIALIZE, [&] {
+                            launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lv[v + 1],
+                                                v + 1, ch, count, bc, homogeneous, flag, diag_mode, s, kb, ke);
+                        });
                     });
                     fstate[other] = face_want(homogeneous);
-                    halo(other, 0);
                     bs_valid = false;
                     std::swap(base, other);
                     base_zero = false;
@@ -929,12 +948,13 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                 ExtLay bl;
                 int wb;
                 base_src(v, bp, bl, wb);
-                launch(SGML_CLASS_MATERIALIZE, [&] {
-                    launch_materialize4(dim, in, Lv[v], v, bp, bl, wb, base_zero, ufinal, Lf, 1, ch, count,
-                                        bc, homogeneous, flag, diag_mode, s);
+                mat_halo(in, v, [&](int kb, int ke) {
+                    launch(SGML_CLASS_MATERIALIZE, [&] {
+                        launch_materialize4(dim, in, Lv[v], v, bp, bl, wb, base_zero, ufinal, Lf, 1, ch, count,
+                                            bc, homogeneous, flag, diag_mode, s, kb, ke);
+                    });
                 });
                 fstate[in] = face_want(homogeneous);
-                halo(in, v);
             }
             ufinal = relax_level(v, in, c, U[v][0], U[v][1]);
             count += c - 1;
@@ -948,12 +968,13 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
         } else if (v1 >= 1) {
             const ChainEntry* ch = chain_at();
             const ExtLay Lf = n > 1 ? Lv[1] : Lv[0];
-            launch(SGML_CLASS_MATERIALIZE, [&] {
-                launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lf, 1, ch, count,
-                                    bc, homogeneous, flag, diag_mode, s);
+            mat_halo(other, 0, [&](int kb, int ke) {
+                launch(SGML_CLASS_MATERIALIZE, [&] {
+                    launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lf, 1, ch, count,
+                                        bc, homogeneous, flag, diag_mode, s, kb, ke);
+                });
             });
             fstate[other] = face_want(homogeneous);
-            halo(other, 0);
             in0 = other;
         } else {
             in0 = base;

@@ -102,7 +102,7 @@ void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
                          const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
                          int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
-                         bool homogeneous, int* flag, bool diag, cudaStream_t s);
+                         bool homogeneous, int* flag, bool diag, cudaStream_t s, int kb = 0, int ke = -1);
 // per-node pseudo-time step of the sigma relaxation at every node of a level
 // array (own planes), from the level's sigma (with ghosts / halos)
 void launch_dtau_ext(int dim, const double* sig, const ExtLay& L, double* dt, const RelaxConst& rc, cudaStream_t s);

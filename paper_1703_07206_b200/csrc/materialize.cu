@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
     k_materialize4(double* __restrict__ out, ExtLay Lw, int w, const double* __restrict__ base,
                    ExtLay L0, int wb, int base_zero, const double* __restrict__ ufine, ExtLay Lf, int frel,
                    const ChainEntry* __restrict__ chain, int nchain, BcDev bc, int homogeneous,
-                   int* flag, int xtail) {
+                   int* flag, int xtail, int k0) {
     __shared__ ChainEntry sch[kMaxChain];
     const int tid = threadIdx.x + MBX * threadIdx.y;
     for (int c = tid; c < nchain; c += MBX * MBY) sch[c] = chain[c];
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
     // spread row index S (warp-uniform); 3D: local plane K (block-uniform),
     // global plane Kg (z-slab arrays start at global plane Lw.z0)
     const int S = blockIdx.y * MBY + threadIdx.y;
-    const int K = DIM == 3 ? (int)blockIdx.z : 0;
+    const int K = DIM == 3 ? k0 + (int)blockIdx.z : 0;
     const int Kg = DIM == 3 ? K + Lw.z0 : 0;
     int bad = 0, tiny = 0;
     if (S <= D && X4 < Nw) {
@@ -445,8 +445,10 @@ uint64_t ext_size(int dim, const ExtLay& L) {
 void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const double* base,
                          const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
                          int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
-                         bool homogeneous, int* flag, bool diag, cudaStream_t s) {
+                         bool homogeneous, int* flag, bool diag, cudaStream_t s, int kb, int ke) {
     const int Nw = Lw.N;
+    if (ke < 0) ke = Lw.Nz;
+    if (dim == 3 && ke <= kb) return;
     // two copies (y and y + (Nw-1)/2): measured faster than one (occupancy
     // does not pay for the lost weight sharing) and than four (16 nodes per
     // thread cost occupancy)
@@ -455,10 +457,11 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
     // and the last group writes the face node (xtail)
     const int xtail = (!bc.neu[1] && (Nw - 1) % MV == 0) ? 1 : 0;
     const int threads_x = xtail ? (Nw - 1) / MV : (Nw + MV - 1) / MV, D = (Nw - 1) / NC;
-    const dim3 grid((threads_x + MBX - 1) / MBX, (D + MBY) / MBY, dim == 3 ? Lw.Nz : 1);
+    const dim3 grid((threads_x + MBX - 1) / MBX, (D + MBY) / MBY, dim == 3 ? ke - kb : 1);
 #define SGML_MAT(DD, CC, GG)                                                                     \
     k_materialize4<DD, CC, GG><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, wb, base_zero, ufine, \
-                                                               Lf, frel, chain, nchain, bc, homogeneous, flag, xtail)
+                                                               Lf, frel, chain, nchain, bc, homogeneous, flag, xtail, \
+                                                               dim == 3 ? kb : 0)
     if (dim == 2) {
         if (diag) SGML_MAT(2, NC, true);
         else SGML_MAT(2, NC, false);
