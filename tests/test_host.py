@@ -111,3 +111,22 @@ def test_c_abi_struct_layouts():
     assert ctypes.sizeof(_capi.Bc) == 72
     assert ctypes.sizeof(_capi.CycleRecord) == 40
     assert ctypes.sizeof(_capi.DiagSample) == 24
+
+
+def test_c_abi_struct_sizes_match_the_header(tmp_path):
+    # the ctypes mirrors (paper_1703_07206_b200/_capi.py) against the C compiler's
+    # view of include/sgml_b200.h
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "sizes.c"
+    src.write_text('#include <stdio.h>\n#include "sgml_b200.h"\nint main(void) {\n'
+                   'printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(sgml_grid), sizeof(sgml_bc), '
+                   'sizeof(sgml_solver_cfg), sizeof(sgml_solver_opts), sizeof(sgml_cycle_record), '
+                   'sizeof(sgml_diag_sample), sizeof(sgml_report));\nreturn 0; }\n')
+    exe = tmp_path / "sizes"
+    subprocess.check_call(["gcc", "-I", os.path.join(root, "include"), str(src), "-o", str(exe)])
+    got = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    want = [ctypes.sizeof(t) for t in (_capi.Grid, _capi.Bc, _capi.SolverCfg, _capi.SolverOpts,
+                                       _capi.CycleRecord, _capi.DiagSample, _capi.Report)]
+    assert got == want
