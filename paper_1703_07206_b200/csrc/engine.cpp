@@ -752,6 +752,32 @@ void sgml_solver::cycle_dense(const double* src_dense, double* out_dense, bool h
     }
 }
 
+// A level visit qualifies for the one-CTA path when the level array is small,
+// single-GPU (or replicated), and no pass needs its Dirichlet faces rewritten
+// (set_faces would be a no-op for every output and du buffer).
+bool sgml_solver::small_visit(int v, const double* in, int c, const double* p0, const double* p1,
+                              bool homogeneous) const {
+    static const bool off = std::getenv("SGML_NO_SMALL_LEVELS") != nullptr;
+    if (off || dist(v) || c > kSmallMaxPasses || !compact()) return false;
+    long long nodes = 1;
+    for (int ax = 0; ax < g.dim; ++ax) nodes *= (long long)(rng[v].hi[ax] - rng[v].lo[ax] + 1);
+    if (nodes <= 0 || nodes > kSmallNodes) return false;
+    if (all_neumann) return true;
+    const int want = face_want(homogeneous);
+    const double* cur = in;
+    for (int p = 1; p <= c; ++p) {
+        const double* out = cur == p0 ? p1 : p0;
+        const int ins = faces_of(cur);
+        if (faces_of(out) != want) return false;
+        if (v > 0 && p < c) {
+            const int need = ins == want ? FS_ZERO : (ins == FS_ZERO && want == FS_BVAL ? FS_BVAL : -1);
+            if (need < 0 || faces_of(DU[v][p - 1]) != need) return false;
+        }
+        cur = out;
+    }
+    return true;
+}
+
 bool sgml_solver::use_graphs() const {
     static const int off = std::getenv("SGML_NO_GRAPHS") ? 1 : 0;
     return compact() && nrk == 1 && !off && opts.use_graph >= 0 && debug_sync <= 0 && !diag_mode;
@@ -848,6 +874,30 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
     auto relax_level = [&](int v, double* in, int c, double* p0, double* p1) -> double* {
         const RelaxConst rc = relax_const(dim, v, g.h, a, cfg.safety, homogeneous, opts.stencil);
         double* cur = in;
+        // small level array, faces already what every pass needs: all c
+        // passes in one CTA (one launch instead of c)
+        if (small_visit(v, in, c, p0, p1, homogeneous)) {
+            SmallPasses sp{};
+            sp.count = c;
+            sp.g = gsrc(v);
+            sp.sig = has_sigma ? S[v] : nullptr;
+            sp.dt = has_sigma ? DT[v] : nullptr;
+            for (int p = 1; p <= c; ++p) {
+                double* out = cur == p0 ? p1 : p0;
+                sp.in[p - 1] = cur;
+                sp.out[p - 1] = out;
+                sp.du[p - 1] = (v > 0 && p < c) ? DU[v][p - 1] : nullptr;
+                sp.slot[p - 1] = diag + slot + (p - 1);
+                sp.pass_slot[p - 1] = slot + (p - 1);
+                cur = out;
+            }
+            launch(v == 0 ? SGML_CLASS_RELAX0 : SGML_CLASS_RELAX_COARSE, [&] {
+                launch_relax_small(dim, has_sigma, sp, Lv[v], rng[v], rc, flag, s);
+            });
+            slot += c;
+            first = false;
+            return cur;
+        }
         for (int p = 1; p <= c; ++p) {
             double* out = cur == p0 ? p1 : p0;
             double* duo = (v > 0 && p < c) ? DU[v][p - 1] : nullptr;

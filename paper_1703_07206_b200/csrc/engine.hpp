@@ -207,6 +207,7 @@ struct sgml_solver {
     CycleGraph graphs[2];                 // by homogeneous
     CycleGraph* capturing = nullptr;
     bool use_graphs() const;
+    bool small_visit(int v, const double* in, int c, const double* p0, const double* p1, bool homogeneous) const;
     const double* cycle_graph(bool homogeneous);
     cudaEvent_t next_event();
     void harvest_spans();  // call after a stream synchronize

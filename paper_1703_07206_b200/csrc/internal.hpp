@@ -72,6 +72,24 @@ int relax_tiled_zb(int dim, int cols, int nz);
 struct NodeRange {
     int lo[3], hi[3];
 };
+// All c passes of one visit of a small level array in one CTA (engine:
+// levels of at most kSmallNodes relaxed nodes, single GPU, faces settled).
+constexpr int kSmallThreads = 512;
+constexpr int kSmallNodes = 6144;
+constexpr int kSmallMaxPasses = 16;
+struct SmallPasses {
+    const double* in[kSmallMaxPasses];
+    double* out[kSmallMaxPasses];
+    double* du[kSmallMaxPasses];
+    unsigned long long* slot[kSmallMaxPasses];
+    int pass_slot[kSmallMaxPasses];
+    int count;
+    const double* g;
+    const double* sig;  // level sigma (with ghosts), SIG only
+    const double* dt;   // per-node pseudo-time step, SIG only
+};
+void launch_relax_small(int dim, bool sig, const SmallPasses& sp, const ExtLay& L, const NodeRange& rg,
+                        const RelaxConst& rc, int* flag, cudaStream_t s);
 // One relaxation pass over a level array (every node a subset node):
 // uo (with mirror ghosts), duo = uo - ui (nullable, DU arrays), diag max
 // into diag_slot.  flag[0] <- 1 on a non-finite output, flag[1] <- 1 on a

@@ -575,6 +575,74 @@ void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, c
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Small level arrays: all c passes of one level visit in one CTA (the levels
+// whose arrays hold a few thousand nodes are launch-latency bound as one
+// kernel per pass).  Same arithmetic as the reference's relax branch
+// (kernels.cpp:94-137) on the ghost-extended array (mirror ghosts in memory),
+// with the edge terms unfused (identical bits whenever the fused form is
+// exact); passes are separated by __syncthreads.
+// ---------------------------------------------------------------------------
+template <int DIM, bool SIG, bool HAS_A>
+__global__ void __launch_bounds__(kSmallThreads) k_relax_small(SmallPasses sp, ExtLay L, int3 lo, int3 hi,
+                                                               RelaxConst rc, int* flag) {
+    const int nx = hi.x - lo.x + 1, ny = hi.y - lo.y + 1, nz = DIM == 3 ? hi.z - lo.z + 1 : 1;
+    const int total = nx * ny * nz;
+    const ptrdiff_t sy = L.Px, sz = DIM == 3 ? (ptrdiff_t)L.plane : 0;
+    for (int p = 0; p < sp.count; ++p) {
+        const double* __restrict__ u = sp.in[p];
+        double* __restrict__ o = sp.out[p];
+        double* __restrict__ du = sp.du[p];
+        double dmax = 0.0;
+        int bad = 0, tiny = 0;
+        for (int e = threadIdx.x; e < total; e += blockDim.x) {
+            const int i = lo.x + e % nx, j = lo.y + (e / nx) % ny, k = DIM == 3 ? lo.z + e / (nx * ny) : 0;
+            const ptrdiff_t pos = eix<DIM>(L, i, j, k);
+            const double uc = u[pos];
+            const double sc = SIG ? sp.sig[pos] : 1.0;
+            double acc = 0.0;
+#pragma unroll
+            for (int r = (DIM == 3 ? -1 : 0); r <= (DIM == 3 ? 1 : 0); ++r)
+#pragma unroll
+                for (int q = -1; q <= 1; ++q)
+#pragma unroll
+                    for (int pp = -1; pp <= 1; ++pp) {
+                        if (r == 0 && q == 0 && pp == 0) continue;
+                        const int l2 = r * r + q * q + pp * pp;
+                        if (stencil_skip(rc.compact, l2)) continue;
+                        const ptrdiff_t d = r * sz + q * sy + pp;
+                        const double sbar = SIG ? 0.5 * (sp.sig[pos + d] + sc) : 1.0;
+                        acc = acc + stencil_t<SIG>(sbar, u[pos + d], uc, l2);
+                    }
+            const double op = (acc * rc.pref) * rc.inv_s2;
+            const double gc = sp.g[pos];
+            const double diag = HAS_A ? fabs((op + rc.a * uc) - gc) : fabs(op - gc);
+            double value;
+            if (SIG) {
+                const double dtau = sp.dt[pos];
+                if (!(dtau > 0.0)) value = __longlong_as_double(0x7ff8000000000000LL);
+                else {
+                    const double num = uc + dtau * (op - gc);
+                    value = HAS_A ? num / (1.0 - dtau * rc.a) : num;
+                }
+            } else {
+                const double num = uc + rc.dtau1 * (op - gc);
+                value = HAS_A ? num / rc.denom1 : num;
+            }
+            dmax = dmax < diag ? diag : dmax;
+            const unsigned ex = (unsigned)__double2hiint(value) & 0x7ff00000u;
+            bad |= ex == 0x7ff00000u;
+            tiny |= ex < 0x03600000u;
+            store_ext<DIM>(o, L, i, j, k, value);
+            if (du) du[pos] = value - uc;
+        }
+        block_max_commit(dmax, sp.slot[p]);
+        block_bad_commit(bad, flag, sp.pass_slot[p]);
+        block_or_commit(tiny, flag + 1);
+        __syncthreads();  // pass p's outputs (and the reduction scratch) before pass p + 1
+    }
+}
 }  // namespace
 
 // planes per CTA: long marches amortise the 2-plane prologue, short ones
@@ -600,6 +668,21 @@ void launch_relax_tma(int dim, bool sig, const TmaSet& tm, double* uo, double* d
                       const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
                       unsigned long long* slot, int* flag, int pass_slot, cudaStream_t s) {
     launch_mode<MODE_RELAX>(dim, sig, tm, uo, duo, L, rg, rc, slot, flag, pass_slot, s);
+}
+
+void launch_relax_small(int dim, bool sig, const SmallPasses& sp, const ExtLay& L, const NodeRange& rg,
+                        const RelaxConst& rc, int* flag, cudaStream_t s) {
+    const int3 lo = make_int3(rg.lo[0], rg.lo[1], rg.lo[2]);
+    const int3 hi = make_int3(rg.hi[0], rg.hi[1], rg.hi[2]);
+#define SGML_SMALL(DD, SS, AA) k_relax_small<DD, SS, AA><<<1, kSmallThreads, 0, s>>>(sp, L, lo, hi, rc, flag)
+    if (dim == 2) {
+        if (sig) { if (rc.has_a) SGML_SMALL(2, true, true); else SGML_SMALL(2, true, false); }
+        else { if (rc.has_a) SGML_SMALL(2, false, true); else SGML_SMALL(2, false, false); }
+    } else {
+        if (sig) { if (rc.has_a) SGML_SMALL(3, true, true); else SGML_SMALL(3, true, false); }
+        else { if (rc.has_a) SGML_SMALL(3, false, true); else SGML_SMALL(3, false, false); }
+    }
+#undef SGML_SMALL
 }
 
 void launch_residual_tma(int dim, bool sig, const TmaSet& tm, double* r, double* utot,
