@@ -5,10 +5,11 @@
 //
 // plus deform (:100-125) and trifoil (:131-164).
 //
-// The problems are built on the host with the reference's closed forms and
-// curve deposition (problems.cpp:160-193, 217-300, 302-325, 374-398,
-// 500-521) so the inputs are the reference's bits (the libm calls stay on
-// the host); every solve, every timed cycle and every post-solve field
+// The closed-form problems are built on the host with the reference's
+// expressions (problems.cpp:160-193, 500-521) and the curve problems by the
+// library's builders (problems.cpp:302-325, 374-398; libm on the host, fields
+// on the device), so the inputs are the reference's bits; every solve,
+// every timed cycle and every post-solve field
 // (gradient, curl, node motion, streamlines) runs on the device through the
 // drop-in C++ API (include/sgml/*.hpp -> libsgml_b200.so).  Outputs use the
 // reference's file formats (io.cpp:35-178: %.17g, report.csv, trace.csv,
@@ -137,187 +138,78 @@ sgml::ProblemSpec capacitor(int n, const std::string& mode) {
 }
 
 
-// ---- curves and singular sources (problems.cpp:100-140, 217-300) ----------
+// ---- curve problems: the library's device builders (csrc/builders.cpp) ----
+// deformation_problem / trifoil_problem (problems.cpp:302-325, 374-398): the
+// curve work runs on the host inside the library, the fields are assembled on
+// the device and copied into the host Fields the drop-in API takes.
 
-struct Curve {
-    std::vector<sgml::Point> points;
-    std::vector<sgml::Point> payload;  // empty or one vector per point
-    bool closed = false;
+void ck(int status) {
+    if (status != SGML_OK) throw std::runtime_error(sgml_last_error());
+}
+
+sgml_ctx* builder_ctx() {
+    static sgml_ctx* ctx = nullptr;
+    if (!ctx) {
+        const char* d = std::getenv("SGML_DEVICE");
+        ck(sgml_ctx_create(d ? std::atoi(d) : 0, &ctx));
+    }
+    return ctx;
+}
+
+// a device field of the grid, freed on scope exit
+struct DevField {
+    sgml_field* f = nullptr;
+    explicit DevField(const sgml::Grid& g) { ck(sgml_field_create(builder_ctx(), g.dim, g.n, &f)); }
+    ~DevField() { sgml_field_destroy(f); }
+    DevField(const DevField&) = delete;
+    DevField& operator=(const DevField&) = delete;
+    sgml::Field host(const sgml::Grid& g) const {
+        sgml::Field h(g);
+        ck(sgml_field_download(f, h.data()));
+        return h;
+    }
 };
 
-sgml::Point sub(const sgml::Point& a, const sgml::Point& b) { return {a[0] - b[0], a[1] - b[1], a[2] - b[2]}; }
-sgml::Point add_scaled(const sgml::Point& a, double s, const sgml::Point& b) {
-    return {a[0] + s * b[0], a[1] + s * b[1], a[2] + s * b[2]};
-}
-double norm(const sgml::Point& a) { return std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]); }
-
-// uniform resampling at spacing ~h, unit tangents when payload is requested
-Curve resample_curve(const Curve& curve, double h) {
-    const std::size_t m_in = curve.points.size();
-    if (m_in < 2) throw std::invalid_argument("resample_curve: need at least 2 points");
-    if (!(h > 0.0)) throw std::invalid_argument("resample_curve: spacing must be positive");
-    const std::size_t segs = curve.closed ? m_in : m_in - 1;
-    std::vector<double> cum(segs + 1, 0.0);
-    for (std::size_t s = 0; s < segs; ++s)
-        cum[s + 1] = cum[s] + norm(sub(curve.points[(s + 1) % m_in], curve.points[s]));
-    const double length = cum[segs];
-    if (!(length > 0.0)) throw std::invalid_argument("resample_curve: curve has zero length");
-    const std::size_t m = static_cast<std::size_t>(std::max<long long>(1, std::llround(length / h)));
-    const double ds = length / static_cast<double>(m);
-    const std::size_t count = curve.closed ? m : m + 1;
-    Curve out;
-    out.closed = curve.closed;
-    std::size_t seg = 0;
-    for (std::size_t i = 0; i < count; ++i) {
-        const double s = std::min(static_cast<double>(i) * ds, length);
-        while (seg + 1 < segs && cum[seg + 1] < s) ++seg;
-        const double seg_len = cum[seg + 1] - cum[seg];
-        const double t = seg_len > 0.0 ? (s - cum[seg]) / seg_len : 0.0;
-        const sgml::Point& a = curve.points[seg % m_in];
-        const sgml::Point& b = curve.points[(seg + 1) % m_in];
-        out.points.push_back(add_scaled(a, t, sub(b, a)));
-    }
-    if (!curve.payload.empty()) {
-        const std::size_t mo = out.points.size();
-        out.payload.resize(mo);
-        for (std::size_t i = 0; i < mo; ++i) {
-            sgml::Point d;
-            if (curve.closed) d = sub(out.points[(i + 1) % mo], out.points[(i + mo - 1) % mo]);
-            else if (i == 0) d = sub(out.points[1], out.points[0]);
-            else if (i == mo - 1) d = sub(out.points[mo - 1], out.points[mo - 2]);
-            else d = sub(out.points[i + 1], out.points[i - 1]);
-            const double len = norm(d);
-            if (!(len > 0.0)) throw std::invalid_argument("resample_curve: degenerate tangent");
-            out.payload[i] = {d[0] / len, d[1] / len, d[2] / len};
-        }
-    }
-    return out;
-}
-
-// half the two adjacent chord lengths per sample
-std::vector<double> arc_elements(const Curve& curve) {
-    const std::size_t m = curve.points.size();
-    std::vector<double> ds(m, 0.0);
-    const std::size_t segs = curve.closed ? m : m - 1;
-    for (std::size_t s = 0; s < segs; ++s) {
-        const double len = norm(sub(curve.points[(s + 1) % m], curve.points[s]));
-        ds[s] += 0.5 * len;
-        ds[(s + 1) % m] += 0.5 * len;
-    }
-    return ds;
-}
-
-// tensor-hat scatter of one point mass, weights scaled by 1 / h^dim
-template <typename Deposit>
-void scatter_mass(const sgml::Point& p, const sgml::Grid& g, Deposit&& into) {
-    int idx[3] = {0, 0, 0};
-    double frac[3] = {0.0, 0.0, 0.0};
-    for (int c = 0; c < g.dim; ++c) {
-        const double x = p[c];
-        if (!(x >= 0.0 && x <= 1.0)) throw std::invalid_argument("deposit_delta: curve sample outside the unit domain");
-        int i0 = static_cast<int>(std::floor(x / g.h));
-        i0 = std::clamp(i0, 0, g.N - 2);
-        idx[c] = i0;
-        frac[c] = x / g.h - i0;
-    }
-    const double inv_hd = g.dim == 2 ? 1.0 / (g.h * g.h) : 1.0 / (g.h * g.h * g.h);
-    const double wx[2] = {1.0 - frac[0], frac[0]};
-    const double wy[2] = {1.0 - frac[1], frac[1]};
-    if (g.dim == 2) {
-        for (int b = 0; b < 2; ++b)
-            for (int a = 0; a < 2; ++a) into(idx[0] + a, idx[1] + b, 0, wx[a] * wy[b] * inv_hd);
-    } else {
-        const double wz[2] = {1.0 - frac[2], frac[2]};
-        for (int c = 0; c < 2; ++c)
-            for (int b = 0; b < 2; ++b)
-                for (int a = 0; a < 2; ++a) into(idx[0] + a, idx[1] + b, idx[2] + c, wx[a] * wy[b] * wz[c] * inv_hd);
-    }
-}
-
-bool inside_unit(const sgml::Point& p, int dim) {
-    for (int c = 0; c < dim; ++c)
-        if (!(p[c] >= 0.0 && p[c] <= 1.0)) return false;
-    return true;
-}
-
-sgml::Field deposit_delta(const Curve& curve, const sgml::Grid& grid, double strength) {
-    if (curve.points.size() < 2) throw std::invalid_argument("deposit_delta: need at least 2 points");
-    sgml::Field f(grid);
-    const std::vector<double> ds = arc_elements(curve);
-    for (std::size_t i = 0; i < curve.points.size(); ++i) {
-        const double mass = strength * ds[i];
-        scatter_mass(curve.points[i], grid, [&](int a, int b, int c, double w) { f.at(a, b, c) += mass * w; });
-    }
-    return f;
-}
-
-sgml::VectorField deposit_delta_vector(const Curve& curve, const sgml::Grid& grid) {
-    if (curve.payload.size() != curve.points.size())
-        throw std::invalid_argument("deposit_delta_vector: curve carries no payload");
-    sgml::VectorField f(grid);
-    const std::vector<double> ds = arc_elements(curve);
-    for (std::size_t i = 0; i < curve.points.size(); ++i) {
-        const sgml::Point& pay = curve.payload[i];
-        scatter_mass(curve.points[i], grid, [&](int a, int b, int c, double w) {
-            for (int comp = 0; comp < 3; ++comp) f.comp[comp].at(a, b, c) += pay[comp] * ds[i] * w;
-        });
-    }
-    return f;
-}
-
-// all-Neumann potential attracting nodes toward a closed curve (problems.cpp:302-325)
 struct DeformationSetup {
     sgml::ProblemSpec problem;
     sgml::Field f_raw;
     double raw_integral = 0.0;
 };
 
-DeformationSetup deformation_problem(const Curve& curve, double a, int n) {
+DeformationSetup deformation_problem(const std::vector<sgml::Point>& curve, double a, int n) {
     int dim = 2;
-    for (const sgml::Point& p : curve.points)
+    for (const sgml::Point& p : curve)
         if (p[2] != 0.0) dim = 3;
     const sgml::Grid grid = sgml::make_grid(dim, n);
+    std::vector<double> pts;
+    for (const sgml::Point& p : curve) pts.insert(pts.end(), p.begin(), p.end());
+    DevField f(grid), raw(grid);
     DeformationSetup setup;
-    const Curve rs = resample_curve(curve, grid.h);
-    setup.f_raw = deposit_delta(rs, grid, 1.0);
-    setup.raw_integral = sgml::trapezoid_mean(setup.f_raw);
+    ck(sgml_build_deformation_sources(pts.data(), (int)curve.size(), f.f, raw.f, &setup.raw_integral));
     setup.problem.grid = grid;
     setup.problem.a = a;
     setup.problem.bc = sgml::BoundarySpec::all_neumann();
-    setup.problem.f = setup.f_raw;
-    sgml::zero_mean_projection(setup.problem.f);
+    setup.problem.f = f.host(grid);
+    setup.f_raw = raw.host(grid);
     return setup;
 }
 
-// knotted vortex filament (problems.cpp:374-398): laplacian psi_c = -omega_c
 struct TrifoilSetup {
     std::array<sgml::ProblemSpec, 3> psi;
 };
 
 TrifoilSetup trifoil_problem(int n, double r) {
-    if (!(r > 0.0)) throw std::invalid_argument("trifoil_problem: r must be positive");
     const sgml::Grid grid = sgml::make_grid(3, n);
-    Curve raw;
-    raw.closed = true;
-    const int samples = 512;
-    raw.payload.resize(samples);
-    for (int s = 0; s < samples; ++s) {
-        const double t = 2.0 * kPi * s / samples;
-        raw.points.push_back({0.5 + r * (std::sin(t) + 2.0 * std::sin(2.0 * t)),
-                              0.5 + r * (std::cos(t) - 2.0 * std::cos(2.0 * t)), 0.5 - r * std::sin(3.0 * t)});
-    }
-    for (const sgml::Point& p : raw.points)
-        if (!inside_unit(p, 3))
-            throw std::invalid_argument("trifoil_problem: curve leaves the unit domain (max extent 3r)");
-    const Curve curve = resample_curve(raw, grid.h);
-    const sgml::VectorField omega = deposit_delta_vector(curve, grid);
+    DevField f0(grid), f1(grid), f2(grid);
+    sgml_field* fs[3] = {f0.f, f1.f, f2.f};
+    ck(sgml_build_trifoil_sources(fs, r));
     TrifoilSetup setup;
+    const DevField* src[3] = {&f0, &f1, &f2};
     for (int c = 0; c < 3; ++c) {
         sgml::ProblemSpec& prob = setup.psi[c];
         prob.grid = grid;
         prob.bc = sgml::BoundarySpec::all_dirichlet(0.0);
-        prob.f = omega.comp[c];
-        for (std::size_t p = 0; p < prob.f.size(); ++p) prob.f[p] = -prob.f[p];
+        prob.f = src[c]->host(grid);
     }
     return setup;
 }
@@ -458,10 +350,7 @@ int cmd_capacitor(const RunConfig& cfg, bool vtk) {
 int cmd_deform(const RunConfig& cfg, bool vtk) {
     if (cfg.curve_path.empty()) throw std::invalid_argument("deform: --curve PATH is required");
     std::filesystem::create_directories(cfg.out);
-    Curve curve;
-    curve.points = read_points_csv(cfg.curve_path);
-    curve.closed = true;
-    const DeformationSetup setup = deformation_problem(curve, cfg.a, cfg.n);
+    const DeformationSetup setup = deformation_problem(read_points_csv(cfg.curve_path), cfg.a, cfg.n);
     const sgml::SolveResult res = sgml::solve(setup.problem, solver_config(cfg));
     write_report(res.report, join(cfg.out, "report.csv"));
     write_trace(res.report, join(cfg.out, "trace.csv"));
