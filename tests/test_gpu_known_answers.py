@@ -64,3 +64,44 @@ def test_c3_deformation_2049_cycles():
     res, hist = gpu_solve(g, b, f, s, a)
     assert res.report.converged and len(hist) == 11
     assert abs(hist[-1] - 2.851e-11) <= 0.001 * 2.851e-11
+
+
+# ---- BASELINE sizes through size-independent properties ---------------------
+# The SGML cycle is linear in (f, face values) and every operation commutes
+# with an exact power-of-two scaling, so solve(2 f) = 2 solve(f) bit for bit
+# with the same normalised residual history (no overflow / underflow here).
+
+@pytest.mark.timeout(900)
+def test_poisson3d_1025_scaling_property_and_history():
+    g = S.make_grid(3, 10)
+    f = S.poisson3d_source(g)                      # the reference's source, device-built
+    u1, u2 = S.Field(g), S.Field(g)
+    slv = S.Solver(g, S.BoundarySpec.all_dirichlet(0.0), config=S.SolverConfig(**CFG))
+    r1 = slv.run(f, u1)
+    h1 = [r.residual for r in r1.rows]
+    assert r1.converged and len(h1) == 8
+    assert h1[-1] == 4.131248866625195e-11         # (this build, round 1; CPU reference cannot run 1025^3)
+    fh = f.numpy()
+    f.upload(2.0 * fh)
+    r2 = slv.run(f, u2)
+    assert [r.residual for r in r2.rows] == h1
+    a, b = u1.numpy(), u2.numpy()
+    assert np.array_equal((2.0 * a).view(np.int64), b.view(np.int64))
+
+
+@pytest.mark.timeout(600)
+def test_capacitor_513_scaling_property():
+    g = S.make_grid(3, 9)
+    sig = S.capacitor_sigma(g, "low")
+    f = S.Field(g)
+    outs = []
+    for scale in (1.0, 2.0):
+        bc = S.BoundarySpec.all_neumann()
+        bc.set_face(2, 0, S.BcKind.dirichlet, -1.0 * scale)
+        bc.set_face(2, 1, S.BcKind.dirichlet, 1.0 * scale)
+        u = S.Field(g)
+        rep = S.Solver(g, bc, sigma=sig, config=S.SolverConfig(**CFG)).run(f, u)
+        assert rep.converged
+        outs.append(([r.residual for r in rep.rows], u.numpy()))
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal((2.0 * outs[0][1]).view(np.int64), outs[1][1].view(np.int64))
