@@ -175,3 +175,27 @@ def test_streamed_vtk_matches_the_reference_bytes(dim, n, tmp_path):
     S.write_vector_vtk(vdev(g, v), tmp_path / "c.vtk", "velocity")
     O.ref_lib().ref_write_vector_vtk(O.C.byref(g), O._ptr(v), str(tmp_path / "d.vtk").encode(), b"velocity")
     assert (tmp_path / "c.vtk").read_bytes() == (tmp_path / "d.vtk").read_bytes()
+
+
+def test_new_entry_points_fail_like_the_reference():
+    g2, g3 = S.make_grid(2, 4), S.make_grid(3, 3)
+    with pytest.raises(ValueError):                 # problems.cpp:178: a 3D problem
+        S.poisson3d_source(g2)
+    with pytest.raises(ValueError):
+        S.capacitor_sigma(g3, "medium")              # problems.cpp:504
+    with pytest.raises(ValueError):
+        S.trifoil_sources(g3, 0.2)                   # problems.cpp:386-389: leaves the unit domain
+    with pytest.raises(ValueError):
+        S.deformation_sources([[0.5, 0.5, 0.0], [0.5, 0.5, 0.0]], g2)   # zero-length curve
+    with pytest.raises(ValueError):
+        S.write_field_vtk(S.Field(g3), "/nonexistent_dir/u.vtk", "u")  # io.cpp:17: cannot open
+    f = S.Field(g3)
+    bad = np.zeros(g3.total)
+    bad[5] = np.nan
+    probs = [S.ProblemSpec(g3, np.zeros(g3.total), bc=S.BoundarySpec.all_dirichlet(1.0)),
+             S.ProblemSpec(g3, bad, bc=S.BoundarySpec.all_dirichlet(1.0))]
+    with pytest.raises(ValueError):                 # cycle.cpp:150-152 inside the pipeline
+        S.solve_many(probs, S.SolverConfig(tol=1e-10))
+    # the context stays usable afterwards
+    res = S.solve_many(probs[:1], S.SolverConfig(tol=1e-10))
+    assert res[0].report.converged
