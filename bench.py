@@ -13,18 +13,29 @@ cycles * U(n, n_r) * N^3 / time (cycle.cpp:191-192, sgml_main.cpp:218-219).
   e2e    the C-ABI with pinned host buffers: every step copies its f in
          (H2D), solves, and copies its u out (D2H) inside the timed region
          (sgml_solve_many: step k+1's H2D and step k-1's D2H overlap step k).
+         e2e_single: the same through one blocking sgml_solve call per step
+         (the drop-in sgml::solve path, no overlap).
   roofline  the level-0 relaxation pass (the dominant kernel), algorithmic
          bytes 24 B per relaxed node (read u_prev and g, write u; (N-2)^3
          nodes off the Dirichlet faces) / its mean launch time from CUDA
          events recorded around each launch inside the timed region;
          roofline_fp64 the same launches against the fp64 issue roof.
   cpu_baseline  the reference core itself (oracle/_ref, compiled from
-         /root/reference) on the host's cores, one single_cycle of
-         poisson3d_problem(7) (129^3) per sample.
+         /root/reference) on the host's cores, on the SAME 513^3 problem: a
+         systematic sample of the steps of its cycle (every m-th schedule
+         step, m odd, ~20 s), executed through the reference's own
+         restriction_into / relaxation_interpolation (oracle/ref_shim.cpp).
 
---impl reference runs only that CPU reference (rank 0) on the same metric.
-Multi-GPU (torchrun, N > 1): the N ranks solve the same 513^3 problem with
-the z-slab decomposition (one NCCL clique, halo planes between
+--impl reference: the reference's CPU solve of the same 513^3 problem on all
+host cores, one full cycle (its schedule steps plus the residual recurrence,
+exactly as solve() runs cycle 0) split into K consecutive timed chunks, one
+chunk per step; value = the cycle's node updates / the K chunks' time.  The
+reference's cost per cycle does not depend on the cycle index, so this is
+its solve rate; the full 8-cycle 513^3 solve takes ~8x the cycle.
+Multi-GPU (--gpus N > 1): without torchrun the script re-launches itself
+under torch.distributed.run with N ranks (exit 2 if fewer GPUs are
+visible); the N ranks solve the same 513^3 problem with the z-slab
+decomposition (one NCCL clique, halo planes between
 neighbours, max reductions; strong scaling, value = the problem's updates /
 the max-over-ranks device time).
 """
@@ -59,7 +70,6 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--n", type=int, default=9, help="grid exponent, N = 2^n + 1 (default 513^3)")
     p.add_argument("--engine", choices=["compact", "literal"], default="compact")
-    p.add_argument("--cpu-n", type=int, default=7, help="grid exponent of the CPU sample")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     return p.parse_args()
@@ -180,50 +190,126 @@ def units(n: int, n_r: int = 2) -> int:
 
 # ------------------------------------------------------------ cpu side ----
 
-def cpu_sample(n: int, budget_s: float = 12.0):
-    """The reference core (oracle/_ref) or, if absent, the C port: single cycles
-    of poisson3d at 2^n+1 until ~budget_s; returns (rate, kind, cores, sample)."""
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def ref_session(n: int):
+    """The reference's solve of the bench problem, steppable (oracle/ref_shim.cpp)."""
     from oracle import oracle as O  # checker / baseline only
-    impl = "ref" if O.ref_lib() is not None else "c"
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     g = O.make_grid(3, n)
-    f = O.fill("poisson3d", g)
-    bc = O.all_dirichlet(0.0)
-    t_total, cycles = 0.0, 0
-    while cycles < 1 or (t_total < budget_s and cycles < 30):
+    sess = O.RefSession(g, O.all_dirichlet(0.0), poisson3d_source(n), None, 0.0, 2, 0.9)
+    return O, g, sess
+
+
+def chunk_plan(schedule, k: int):
+    """Split one cycle's schedule steps into min(k, steps) consecutive chunks
+    of about equal work units."""
+    from oracle import oracle as O
+    w = [O.RefSession.units(st) for st in schedule]
+    U = sum(w)
+    k = max(1, min(k, len(schedule)))
+    chunks, cur, acc = [], [], 0
+    for i, wi in enumerate(w):
+        cur.append(i)
+        acc += wi
+        left_steps = len(w) - i - 1
+        left_chunks = k - len(chunks) - 1
+        if left_chunks > 0 and (acc >= U * (len(chunks) + 1) / k or left_steps == left_chunks):
+            chunks.append(cur)
+            cur = []
+    chunks.append(cur)
+    return chunks, w, U
+
+
+def cpu_sample(n: int, budget_s: float = 20.0):
+    """cpu_baseline: the reference core (oracle/_ref) on the same problem, a
+    systematic sample of its cycle's schedule steps (every m-th step, m odd so
+    both step kinds are sampled) sized for ~budget_s; the C port's single
+    cycles at 129^3 if the reference build is absent."""
+    from oracle import oracle as O  # checker / baseline only
+    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+    cores = int(os.environ["OMP_NUM_THREADS"])  # the threads the reference's OpenMP loops use
+    if O.ref_lib() is None:
+        g = O.make_grid(3, 7)
+        f = O.fill("poisson3d", g)
         t0 = time.perf_counter()
-        st, _, _, w = O.single_cycle(g, bc, f, None, 0.0, False, 2, 0.9, 0, 1.0, impl=impl)
+        st, _, _, w = O.single_cycle(g, O.all_dirichlet(0.0), f, None, 0.0, False, 2, 0.9, 0, 1.0, impl="c")
+        dt = time.perf_counter() - t0
+        return (units(7) * g.total / dt, "port", 1,
+                f"1 x single_cycle of poisson3d_problem(7) (129^3) by the C restatement, 1 thread, {dt:.1f} s")
+    _, g, sess = ref_session(n)
+    sched = sess.schedule
+    U = units(n)
+    est_s = U * g.total / 3e8  # rough reference rate on ~16 cores
+    m = max(1, int(round(est_s / budget_s)))
+    if m % 2 == 0:
+        m += 1
+    picks = list(range(0, len(sched), m))
+    sess.begin_cycle(False)
+    t_total, done = 0.0, 0
+    for i in picks:
+        t0 = time.perf_counter()
+        assert sess.step(i) == 0
         t_total += time.perf_counter() - t0
-        cycles += 1
-        assert st == 0 and w == units(n)
-    rate = cycles * units(n) * g.total / t_total
-    kind = "reference" if impl == "ref" else "port"
-    sample = (f"{cycles} x single_cycle of poisson3d_problem({n}) ({g.N}^3, U={units(n)} passes) "
-              f"on {cores} OpenMP threads, {t_total:.1f} s")
-    return rate, kind, cores, sample, t_total / cycles
+        done += O.RefSession.units(sched[i])
+    sess.close()
+    rate = done * g.total / t_total
+    sample = (f"reference solve of poisson3d_problem({n}) ({g.N}^3): every {m}-th of the {len(sched)} "
+              f"schedule steps of its cycle ({len(picks)} steps, {done} of {U} work units) on {cores} "
+              f"OpenMP threads, {t_total:.1f} s")
+    return rate, "reference", cores, sample, t_total
 
 
 def run_reference(args, dist):
-    """--impl reference: the reference's CPU path on this box's host cores."""
+    """--impl reference: the reference's CPU solve of the same problem on this
+    box's host cores, one full cycle in K consecutive chunks (one per step)."""
     if dist.rank != 0:
         return None
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
-    rates, secs = [], []
-    for i in range(args.warmup + args.steps):
-        rate, kind, cores, sample, sec = cpu_sample(args.cpu_n, budget_s=0.0)
-        if i >= args.warmup:
-            rates.append(rate)
-            secs.append(sec)
-    value = statistics.median(rates)
+    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+    cores = int(os.environ["OMP_NUM_THREADS"])
+    O, g, sess = ref_session(args.n)
+    chunks, w, U = chunk_plan(sess.schedule, args.steps)
+    T = g.total
+
+    def run_chunk(c: int) -> float:
+        t0 = time.perf_counter()
+        if c == 0:
+            sess.begin_cycle(False)
+        for i in chunks[c]:
+            if sess.step(i) != 0:
+                raise RuntimeError("reference pass failed")
+        if c == len(chunks) - 1:
+            sess.recurrence()
+        return time.perf_counter() - t0
+
+    for i in range(args.warmup):
+        run_chunk(i % len(chunks))
+    secs, work = [], 0
+    for i in range(args.steps):
+        c = i % len(chunks)
+        secs.append(run_chunk(c))
+        work += sum(w[j] for j in chunks[c])
+    sess.close()
+    total_s = sum(secs)
+    value = work * T / total_s
+    cycle_s = total_s * U / work
+    sample = (f"cycle 0 of the reference solve of poisson3d_problem({args.n}) ({g.N}^3, U={U} work units, "
+              f"{len(sess.schedule)} schedule steps + the residual recurrence) split into {len(chunks)} "
+              f"consecutive chunks, one per step; {cores} OpenMP threads")
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
+        "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"3D Poisson {(1 << args.n) + 1}^3 fp64 solve to 1e-10 "
-                               f"(sampled: one reference cycle per step at {(1 << args.cpu_n) + 1}^3)",
-                   "n": args.n, "sample_n": args.cpu_n, "n_r": 2, "tol": 1e-10, "safety": 0.9},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+        "config": {"workload": f"3D Poisson {g.N}^3 fp64, Dirichlet 0, manufactured "
+                               f"sin(pi x)sin(pi y)sin(pi z) (poisson3d_problem({args.n})), "
+                               "solve to 1e-10 normalised residual",
+                   "n": args.n, "N": g.N, "n_r": 2, "tol": 1e-10, "safety": 0.9,
+                   "sample": "one full cycle of the solve (every cycle costs the same)"},
+        "cycle_s": cycle_s,
+        "time_to_tol_s_est": 8 * cycle_s,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -372,6 +458,30 @@ def run_ours(args, dist):
                "finite": e2e_ok, "final_residual": e2e_final}
         lib.sgml_host_free(fp)
         lib.sgml_host_free(up)
+        # the single-call drop-in path: sgml::solve(ProblemSpec) -> one blocking
+        # sgml_solve per step on pageable host memory (std::vector-like numpy
+        # arrays), no overlap between steps
+        fpg = np.ascontiguousarray(f_host)
+        upg = np.empty(T, np.float64)
+
+        def call_pageable():
+            rbuf.c.n_rows = rbuf.c.n_trace = 0
+            _capi.check(lib.sgml_solve(ctx.handle, 3, n, C.byref(cbc), fpg.ctypes.data_as(_capi._D), None, 0.0,
+                                       C.byref(ccfg), C.byref(copts), upg.ctypes.data_as(_capi._D),
+                                       C.byref(rbuf.c)))
+            return rbuf.c.n_rows
+
+        call_pageable()
+        k1 = min(args.steps, 5)
+        dist.barrier()
+        t_0 = time.perf_counter()
+        cyc1 = sum(call_pageable() for _ in range(k1))
+        dt1 = dist.reduce(time.perf_counter() - t_0, "max")
+        e2e["single_call"] = {"value": cyc1 * units(n) * T / dt1, "unit": UNIT, "steps": k1,
+                              "ms_per_step": 1e3 * dt1 / k1, "h2d_bytes_per_step": nbytes,
+                              "d2h_bytes_per_step": nbytes,
+                              "api": "sgml_solve per step (the sgml::solve drop-in path), pageable host f/u, "
+                                     "host wall clock around the blocking call"}
 
     last = reps[-1]
     line = {
@@ -406,7 +516,7 @@ def run_ours(args, dist):
         line["e2e"] = e2e
     if not args.no_cpu and dist.rank == 0 and args.gpus == 1:
         try:
-            rate, kind, cores, sample, _ = cpu_sample(args.cpu_n)
+            rate, kind, cores, sample, _ = cpu_sample(args.n)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                                     "sample": sample}
         except Exception as exc:  # the baseline must not sink the measurement
@@ -415,11 +525,51 @@ def run_ours(args, dist):
     return line if dist.rank == 0 else None
 
 
+def visible_gpus() -> int:
+    try:
+        import torch
+        return torch.cuda.device_count() if torch.cuda.is_available() else 0
+    except Exception:
+        return 0
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def launcher_cmd(gpus: int, argv) -> list:
+    """The torch.distributed.run command that runs this script on `gpus` ranks
+    of this node (one process per GPU)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+
+
 def main():
     args = parse()
     world, rank, local = dist_env()
+    if world == 1 and args.gpus > 1 and args.impl == "ours":
+        # --gpus N without torchrun: one process per GPU, or fail loudly (a
+        # single process must never report an N-GPU number)
+        have = visible_gpus()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
+                  file=sys.stderr, flush=True)
+            sys.exit(2)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # keep stdout one JSON line
+        cmd = launcher_cmd(args.gpus, sys.argv[1:])
+        os.execv(cmd[0], cmd)
     if world > 1:
         args.gpus = world
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        if args.impl == "ours" and visible_gpus() < world:
+            print(f"bench.py: {world} ranks need {world} visible GPUs, found {visible_gpus()}",
+                  file=sys.stderr, flush=True)
+            sys.exit(2)
     dist = Dist(world, rank, local)
     try:
         line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)

@@ -82,6 +82,9 @@ typedef struct {
     int stencil;    /* SGML_STENCIL_RADIAL (0, the reference's 9/27-point form) or
                        SGML_STENCIL_COMPACT (1, 5/7-point, no
                        reference counterpart, parity unpinned) */
+    int small_levels; /* 0 (default): a visit of a small level array (<= 6144 relaxed
+                       nodes) runs all its passes in one CTA; -1: one TMA launch per
+                       pass on every level (same bits either way) */
 } sgml_solver_opts;
 
 enum { SGML_STENCIL_RADIAL = 0, SGML_STENCIL_COMPACT = 1 };

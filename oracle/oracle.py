@@ -148,6 +148,14 @@ def _load_ref():
     lib.ref_deformation_setup.argtypes = [_D, C.c_int, C.c_double, C.c_int, _D, _D, _D]
     lib.ref_write_field_vtk.argtypes = [G, _D, C.c_char_p, C.c_char_p]
     lib.ref_write_vector_vtk.argtypes = [G, _D, C.c_char_p, C.c_char_p]
+    lib.ref_session_create.argtypes = [G, B, _D, _D, C.c_double, C.c_int, C.c_double]
+    lib.ref_session_create.restype = C.c_void_p
+    lib.ref_session_destroy.argtypes = [C.c_void_p]
+    lib.ref_session_nsteps.argtypes = [C.c_void_p]
+    lib.ref_session_begin_cycle.argtypes = [C.c_void_p, C.c_int]
+    lib.ref_session_step.argtypes = [C.c_void_p, C.c_int, _D]
+    lib.ref_session_recurrence.argtypes = [C.c_void_p]
+    lib.ref_session_recurrence.restype = C.c_double
     return lib
 
 
@@ -350,6 +358,45 @@ def ref_problem(name: str, n: int):
         raise ValueError(name)
     bc = make_bc(list(kinds), list(vals))
     return g, bc, f, (sig if rc == 3 else None), a.value
+
+
+class RefSession:
+    """The reference's solve driven one schedule step at a time (timing only:
+    bench.py's reference arm and cpu_baseline; oracle/ref_shim.cpp)."""
+
+    def __init__(self, g: Grid, bc: Bc, f, sigma=None, a=0.0, n_r=2, safety=0.9):
+        lib = ref_lib()
+        if lib is None:
+            raise RuntimeError("reference build unavailable")
+        self.lib = lib
+        f = np.ascontiguousarray(f, np.float64).reshape(-1)
+        sig = None if sigma is None else np.ascontiguousarray(sigma, np.float64).reshape(-1)
+        self.h = lib.ref_session_create(C.byref(g), C.byref(bc), _ptr(f), _ptr(sig), a, n_r, safety)
+        self.schedule = build_schedule(g.n, n_r)
+        assert lib.ref_session_nsteps(self.h) == len(self.schedule)
+
+    @staticmethod
+    def units(step) -> int:
+        kind, level, count = step
+        return level if kind == 0 else count
+
+    def begin_cycle(self, homogeneous: bool = False) -> None:
+        self.lib.ref_session_begin_cycle(self.h, int(homogeneous))
+
+    def step(self, index: int) -> int:
+        d = np.zeros(1)
+        return self.lib.ref_session_step(self.h, index, _ptr(d))
+
+    def recurrence(self) -> float:
+        return self.lib.ref_session_recurrence(self.h)
+
+    def close(self) -> None:
+        if self.h:
+            self.lib.ref_session_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 def closed_form_work_units(n: int, n_r: int) -> int:

@@ -7,7 +7,9 @@
 // anything else loaded in the process.  The functions mirror
 // oracle/sgml_oracle.h (prefix ref_ instead of og_) so tests can run the
 // restatement and the reference side by side on identical inputs.
+#include <cstdlib>
 #include <cstring>
+#include <new>
 #include <stdexcept>
 
 #include "sgml/cycle.hpp"
@@ -20,6 +22,31 @@ extern "C" {
 }
 
 namespace R = sgml;  // expands to sgml_ref under -Dsgml=sgml_ref
+
+// ---- zero-padded allocations for the reference's code in this library -----
+// The reference's interpolation reads zero-weight corners past the end of
+// du_prev on non-Dirichlet high faces (kernels.cpp:140-174):
+// up to half an array past its end.  What those bytes decode to is heap
+// layout (undefined behaviour); Inf/NaN there turns 0 * x non-finite and
+// the reference reports nan_detected at random.  Every allocation the
+// reference's code makes in this library is therefore followed by as many
+// zero bytes as it holds (calloc; large blocks are fresh zero pages that are
+// never touched), so the past-the-end reads see 0 -- the outcome the C
+// restatement and the B200 engine implement.  The library is linked with
+// -Bsymbolic-functions and loaded RTLD_LOCAL, so only this library's calls
+// bind here; calloc/free stay compatible with the process's own
+// operator new/delete.
+#define SGML_REF_HIDDEN
+SGML_REF_HIDDEN void* operator new(std::size_t n) {
+    void* p = std::calloc(1, 2 * n + 64);
+    if (!p) throw std::bad_alloc();
+    return p;
+}
+SGML_REF_HIDDEN void* operator new[](std::size_t n) { return ::operator new(n); }
+SGML_REF_HIDDEN void operator delete(void* p) noexcept { std::free(p); }
+SGML_REF_HIDDEN void operator delete[](void* p) noexcept { std::free(p); }
+SGML_REF_HIDDEN void operator delete(void* p, std::size_t) noexcept { std::free(p); }
+SGML_REF_HIDDEN void operator delete[](void* p, std::size_t) noexcept { std::free(p); }
 
 namespace {
 
@@ -167,6 +194,97 @@ int ref_solve(const og_grid* g, const og_bc* bc, const double* f, const double* 
     rep->normalization = r.normalization;
     rep->node_updates = r.node_updates;
     return 0;
+}
+
+// ---- timing sessions (bench.py --impl reference / cpu_baseline) ----------
+// The reference's solve (cycle.cpp:140-247) driven one schedule step at a
+// time through its own public functions, so a bounded part of a large solve
+// can be timed: begin_cycle = the per-cycle set-up of solve + single_cycle
+// (cycle.cpp:179-180, 83-84), step = one ScheduleStep exactly as
+// single_cycle runs it (cycle.cpp:88-109: restriction_into, or reset_level
+// on a level change + count x (swap_buffers, relaxation_interpolation)),
+// recurrence = the rest of solve's cycle (u_total += e, residual_update,
+// max_abs; cycle.cpp:191-198).
+struct ref_session {
+    R::Grid grid;
+    R::BoundarySpec bc;
+    R::Field r, u_total;
+    R::SolveState state;
+    R::Field g, scratch;
+    R::CycleSchedule schedule;
+    std::vector<R::Field> sigma_levels;
+    R::Field sigma;
+    double a = 0.0, safety = 0.9;
+    int current_level = -1;
+    std::uint64_t work = 0;
+    bool homogeneous = false;
+    explicit ref_session(const R::Grid& gr) : grid(gr), r(gr), u_total(gr), state(gr) {}
+};
+
+void* ref_session_create(const og_grid* g, const og_bc* bc, const double* f, const double* sigma, double a,
+                         int n_r, double safety) {
+    const R::Grid gr = grid_of(g);
+    auto* s = new ref_session(gr);
+    s->bc = to_bc(bc);
+    s->r = to_field(gr, f);
+    if (sigma) {
+        s->sigma = to_field(gr, sigma);
+        s->sigma_levels = R::restrict_sigma_levels(s->sigma, gr.n);
+    }
+    s->a = a;
+    s->safety = safety;
+    s->schedule = R::build_schedule(gr.n, n_r);
+    return s;
+}
+
+void ref_session_destroy(void* p) { delete static_cast<ref_session*>(p); }
+
+int ref_session_nsteps(void* p) { return (int)static_cast<ref_session*>(p)->schedule.steps.size(); }
+
+void ref_session_begin_cycle(void* p, int homogeneous) {
+    auto* s = static_cast<ref_session*>(p);
+    s->state.u.fill(0.0);
+    s->state.u_prev.fill(0.0);
+    s->g = R::Field(s->grid);
+    s->scratch = R::Field(s->grid);
+    s->current_level = -1;
+    s->homogeneous = homogeneous != 0;
+}
+
+// returns 0, or 1 when a pass throws kernel_error
+int ref_session_step(void* p, int index, double* diag_max) {
+    auto* s = static_cast<ref_session*>(p);
+    const R::ScheduleStep& st = s->schedule.steps.at((size_t)index);
+    try {
+        if (st.kind == R::ScheduleStep::Kind::restrict_source) {
+            R::restriction_into(s->r, st.level, s->bc, s->g, s->scratch, &s->work);
+        } else {
+            if (st.level != s->current_level) {
+                s->state.reset_level(st.level);
+                s->current_level = st.level;
+            }
+            const R::Field* sig = s->sigma_levels.empty() ? nullptr : &s->sigma_levels[(size_t)st.level];
+            double dmax = 0.0;
+            for (int c = 0; c < st.count; ++c) {
+                s->state.swap_buffers();
+                const double d = R::relaxation_interpolation(s->state, s->g, sig, s->a, s->safety, s->bc,
+                                                             s->homogeneous, &s->work);
+                dmax = d > dmax ? d : dmax;
+            }
+            if (diag_max) *diag_max = dmax;
+        }
+    } catch (const R::kernel_error&) {
+        return 1;
+    }
+    return 0;
+}
+
+double ref_session_recurrence(void* p) {
+    auto* s = static_cast<ref_session*>(p);
+    const R::Field& e = s->state.u;
+    for (std::size_t q = 0; q < s->u_total.size(); ++q) s->u_total[q] += e[q];
+    R::residual_update(s->r, e, R::OperatorCoefficients{s->sigma.size() ? &s->sigma : nullptr, s->a}, s->bc);
+    return R::max_abs(s->r);
 }
 
 // Reference problem builders: the exact source/coefficient bits the

@@ -474,13 +474,14 @@ class SolverOptions:
     timing: bool = False
     timing_classes: int = 0     # 0: time every kernel class; else a mask of 1 << class index
     stencil: str = "radial"     # "radial" (the reference's) or "compact" 5/7-point (no reference)
+    small_levels: bool = True   # one CTA per visit of a small level array (else one launch per pass)
 
     def to_c(self) -> _capi.SolverOpts:
         if self.stencil not in ("radial", "compact"):
             raise ValueError("stencil must be 'radial' or 'compact'")
         return _capi.SolverOpts(0 if self.engine == "compact" else 1, 1 if self.use_graph else -1,
                                 int(self.timing), int(self.timing_classes),
-                                0 if self.stencil == "radial" else 1)
+                                0 if self.stencil == "radial" else 1, 0 if self.small_levels else -1)
 
 
 @dataclass
@@ -631,12 +632,28 @@ def solve_many(problems: Sequence[ProblemSpec], config: SolverConfig = SolverCon
     p0 = problems[0]
     g = p0.grid
     fs = [np.ascontiguousarray(p.f, np.float64).reshape(-1) for p in problems]
-    for p, f in zip(problems, fs):
-        if p.grid != g or f.size != g.total:
-            raise ValueError("solve_many: every problem must share the grid")
+    bc0 = bytes(p0.bc.to_c())
     sig = None
     if p0.sigma is not None:
         sig = np.ascontiguousarray(p0.sigma, np.float64).reshape(-1)
+    for p, f in zip(problems, fs):
+        if p.grid != g or f.size != g.total:
+            raise ValueError("solve_many: every problem must share the grid")
+        if bytes(p.bc.to_c()) != bc0 or float(p.a) != float(p0.a):
+            raise ValueError("solve_many: every problem must share bc and a")
+        if (p.sigma is None) != (sig is None) or (
+                sig is not None and p.sigma is not p0.sigma
+                and not np.array_equal(np.asarray(p.sigma, np.float64).reshape(-1), sig)):
+            raise ValueError("solve_many: every problem must share sigma")
+        if p.exact is not None:
+            raise ValueError("solve_many: exact solutions (l1 rows) need solve()")
+    if out is not None:
+        if len(out) != len(problems):
+            raise ValueError("solve_many: one output array per problem")
+        for u in out:
+            if not (isinstance(u, np.ndarray) and u.dtype == np.float64 and u.flags.c_contiguous
+                    and u.size == g.total):
+                raise ValueError("solve_many: outputs must be C-contiguous float64 arrays of grid.total")
     us = list(out) if out is not None else [np.empty(g.total, np.float64) for _ in problems]
     rbs = [_ReportBuffers() for _ in problems]
     reps = (_capi.Report * len(problems))(*[rb.c for rb in rbs])

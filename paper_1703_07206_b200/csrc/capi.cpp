@@ -31,6 +31,11 @@ void same_grid(const sgml_field* a, const sgml_field* b, const char* what) {
 
 void activate(sgml_ctx* ctx) { SGML_CUDA(cudaSetDevice(ctx->device)); }
 
+// entry points that use the context's reduction slots, flags or pinned
+// staging hold its lock for the whole call (the reference's functions are
+// reentrant; concurrent callers of one context must not share that scratch)
+using CtxLock = std::lock_guard<std::recursive_mutex>;
+
 double slot_to_double(unsigned long long bits) {
     double d;
     std::memcpy(&d, &bits, sizeof d);
@@ -106,7 +111,7 @@ int sgml_ctx_join_nccl(sgml_ctx* ctx, int nranks, int rank, const unsigned char 
     return guarded([&] {
         require(ctx && id, SGML_EINVAL, "ctx_join_nccl: null argument");
         require(nranks >= 1 && rank >= 0 && rank < nranks, SGML_EINVAL, "ctx_join_nccl: bad rank");
-        std::lock_guard<std::mutex> lk(ctx->mu);
+        std::lock_guard<std::recursive_mutex> lk(ctx->mu);
         SGML_CUDA(cudaSetDevice(ctx->device));
         delete ctx->cached;
         ctx->cached = nullptr;
@@ -132,7 +137,7 @@ int sgml_ctx_join_local(sgml_ctx* ctx, sgml_group* g, int rank) {
     return guarded([&] {
         require(ctx && g, SGML_EINVAL, "ctx_join_local: null argument");
         require(rank >= 0 && rank < g->g->size, SGML_EINVAL, "ctx_join_local: bad rank");
-        std::lock_guard<std::mutex> lk(ctx->mu);
+        std::lock_guard<std::recursive_mutex> lk(ctx->mu);
         delete ctx->cached;
         ctx->cached = nullptr;
         ctx->cached_key.clear();
@@ -356,6 +361,7 @@ int sgml_relaxation_interpolation(sgml_field* u, const sgml_field* u_prev, sgml_
         require(level >= 0 && level <= u->grid.n, SGML_EINVAL, "relaxation_interpolation: bad level");
         sgml_ctx* ctx = u->ctx;
         activate(ctx);
+        CtxLock lk(ctx->mu);
         const cudaStream_t s = ctx->stream;
         const sgml_grid& gr = u->grid;
         SGML_CUDA(cudaMemsetAsync(ctx->d_slots, 0, sizeof(unsigned long long), s));
@@ -398,6 +404,7 @@ int sgml_max_abs(const sgml_field* f, double* out) {
         require(f && out, SGML_EINVAL, "max_abs: null argument");
         sgml_ctx* ctx = f->ctx;
         activate(ctx);
+        CtxLock lk(ctx->mu);
         const cudaStream_t s = ctx->stream;
         SGML_CUDA(cudaMemsetAsync(ctx->d_slots, 0, sizeof(unsigned long long), s));
         launch_max_abs(f->d, f->grid.total, ctx->d_slots, s);
@@ -412,6 +419,7 @@ int sgml_trapezoid_mean(const sgml_field* f, double* out) {
     return guarded([&] {
         require(f && out, SGML_EINVAL, "trapezoid_mean: null argument");
         activate(f->ctx);
+        CtxLock lk(f->ctx->mu);
         *out = trapezoid_mean_host(f->ctx, f->grid, f->d);
     });
 }
@@ -420,6 +428,7 @@ int sgml_zero_mean_projection(sgml_field* f) {
     return guarded([&] {
         require(f != nullptr, SGML_EINVAL, "zero_mean_projection: null field");
         activate(f->ctx);
+        CtxLock lk(f->ctx->mu);
         const double mean = trapezoid_mean_host(f->ctx, f->grid, f->d);
         launch_sub_scalar(f->d, f->grid.total, mean, f->ctx->stream);
         SGML_CUDA(cudaGetLastError());
@@ -446,6 +455,7 @@ int sgml_restrict_sigma_levels(const sgml_field* sigma, sgml_field* const* level
         for (int v = 0; v < g.n; ++v) same_grid(sigma, levels[v], "restrict_sigma_levels: grid mismatch");
         sgml_ctx* ctx = sigma->ctx;
         activate(ctx);
+        CtxLock lk(ctx->mu);
         const cudaStream_t s = ctx->stream;
         sgml_bc even{};
         for (int f = 0; f < 6; ++f) even.kind[f] = 1;
@@ -486,6 +496,7 @@ int sgml_single_cycle(sgml_ctx* ctx, sgml_field* state_u, const sgml_field* sour
         require(n_r >= 1, SGML_EINVAL, "build_schedule: n_r must be >= 1");
         const sgml_grid& g = source->grid;
         activate(ctx);
+        CtxLock lk(ctx->mu);
         sgml_solver_opts o{};
         if (opts) o = *opts;
         sgml_solver_cfg cfg{n_r, 1, 1.0, safety};
@@ -534,6 +545,7 @@ int sgml_solver_create(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, double 
         if (sigma) require(sigma->grid.dim == dim && sigma->grid.n == n, SGML_EINVAL, "solve: sigma grid mismatch");
         sgml_solver_opts o{};
         if (opts) o = *opts;
+        CtxLock lk(ctx->mu);
         auto sv = std::make_unique<sgml_solver>();
         sv->build(ctx, dim, n, *bc, a, sigma ? sigma->d : nullptr, *cfg, o);
         *out = sv.release();
@@ -550,6 +562,7 @@ int sgml_solver_run(sgml_solver* s, const sgml_field* f, sgml_field* u_out, sgml
         require(f->grid.dim == s->g.dim && f->grid.n == s->g.n, SGML_EINVAL, "solve: source grid mismatch");
         if (u_out) require(u_out->grid.dim == s->g.dim && u_out->grid.n == s->g.n, SGML_EINVAL,
                            "solve: output grid mismatch");
+        CtxLock lk(s->ctx->mu);
         s->run(f->d, u_out ? u_out->d : nullptr, rep);
     });
 }
@@ -626,7 +639,7 @@ int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f
         check_solve_args(cfg);
         sgml_solver_opts o{};
         if (opts) o = *opts;
-        std::lock_guard<std::mutex> lock(ctx->mu);
+        std::lock_guard<std::recursive_mutex> lock(ctx->mu);
         sgml_solver* sv = cached_solver(ctx, dim, n, bc, sigma_host, a, cfg, o);
         const size_t bytes = g.total * sizeof(double);
         SGML_CUDA(cudaMemcpyAsync(sv->fin, f_host, bytes, cudaMemcpyHostToDevice, s));
@@ -648,7 +661,7 @@ int sgml_solve_many(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, int count,
         check_solve_args(cfg);
         sgml_solver_opts o{};
         if (opts) o = *opts;
-        std::lock_guard<std::mutex> lock(ctx->mu);
+        std::lock_guard<std::recursive_mutex> lock(ctx->mu);
         sgml_solver* sv = cached_solver(ctx, dim, n, bc, sigma_host, a, cfg, o);
         if (count == 0) return;
         const size_t bytes = g.total * sizeof(double);
@@ -795,6 +808,7 @@ int sgml_deformation_velocity(const sgml_field* u, const sgml_field* f_raw, doub
         }
         sgml_ctx* ctx = u->ctx;
         activate(ctx);
+        CtxLock lk(ctx->mu);
         const cudaStream_t s = ctx->stream;
         SGML_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), s));
         launch_gradient(g.dim, u->d, o, g.N, inv2h_of(g), f_raw->d, raw_integral, t, ctx->d_flags, s);

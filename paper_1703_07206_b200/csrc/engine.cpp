@@ -333,6 +333,7 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
     has_sigma = sigma_dev != nullptr;
     cfg = cfg_;
     opts = opts_;
+    if (std::getenv("SGML_NO_SMALL_LEVELS")) opts.small_levels = -1;  // (INTEGRATION.md switch)
     SGML_CUDA(cudaSetDevice(ctx->device));
 
     // schedule (cycle.cpp:28-45) flattened to relax passes
@@ -757,8 +758,7 @@ void sgml_solver::cycle_dense(const double* src_dense, double* out_dense, bool h
 // (set_faces would be a no-op for every output and du buffer).
 bool sgml_solver::small_visit(int v, const double* in, int c, const double* p0, const double* p1,
                               bool homogeneous) const {
-    static const bool off = std::getenv("SGML_NO_SMALL_LEVELS") != nullptr;
-    if (off || dist(v) || c > kSmallMaxPasses || !compact()) return false;
+    if (opts.small_levels < 0 || dist(v) || c > kSmallMaxPasses || !compact()) return false;
     long long nodes = 1;
     for (int ax = 0; ax < g.dim; ++ax) nodes *= (long long)(rng[v].hi[ax] - rng[v].lo[ax] + 1);
     if (nodes <= 0 || nodes > kSmallNodes) return false;
@@ -975,7 +975,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                 SGML_CUDA(cudaMemsetAsync(in, 0, ext_size(dim, Lv[v]) * sizeof(double), s));
                 fstate[in] = FS_ZERO;
             } else {
-                if (count + (c - 1) > kMaxChain) {
+                if (count > 0 && count + (c - 1) > kMaxChain) {
                     // fold the pending increments into a full-grid base
                     const ChainEntry* ch = chain_at();
                     mat_halo(other, 0, [&](int kb, int ke) {

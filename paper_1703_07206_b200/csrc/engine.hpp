@@ -33,7 +33,10 @@ struct sgml_ctx {
     // sgml_solve's engine cache (one problem shape), see capi.cpp
     struct sgml_solver* cached = nullptr;
     std::string cached_key;
-    std::mutex mu;
+    // serialises every entry point that uses the context's stream scratch
+    // (d_slots / d_flags / h_slots / h_flags / h_stage) or its solver cache;
+    // recursive: a guarded entry point may call another one
+    std::recursive_mutex mu;
     // multi-GPU clique this context belongs to (z-slab solves); null: single GPU
     std::unique_ptr<sgmlb::Transport> tp;
 };

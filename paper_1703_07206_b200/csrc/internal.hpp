@@ -52,8 +52,11 @@ struct ChainEntry {
     int level;
     int fslot;  // cycle slot of the reference pass that adds this increment
 };
-// Most increments one materialisation applies before the engine folds them
-// into a full-grid base (only reached for large n_r).
+// Most increments one materialisation keeps in shared memory; the engine
+// folds pending increments into a full-grid base before a chain outgrows it
+// (only reached for large n_r).  A single visit may still add more (n_r >
+// kMaxChain + 1): the kernel then reads the entries past kMaxChain from
+// global memory.
 constexpr int kMaxChain = 96;
 
 // TMA descriptors of one relaxation / residual launch (relax_tiled.cu):

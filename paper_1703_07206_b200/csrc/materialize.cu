@@ -46,9 +46,13 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
                    ExtLay L0, int wb, int base_zero, const double* __restrict__ ufine, ExtLay Lf, int frel,
                    const ChainEntry* __restrict__ chain, int nchain, BcDev bc, int homogeneous,
                    int* flag, int xtail, int k0) {
+    // the first kMaxChain entries sit in shared memory; a longer chain (a
+    // single visit adding more than kMaxChain increments, n_r > kMaxChain + 1)
+    // reads the rest from global memory
     __shared__ ChainEntry sch[kMaxChain];
     const int tid = threadIdx.x + MBX * threadIdx.y;
-    for (int c = tid; c < nchain; c += MBX * MBY) sch[c] = chain[c];
+    const int nsh = min(nchain, kMaxChain);
+    for (int c = tid; c < nsh; c += MBX * MBY) sch[c] = chain[c];
     __syncthreads();
 
     // NC copies along y at spacing D = (Nw - 1) / NC: rows s0 + c D
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
         }
 
         for (int c = 0; c < nch; ++c) {
-            const ChainEntry ce = sch[c];
+            const ChainEntry ce = c < kMaxChain ? sch[c] : chain[c];
             const int l = ce.level, Nl = ce.L.N;
             const int msk = (1 << l) - 1;
             const double inv = __longlong_as_double((long long)(1023 - l) << 52);  // 2^-l, exact

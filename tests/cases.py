@@ -134,6 +134,24 @@ def solve_problem(name: str, n: int):
     if name == "sigma3d_dirichlet":
         g = O.make_grid(3, n)
         return g, bc("dir_distinct"), O.fill("poisson3d", g), sigma_field(g, 77), 0.0
+    if name == "sigma2d_mixed_a":
+        # 2D: sigma + x faces Dirichlet (distinct values) / y faces Neumann + a
+        g = O.make_grid(2, n)
+        return g, bc("mixed_x"), O.fill("sinsin2d", g), sigma_field(g, 91), 0.2
+    if name == "sigma2d_neumann_a":
+        # 2D all-Neumann with sigma and a = 0.1 (cosine source)
+        g = O.make_grid(2, n)
+        x = np.arange(g.N) * g.h
+        yy, xx = np.meshgrid(x, x, indexing="ij")
+        f = (-2.0 * math.pi ** 2 * np.cos(math.pi * xx) * np.cos(math.pi * yy)).reshape(-1)
+        return g, bc("neumann"), f, sigma_field(g, 93), 0.1
+    if name == "mixed2d_a":
+        # 2D low faces Dirichlet / high faces Neumann (the F5 wrap reads), a = 0.15
+        g = O.make_grid(2, n)
+        return g, bc("low_dir_high_neu"), O.fill("sinsin2d", g), None, 0.15
+    if name == "sigma3d_mixed_a":
+        g = O.make_grid(3, n)
+        return g, bc("low_dir_high_neu"), O.fill("poisson3d", g), sigma_field(g, 95), 0.2
     if name == "zero_source_dirichlet1":
         g = O.make_grid(2, n)
         return g, bc("dir_quarter"), np.zeros(g.total), None, 0.0
@@ -144,6 +162,14 @@ SOLVE_CASES = [
     ("sinsin2d", 4), ("sinsin2d", 6), ("poisson2d", 5), ("poisson3d", 3), ("poisson3d", 4),
     ("capacitor_high", 3), ("capacitor_low", 4), ("neumann2d_a", 4), ("neumann2d", 5),
     ("mixed2d", 5), ("mixed3d_a", 3), ("sigma3d_dirichlet", 3), ("zero_source_dirichlet1", 3),
+]
+
+# Solves large enough that the level-0 (and coarser) arrays exceed the
+# one-CTA small-level path (2D > 65^2, 3D > 17^3), so the TMA relaxation
+# kernels run with sigma, a != 0, all-Neumann and mixed faces.
+SOLVE_CASES_LARGE = [
+    ("sigma2d_mixed_a", 7), ("sigma2d_neumann_a", 7), ("neumann2d_a", 8), ("mixed2d_a", 8),
+    ("sigma2d_mixed_a", 8), ("neumann3d_a", 5), ("sigma3d_mixed_a", 5), ("sigma3d_dirichlet", 5),
 ]
 
 

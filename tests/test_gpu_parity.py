@@ -30,6 +30,16 @@ def dev(g, arr):
     return S.Field.from_numpy(sgrid(g), arr)
 
 
+# engine variants: the compact engine with and without the one-CTA
+# small-level path (SolverOptions.small_levels), and the literal engine
+ENGINES = ["compact", "compact-nosmall", "literal"]
+
+
+def opts(engine):
+    return S.SolverOptions(engine="literal" if engine == "literal" else "compact",
+                           small_levels=engine != "compact-nosmall")
+
+
 @pytest.fixture(scope="module", autouse=True)
 def _device():
     assert S.device_count() >= 1, "no CUDA device: GPU tests must run on the B200 box"
@@ -139,7 +149,7 @@ def test_restrict_sigma_levels_and_positivity():
 
 # -------------------------------------------------------------- cycle ----
 
-@pytest.mark.parametrize("engine", ["compact", "literal"])
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("n_r", [1, 2, 3, 8])
 @pytest.mark.parametrize("dim,n,bcn", [(2, 5, "mixed_x"), (3, 3, "plates"), (2, 4, "neumann"),
                                        (3, 4, "dir_distinct"), (2, 1, "dir0"), (3, 2, "low_dir_high_neu")])
@@ -158,7 +168,7 @@ def test_single_cycle_bitwise(engine, n_r, dim, n, bcn, sig):
         work = S.Work(7)
         slv = S.restrict_sigma_levels(dev(g, sfull), g.n) if sig else []
         S.single_cycle(state, dev(g, src), slv, 0.2, sbc(bcn), hom, S.build_schedule(n, n_r), 0.9, 3,
-                       2.5, rep, work, S.SolverOptions(engine=engine))
+                       2.5, rep, work, opts(engine))
         assert work.value == 7 + w_ref
         assert K.bits_equal(state.u.numpy(), u_ref)
         assert [(t.cycle, t.pass_, t.level) for t in rep.trace] == [t[:3] for t in trace_ref]
@@ -171,8 +181,7 @@ def check_solve(name, n, engine="compact", n_r=2, tol=1e-10, max_cycles=40):
     g, b, f, s, a = K.solve_problem(name, n)
     ref = O.solve(g, b, f, s, a, n_r=n_r, tol=tol, max_cycles=max_cycles)
     prob = S.ProblemSpec(sgrid(g), f, bc=sbc_of(b), sigma=s, a=a)
-    res = S.solve(prob, S.SolverConfig(n_r=n_r, tol=tol, max_cycles=max_cycles, safety=0.9),
-                  S.SolverOptions(engine=engine))
+    res = S.solve(prob, S.SolverConfig(n_r=n_r, tol=tol, max_cycles=max_cycles, safety=0.9), opts(engine))
     rep = res.report
     assert (rep.converged, rep.nan_detected, rep.stagnated) == (ref.converged, ref.nan_detected,
                                                                 ref.stagnated)
@@ -190,7 +199,7 @@ def sbc_of(b):
 
 
 @pytest.mark.parametrize("name,n", K.SOLVE_CASES, ids=lambda x: str(x))
-@pytest.mark.parametrize("engine", ["compact", "literal"])
+@pytest.mark.parametrize("engine", ENGINES)
 def test_solve_bitwise(name, n, engine):
     check_solve(name, n, engine)
 

@@ -122,13 +122,9 @@ def test_live_reference_relax_full_case_list():
         g, b, up, dup, gs, s = K.relax_inputs(*case)
         mine = O.relax(g, b, up, dup, level, gs, s, a, 0.9, hom)
         ref = O.relax(g, b, up, dup, level, gs, s, a, 0.9, hom, impl="ref")
-        outer_high_neumann = K.BCS[bcn][0][2 * dim - 1] == K.NEU
-        if ref[0] == 3 and mine[0] == 0 and level >= 1 and outer_high_neumann:
-            # the reference's zero-weight corner read runs past the
-            # end of du_prev (undefined behaviour, garbage may be NaN); the
-            # restatement reads 0 there.  Everything else must still agree.
-            assert np.isfinite(mine[1]).all()
-            continue
+        # the reference's zero-weight corner reads past the end
+        # of du_prev see zeros (oracle/ref_shim.cpp pads its allocations), the
+        # value the restatement uses: every case must agree exactly
         assert mine[0] == ref[0] and mine[3] == ref[3], case
         assert K.bits_equal(mine[1], ref[1]) and K.bits_equal(mine[2], ref[2]), case
 
@@ -143,12 +139,6 @@ def test_live_reference_single_cycle(n_r):
         for levels in (None, sig):
             a = O.single_cycle(g, K.bc(bcn), src, levels, 0.2, False, n_r, 0.9, 0, 1.0)
             b = O.single_cycle(g, K.bc(bcn), src, levels, 0.2, False, n_r, 0.9, 0, 1.0, impl="ref")
-            if b[0] == 3 and a[0] == 0 and K.BCS[bcn][0][2 * dim - 1] == K.NEU:
-                # SURVEY.md F5 (see test_live_reference_relax): the reference read
-                # past the end of du_prev and met non-finite garbage; heap-layout
-                # dependent, so only the restatement's finiteness is checked
-                assert np.isfinite(a[1]).all()
-                continue
             assert a[0] == b[0] and a[3] == b[3]
             assert K.bits_equal(a[1], b[1])
             assert [t[3] for t in a[2]] == [t[3] for t in b[2]]
