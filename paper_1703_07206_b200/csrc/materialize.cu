@@ -287,10 +287,12 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
                     store_ext<DIM>(out, Lw, I, Jn, K, value);
                 }
                 // Dirichlet x-high face: the last group also writes node Nw - 1 (the
-                // grid stops at Nw - 2, so no block is spent on that column)
+                // grid stops at Nw - 2, so no block is spent on that column),
+                // with its y / z mirror ghosts (rows / planes 1 and Nw - 2 next to
+                // a Neumann face: the corner ghost the relaxation reads)
                 if (xtail && X4 + MV == Nw - 1)
-                    out[eix<DIM>(Lw, Nw - 1, Jn, K)] =
-                        homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, Nw - 1, Jn, Kn);
+                    store_ext<DIM>(out, Lw, Nw - 1, Jn, K,
+                                   homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, Nw - 1, Jn, Kn));
             }
         }
     }

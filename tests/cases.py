@@ -32,6 +32,9 @@ BCS = {
     "dir_distinct": ([D] * 6, [1.0, -2.0, 3.0, -4.0, 5.0, -6.0]),
     # high faces Neumann, low faces Dirichlet (exercises the F5 wrap reads)
     "low_dir_high_neu": ([D, NEU, D, NEU, D, NEU], [0.3, 0, -0.2, 0, 0.1, 0]),
+    # x faces Dirichlet (distinct values), every other face Neumann: the
+    # x-high face column next to Neumann rows / planes (corner mirror ghosts)
+    "xdir_yzneu": ([D, D, NEU, NEU, NEU, NEU], [0.5, -0.75, 0, 0, 0, 0]),
 }
 
 
@@ -167,6 +170,24 @@ SOLVE_CASES = [
 # Solves large enough that the level-0 (and coarser) arrays exceed the
 # one-CTA small-level path (2D > 65^2, 3D > 17^3), so the TMA relaxation
 # kernels run with sigma, a != 0, all-Neumann and mixed faces.
+# Every relaxation-kernel specialisation at sizes where the TMA kernels carry
+# the large levels (2D 129^2, 3D 33^3): (dim, n, bc, sigma, a)
+SPEC_CASES = [(dim, n, bcn, sig, a)
+              for dim, n in ((2, 7), (3, 5))
+              for bcn in ("dir_distinct", "neumann", "xdir_yzneu", "low_dir_high_neu")
+              for sig in (False, True) for a in (0.0, 0.25)]
+
+
+def spec_key(dim, n, bcn, sig, a) -> str:
+    return f"spec:{dim}:{n}:{bcn}:{int(sig)}:{a}"
+
+
+def spec_problem(dim, n, bcn, sig, a):
+    g = O.make_grid(dim, n)
+    f = O.fill("sinsin2d" if dim == 2 else "poisson3d", g)
+    return g, bc(bcn), f, (sigma_field(g, 57 + dim) if sig else None), a
+
+
 SOLVE_CASES_LARGE = [
     ("sigma2d_mixed_a", 7), ("sigma2d_neumann_a", 7), ("neumann2d_a", 8), ("mixed2d_a", 8),
     ("sigma2d_mixed_a", 8), ("neumann3d_a", 5), ("sigma3d_mixed_a", 5), ("sigma3d_dirichlet", 5),

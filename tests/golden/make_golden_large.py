@@ -62,6 +62,9 @@ def problem(case: str):
         return mixed_deformation(name[-1], n)
     if name.startswith("case:"):  # tests/cases.py solve problems
         return K.solve_problem(name[5:], n)
+    if name.startswith("spec:"):  # spec:dim:n:bc:sig:a (tests/cases.py SPEC_CASES)
+        _, dim, n2, bcn, sig, a = name.split(":")
+        return K.spec_problem(int(dim), int(n2), bcn, sig == "1", float(a))
     return O.ref_problem(name, n)
 
 
@@ -72,7 +75,8 @@ CASES = [
 ]
 # tests/golden/solves.json: the tests/cases.py solves that run the TMA
 # relaxation kernels with sigma / a / Neumann / mixed faces (SOLVE_CASES_LARGE)
-SOLVE_CASES = [f"case:{name}@{n}" for name, n in K.SOLVE_CASES_LARGE]
+SOLVE_CASES = [f"case:{name}@{n}" for name, n in K.SOLVE_CASES_LARGE] + \
+    [K.spec_key(*c) + f"@{c[1]}" for c in K.SPEC_CASES]
 
 
 def run(case: str) -> dict:

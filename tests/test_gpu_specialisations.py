@@ -7,7 +7,9 @@ path) carry sigma, a != 0, all-Neumann and mixed faces.
   without du output, the residual recurrence with u_tot) with the small-level
   path switched off (SolverOptions.small_levels = False), so every level
   runs through the TMA kernel, against the C restatement bit for bit.
-* SOLVE_CASES_LARGE: the device against golden results produced by the
+* SOLVE_CASES_LARGE and SPEC_CASES (every specialisation at 2D 129^2 /
+  3D 33^3, including x-high Dirichlet faces next to Neumann rows): the
+  device against golden results produced by the
   UNMODIFIED reference (tests/golden/solves.json, make_golden_large.py
   --solves): residual history (hex), flags, normalisation, node updates,
   trace digest, solution digest.  Small-level path on and off.
@@ -15,6 +17,7 @@ path) carry sigma, a != 0, all-Neumann and mixed faces.
   materialisation keeps in shared memory (kMaxChain), and the fold of a
   long chain into a full-grid base.
 """
+import functools
 import hashlib
 import json
 import os
@@ -46,13 +49,13 @@ def digest(a) -> str:
     return hashlib.sha256(K.canon(np.asarray(a, np.float64)).tobytes()).hexdigest()
 
 
-BCS = {2: ["dir_distinct", "neumann", "mixed_x"], 3: ["dir_distinct", "neumann", "low_dir_high_neu"]}
+BCS = {2: ["dir_distinct", "neumann", "mixed_x"], 3: ["dir_distinct", "neumann", "low_dir_high_neu", "xdir_yzneu"]}
 
 
 @pytest.mark.parametrize("stencil", ["radial", "compact"])
 @pytest.mark.parametrize("a", [0.0, 0.25])
 @pytest.mark.parametrize("sig", [False, True])
-@pytest.mark.parametrize("dim,bci", [(d, i) for d in (2, 3) for i in range(3)])
+@pytest.mark.parametrize("dim,bci", [(d, i) for d in (2, 3) for i in range(len(BCS[d]))])
 def test_every_tma_specialisation_bitwise(dim, bci, sig, a, stencil):
     n = 5 if dim == 2 else 4
     g = O.make_grid(dim, n)
@@ -71,18 +74,17 @@ def test_every_tma_specialisation_bitwise(dim, bci, sig, a, stencil):
     assert K.bits_equal(res.u, ref.u)
 
 
+@functools.lru_cache(maxsize=1)
 def golden_solves():
     if not os.path.exists(SOLVES_JSON):
         return {}
     return json.load(open(SOLVES_JSON))
 
 
-@pytest.mark.parametrize("small_levels", [True, False])
-@pytest.mark.parametrize("name,n", K.SOLVE_CASES_LARGE, ids=lambda x: str(x))
-def test_large_solves_match_reference_golden(name, n, small_levels):
-    gold = golden_solves().get(f"case:{name}@{n}")
-    assert gold is not None, "tests/golden/solves.json lacks this case (make_golden_large.py --solves)"
-    g, b, f, s, a = K.solve_problem(name, n)
+def check_against_golden(key, g, b, f, s, a, small_levels):
+    gold = golden_solves().get(key)
+    assert gold is not None, f"tests/golden/solves.json lacks {key} (make_golden_large.py --solves)"
+    n = g.n
     assert digest(f) == gold["f"]
     res = S.solve(S.ProblemSpec(S.make_grid(g.dim, n), f, bc=sbc_of(b), sigma=s, a=a),
                   S.SolverConfig(n_r=2, tol=1e-10, max_cycles=60, safety=0.9),
@@ -95,6 +97,20 @@ def test_large_solves_match_reference_golden(name, n, small_levels):
     assert len(rep.trace) == gold["trace_len"]
     assert digest([t.value for t in rep.trace]) == gold["trace"]
     assert digest(res.u) == gold["u"]
+
+
+@pytest.mark.parametrize("small_levels", [True, False])
+@pytest.mark.parametrize("name,n", K.SOLVE_CASES_LARGE, ids=lambda x: str(x))
+def test_large_solves_match_reference_golden(name, n, small_levels):
+    g, b, f, s, a = K.solve_problem(name, n)
+    check_against_golden(f"case:{name}@{n}", g, b, f, s, a, small_levels)
+
+
+@pytest.mark.parametrize("small_levels", [True, False])
+@pytest.mark.parametrize("case", K.SPEC_CASES, ids=lambda c: K.spec_key(*c))
+def test_specialisations_at_size_match_reference_golden(case, small_levels):
+    g, b, f, s, a = K.spec_problem(*case)
+    check_against_golden(K.spec_key(*case) + f"@{case[1]}", g, b, f, s, a, small_levels)
 
 
 @pytest.mark.parametrize("engine,small_levels", [("compact", True), ("compact", False), ("literal", True)])
