@@ -91,8 +91,7 @@ SolveResult solve(const ProblemSpec& problem, const SolverConfig& config);
 void pure_neumann_pin(Field& u);
 std::vector<Field> restrict_sigma_levels(const Field& sigma, int n);
 
-// Relative L1 error by trapezoid quadrature (reference problems.cpp:195-215),
-// used for the l1_error column.
-double l1_error(const Field& v_h, const ExactSolution& exact);
+// (l1_error, the l1_error column's quadrature, is declared in sgml/problems.hpp
+// as in the reference.)
 
 }  // namespace sgml

@@ -40,7 +40,8 @@ typedef enum {
     SGML_ENONFINITE = 3, /* kernel_error: non-finite value produced */
     SGML_ECUDA = 4,      /* std::runtime_error (CUDA) */
     SGML_ENCCL = 5,      /* std::runtime_error (NCCL) */
-    SGML_ELOGIC = 6      /* std::logic_error / std::out_of_range */
+    SGML_ELOGIC = 6,     /* std::logic_error / std::out_of_range */
+    SGML_EIO = 7         /* io_error: a file cannot be opened / written */
 } sgml_status;
 
 typedef struct sgml_ctx sgml_ctx;       /* one device + one stream + buffer pool */
@@ -305,6 +306,30 @@ int sgml_build_trifoil_sources(sgml_field* const* f3, double r);
  * it 3D): f_raw, the zero-mean source f and the raw trapezoid integral */
 int sgml_build_deformation_sources(const double* points, int npts, sgml_field* f, sgml_field* f_raw,
                                    double* raw_integral);
+
+/* problems.cpp:302-325 for any curve (closed flag; with_payload: the curve
+ * carries a payload, so resampling also forms unit tangents and rejects
+ * degenerate ones, as the reference does) */
+int sgml_build_deformation_problem(const double* points, int npts, int closed, int with_payload, sgml_field* f,
+                                   sgml_field* f_raw, double* raw_integral);
+
+/* ---- curves (problems.cpp:217-300) -------------------------------------------
+ * Host curve work (a few thousand samples) with the reference's arithmetic.
+ * Points / payloads are xyz triples.  resample_curve writes min(count, cap)
+ * samples and sets *count to the full count (call again with a larger cap
+ * when *count > cap); out_payload may be NULL unless with_payload. */
+int sgml_resample_curve(const double* points, int npts, int closed, int with_payload, double h, double* out_points,
+                        double* out_payload, int cap, int* count);
+/* deposit_delta: strength * arc element per sample, hat weights / h^dim,
+ * into the device field f (zeroed first) */
+int sgml_deposit_delta(const double* points, int npts, int closed, double strength, sgml_field* f);
+/* deposit_delta_vector: payload * arc element into the 3 component fields */
+int sgml_deposit_delta_vector(const double* points, const double* payload, int npts, int closed,
+                              sgml_field* const* f3);
+/* trifoil_problem's curve (problems.cpp:374-398): the 512-sample overhand
+ * knot of scale r, checked inside the unit cube, resampled at spacing h with
+ * unit tangents (same count / cap protocol as sgml_resample_curve) */
+int sgml_trifoil_curve(double r, double h, double* out_points, double* out_payload, int cap, int* count);
 
 /* ---- output (io.cpp:14-64) ------------------------------
  * The reference's legacy ASCII VTK files ("%.17g"), byte for byte, streamed

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libsgml_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "sgml_b200.h")
 
-OK, EINVAL, EBADSTEP, ENONFINITE, ECUDA, ENCCL, ELOGIC = range(7)
+OK, EINVAL, EBADSTEP, ENONFINITE, ECUDA, ENCCL, ELOGIC, EIO = range(8)
 
 
 class Grid(C.Structure):
@@ -182,6 +182,8 @@ def check(status: int) -> None:
         raise kernel_error(msg)
     if status == ELOGIC:
         raise LookupError(msg)
+    if status == EIO:
+        raise OSError(msg)
     raise SgmlError(msg)
 
 

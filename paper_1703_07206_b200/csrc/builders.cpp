@@ -182,6 +182,68 @@ void upload_sparse(sgml_field* f, const Sparse& sp, double z, bool negate) {
     finish(ctx);
 }
 
+Curve curve_of(const double* pts, const double* payload, int npts, bool closed) {
+    Curve c;
+    c.closed = closed;
+    for (int q = 0; q < npts; ++q) {
+        c.points.push_back({pts[3 * q], pts[3 * q + 1], pts[3 * q + 2]});
+        if (payload) c.payload.push_back({payload[3 * q], payload[3 * q + 1], payload[3 * q + 2]});
+    }
+    return c;
+}
+
+void emit_curve(const Curve& c, double* pts, double* payload, int cap, int* count) {
+    const std::size_t m = c.points.size();
+    need(m <= 0x7fffffff, "resample_curve: too many samples");
+    *count = (int)m;
+    for (std::size_t i = 0; i < m && (long long)i < cap; ++i)
+        for (int k = 0; k < 3; ++k) {
+            if (pts) pts[3 * i + k] = c.points[i][k];
+            if (payload && !c.payload.empty()) payload[3 * i + k] = c.payload[i][k];
+        }
+}
+
+// problems.cpp:282-291: strength * ds per sample, summed per node in sample order
+Sparse deposit_scalar(const Curve& curve, const sgml_grid& g, double strength) {
+    need(curve.points.size() >= 2, "deposit_delta: need at least 2 points");
+    const std::vector<double> ds = arc_elements(curve);
+    Sparse out;
+    for (std::size_t i = 0; i < curve.points.size(); ++i) {
+        const double mass = strength * ds[i];
+        scatter_mass(curve.points[i], g, [&](unsigned long long p, double w) { out[p] += mass * w; });
+    }
+    return out;
+}
+
+// problems.cpp:293-302: payload_c * ds * w into the three components
+void deposit_vector(const Curve& curve, const sgml_grid& g, Sparse* w3) {
+    need(curve.payload.size() == curve.points.size(), "deposit_delta_vector: curve carries no payload");
+    const std::vector<double> ds = arc_elements(curve);
+    for (std::size_t i = 0; i < curve.points.size(); ++i) {
+        const Point& pay = curve.payload[i];
+        scatter_mass(curve.points[i], g, [&](unsigned long long p, double w) {
+            for (int comp = 0; comp < 3; ++comp) w3[comp][p] += pay[comp] * ds[i] * w;
+        });
+    }
+}
+
+// problems.cpp:374-398: the overhand knot, 512 samples, resampled at h with unit tangents
+Curve trifoil_curve(double r, double h) {
+    need(r > 0.0, "trifoil_problem: r must be positive");
+    Curve raw;
+    raw.closed = true;
+    const int samples = 512;
+    raw.payload.resize(samples);
+    for (int s = 0; s < samples; ++s) {
+        const double t = 2.0 * kPi * s / samples;
+        raw.points.push_back({0.5 + r * (std::sin(t) + 2.0 * std::sin(2.0 * t)),
+                              0.5 + r * (std::cos(t) - 2.0 * std::cos(2.0 * t)), 0.5 - r * std::sin(3.0 * t)});
+    }
+    for (const Point& p : raw.points)
+        need(inside_unit(p, 3), "trifoil_problem: curve leaves the unit domain (max extent 3r)");
+    return resample_curve(raw, h);
+}
+
 }  // namespace
 
 extern "C" {
@@ -248,64 +310,86 @@ int sgml_build_trifoil_sources(sgml_field* const* f3, double r) {
         need(g.dim == 3, "trifoil_problem: 3D fields are required");
         for (int c = 1; c < 3; ++c)
             need(f3[c]->grid.dim == 3 && f3[c]->grid.n == g.n, "trifoil_problem: grid mismatch");
-        need(r > 0.0, "trifoil_problem: r must be positive");
         SGML_CUDA(cudaSetDevice(f3[0]->ctx->device));
-        Curve raw;
-        raw.closed = true;
-        const int samples = 512;
-        raw.payload.resize(samples);
-        for (int s = 0; s < samples; ++s) {
-            const double t = 2.0 * kPi * s / samples;
-            raw.points.push_back({0.5 + r * (std::sin(t) + 2.0 * std::sin(2.0 * t)),
-                                  0.5 + r * (std::cos(t) - 2.0 * std::cos(2.0 * t)), 0.5 - r * std::sin(3.0 * t)});
-        }
-        for (const Point& p : raw.points)
-            need(inside_unit(p, 3), "trifoil_problem: curve leaves the unit domain (max extent 3r)");
-        const Curve curve = resample_curve(raw, g.h);
-        const std::vector<double> ds = arc_elements(curve);
+        const Curve curve = trifoil_curve(r, g.h);
         Sparse omega[3];
-        for (std::size_t i = 0; i < curve.points.size(); ++i) {
-            const Point& pay = curve.payload[i];
-            scatter_mass(curve.points[i], g, [&](unsigned long long p, double w) {
-                for (int comp = 0; comp < 3; ++comp) omega[comp][p] += pay[comp] * ds[i] * w;
-            });
-        }
+        deposit_vector(curve, g, omega);
         // psi_c's source is -omega_c over the whole field (-0.0 away from the curve)
         for (int comp = 0; comp < 3; ++comp) upload_sparse(f3[comp], omega[comp], -0.0, true);
         finish(f3[0]->ctx);
     });
 }
 
-int sgml_build_deformation_sources(const double* points, int npts, sgml_field* f, sgml_field* f_raw,
-                                   double* raw_integral) {
+int sgml_build_deformation_problem(const double* points, int npts, int closed, int with_payload, sgml_field* f,
+                                   sgml_field* f_raw, double* raw_integral) {
     return guarded([&] {
-        need(points && npts >= 2 && f && f_raw && raw_integral, "deformation_problem: bad arguments");
-        Curve curve;
-        curve.closed = true;
+        need(points && npts >= 0 && f && f_raw && raw_integral, "deformation_problem: bad arguments");
+        Curve curve = curve_of(points, nullptr, npts, closed);
+        if (with_payload) curve.payload.assign(curve.points.size(), Point{0.0, 0.0, 0.0});
         int dim = 2;
-        for (int q = 0; q < npts; ++q) {
-            curve.points.push_back({points[3 * q], points[3 * q + 1], points[3 * q + 2]});
-            if (points[3 * q + 2] != 0.0) dim = 3;
-        }
+        for (const Point& p : curve.points)
+            if (p[2] != 0.0) dim = 3;
         const sgml_grid g = f->grid;
         need(g.dim == dim && f_raw->grid.dim == dim && f_raw->grid.n == g.n,
              "deformation_problem: field grids must match the curve's dimension");
         sgml_ctx* ctx = f->ctx;
         SGML_CUDA(cudaSetDevice(ctx->device));
         const Curve rs = resample_curve(curve, g.h);
-        const std::vector<double> ds = arc_elements(rs);
-        Sparse raw;
-        for (std::size_t i = 0; i < rs.points.size(); ++i) {
-            const double mass = 1.0 * ds[i];  // strength 1 (problems.cpp:309)
-            scatter_mass(rs.points[i], g, [&](unsigned long long p, double w) { raw[p] += mass * w; });
-        }
-        upload_sparse(f_raw, raw, 0.0, false);
+        upload_sparse(f_raw, deposit_scalar(rs, g, 1.0), 0.0, false);  // strength 1 (problems.cpp:309)
         // raw_integral = trapezoid_mean(f_raw); f = f_raw projected to zero mean
         *raw_integral = trapezoid_mean_host(ctx, g, f_raw->d);
         SGML_CUDA(cudaMemcpyAsync(f->d, f_raw->d, g.total * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
         const double mean = trapezoid_mean_host(ctx, g, f->d);
         launch_sub_scalar(f->d, g.total, mean, ctx->stream);
         finish(ctx);
+    });
+}
+
+int sgml_build_deformation_sources(const double* points, int npts, sgml_field* f, sgml_field* f_raw,
+                                   double* raw_integral) {
+    return sgml_build_deformation_problem(points, npts, 1, 0, f, f_raw, raw_integral);
+}
+
+int sgml_resample_curve(const double* points, int npts, int closed, int with_payload, double h, double* out_points,
+                        double* out_payload, int cap, int* count) {
+    return guarded([&] {
+        need(points && npts >= 0 && count && cap >= 0, "resample_curve: bad arguments");
+        Curve c = curve_of(points, nullptr, npts, closed);
+        if (with_payload) c.payload.assign(c.points.size(), Point{0.0, 0.0, 0.0});
+        emit_curve(resample_curve(c, h), out_points, with_payload ? out_payload : nullptr, cap, count);
+    });
+}
+
+int sgml_deposit_delta(const double* points, int npts, int closed, double strength, sgml_field* f) {
+    return guarded([&] {
+        need(points && f, "deposit_delta: bad arguments");
+        need(npts >= 2, "deposit_delta: need at least 2 points");
+        SGML_CUDA(cudaSetDevice(f->ctx->device));
+        upload_sparse(f, deposit_scalar(curve_of(points, nullptr, npts, closed), f->grid, strength), 0.0, false);
+        finish(f->ctx);
+    });
+}
+
+int sgml_deposit_delta_vector(const double* points, const double* payload, int npts, int closed,
+                              sgml_field* const* f3) {
+    return guarded([&] {
+        need(points && f3 && f3[0] && f3[1] && f3[2], "deposit_delta_vector: bad arguments");
+        need(payload != nullptr, "deposit_delta_vector: curve carries no payload");
+        const sgml_grid g = f3[0]->grid;
+        for (int c = 1; c < 3; ++c)
+            need(f3[c]->grid.dim == g.dim && f3[c]->grid.n == g.n, "deposit_delta_vector: grid mismatch");
+        SGML_CUDA(cudaSetDevice(f3[0]->ctx->device));
+        Sparse w[3];
+        deposit_vector(curve_of(points, payload, npts, closed), g, w);
+        for (int comp = 0; comp < 3; ++comp) upload_sparse(f3[comp], w[comp], 0.0, false);
+        finish(f3[0]->ctx);
+    });
+}
+
+int sgml_trifoil_curve(double r, double h, double* out_points, double* out_payload, int cap, int* count) {
+    return guarded([&] {
+        need(count && cap >= 0, "trifoil_problem: bad arguments");
+        emit_curve(trifoil_curve(r, h), out_points, out_payload, cap, count);
     });
 }
 

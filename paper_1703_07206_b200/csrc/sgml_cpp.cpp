@@ -20,55 +20,14 @@
 #include "../../include/sgml/kernels.hpp"
 #include "../../include/sgml/problems.hpp"
 #include "../../include/sgml_b200.h"
+#include "sgml_cpp_internal.hpp"
 
 namespace sgml {
 
-namespace {
-
-void check(int status) {
-    if (status == SGML_OK) return;
-    const std::string msg = sgml_last_error();
-    switch (status) {
-        case SGML_EINVAL: throw std::invalid_argument(msg);
-        case SGML_EBADSTEP:
-        case SGML_ENONFINITE: throw kernel_error(msg);
-        case SGML_ELOGIC: throw std::logic_error(msg);
-        default: throw std::runtime_error(msg);
-    }
-}
-
-// One context per process on SGML_DEVICE (default 0), created on first use.
-sgml_ctx* context() {
-    static std::once_flag once;
-    static sgml_ctx* ctx = nullptr;
-    std::call_once(once, [] {
-        const char* d = std::getenv("SGML_DEVICE");
-        check(sgml_ctx_create(d ? std::atoi(d) : 0, &ctx));
-    });
-    return ctx;
-}
-
-sgml_bc to_c(const BoundarySpec& bc) {
-    sgml_bc b{};
-    for (int f = 0; f < 6; ++f) {
-        b.kind[f] = bc.faces[f].kind == BcKind::neumann ? 1 : 0;
-        b.value[f] = bc.faces[f].value;
-    }
-    return b;
-}
-
-// device copy of a host field for the duration of one call
-struct Dev {
-    sgml_field* f = nullptr;
-    explicit Dev(const Grid& g) { check(sgml_field_create(context(), g.dim, g.n, &f)); }
-    Dev(const Field& h) : Dev(h.grid()) { check(sgml_field_upload(f, h.data())); }
-    ~Dev() { sgml_field_destroy(f); }
-    Dev(const Dev&) = delete;
-    Dev& operator=(const Dev&) = delete;
-    void to(Field& h) const { check(sgml_field_download(f, h.data())); }
-};
-
-}  // namespace
+using cabi::check;
+using cabi::context;
+using cabi::Dev;
+using cabi::to_c;
 
 // ---- grid.hpp --------------------------------------------------------------
 

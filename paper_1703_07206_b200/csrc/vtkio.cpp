@@ -47,18 +47,18 @@ struct File {
     std::string path;
     explicit File(const std::string& p) : path(p) {
         f = std::fopen(p.c_str(), "wb");
-        if (!f) fail(SGML_EINVAL, "cannot open for writing: " + p);
+        if (!f) fail(SGML_EIO, "cannot open for writing: " + p);
     }
     ~File() {
         if (f) std::fclose(f);
     }
     void put(const char* s, size_t n) {
-        if (n && std::fwrite(s, 1, n, f) != n) fail(SGML_ECUDA, "write failed: " + path);
+        if (n && std::fwrite(s, 1, n, f) != n) fail(SGML_EIO, "write failed: " + path);
     }
     void close() {
         if (std::fclose(f) != 0) {
             f = nullptr;
-            fail(SGML_ECUDA, "write failed: " + path);
+            fail(SGML_EIO, "write failed: " + path);
         }
         f = nullptr;
     }
