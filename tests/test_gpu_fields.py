@@ -187,8 +187,8 @@ def test_new_entry_points_fail_like_the_reference():
         S.trifoil_sources(g3, 0.2)                   # problems.cpp:386-389: leaves the unit domain
     with pytest.raises(ValueError):
         S.deformation_sources([[0.5, 0.5, 0.0], [0.5, 0.5, 0.0]], g2)   # zero-length curve
-    with pytest.raises(ValueError):
-        S.write_field_vtk(S.Field(g3), "/nonexistent_dir/u.vtk", "u")  # io.cpp:17: cannot open
+    with pytest.raises(OSError):
+        S.write_field_vtk(S.Field(g3), "/nonexistent_dir/u.vtk", "u")  # io.cpp:17: io_error, cannot open
     f = S.Field(g3)
     bad = np.zeros(g3.total)
     bad[5] = np.nan
