@@ -183,6 +183,7 @@ int sgml_ctx_destroy(sgml_ctx* ctx) {
         cudaFreeHost(ctx->h_flags);
         if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
         for (cudaEvent_t e : ctx->h_stage_events) cudaEventDestroy(e);
+        destroy_stager(ctx->stager);
         delete ctx->cached;
         cudaStreamDestroy(ctx->stream);
         delete ctx;
@@ -269,8 +270,8 @@ int sgml_field_upload(sgml_field* f, const double* host) {
     return guarded([&] {
         require(f && host, SGML_EINVAL, "field_upload: null argument");
         activate(f->ctx);
-        SGML_CUDA(cudaMemcpyAsync(f->d, host, f->grid.total * sizeof(double), cudaMemcpyHostToDevice,
-                                  f->ctx->stream));
+        CtxLock lk(f->ctx->mu);
+        copy_h2d(f->ctx, f->d, host, f->grid.total * sizeof(double));
         SGML_CUDA(cudaStreamSynchronize(f->ctx->stream));
     });
 }
@@ -279,9 +280,8 @@ int sgml_field_download(const sgml_field* f, double* host) {
     return guarded([&] {
         require(f && host, SGML_EINVAL, "field_download: null argument");
         activate(f->ctx);
-        SGML_CUDA(cudaMemcpyAsync(host, f->d, f->grid.total * sizeof(double), cudaMemcpyDeviceToHost,
-                                  f->ctx->stream));
-        SGML_CUDA(cudaStreamSynchronize(f->ctx->stream));
+        CtxLock lk(f->ctx->mu);
+        copy_d2h(f->ctx, host, f->d, f->grid.total * sizeof(double));
     });
 }
 
@@ -603,7 +603,7 @@ sgml_solver* cached_solver(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, con
         } sg;
         if (sigma_host) {
             sg.p = sig = dalloc(g.total);
-            SGML_CUDA(cudaMemcpyAsync(sig, sigma_host, bytes, cudaMemcpyHostToDevice, s));
+            copy_h2d(ctx, sig, sigma_host, bytes);
         }
         auto sv = std::make_unique<sgml_solver>();
         sv->build(ctx, dim, n, *bc, a, sig, *cfg, o);
@@ -612,7 +612,7 @@ sgml_solver* cached_solver(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, con
         ctx->cached_key = key;
     } else if (sigma_host) {
         sgml_solver* sv = ctx->cached;
-        SGML_CUDA(cudaMemcpyAsync(sv->sigma_stage(), sigma_host, bytes, cudaMemcpyHostToDevice, s));
+        copy_h2d(ctx, sv->sigma_stage(), sigma_host, bytes);
         sv->load_sigma(sv->sigma_stage());
     }
     return ctx->cached;
@@ -642,10 +642,9 @@ int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f
         std::lock_guard<std::recursive_mutex> lock(ctx->mu);
         sgml_solver* sv = cached_solver(ctx, dim, n, bc, sigma_host, a, cfg, o);
         const size_t bytes = g.total * sizeof(double);
-        SGML_CUDA(cudaMemcpyAsync(sv->fin, f_host, bytes, cudaMemcpyHostToDevice, s));
+        copy_h2d(ctx, sv->fin, f_host, bytes);  // (pageable sources at pinned speed)
         sv->run(sv->fin, nullptr, rep);
-        if (u_host_out)
-            SGML_CUDA(cudaMemcpyAsync(u_host_out, sv->result(), bytes, cudaMemcpyDeviceToHost, s));
+        if (u_host_out) copy_d2h(ctx, u_host_out, sv->result(), bytes);
         SGML_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -426,6 +426,24 @@ __device__ __forceinline__ void mbar_wait_u32(unsigned bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+// Ampere-style asynchronous 8-byte copy global -> shared (LDGSTS), grouped
+// with commit / wait_group
+__device__ __forceinline__ void cp_async8(unsigned dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+// 1D bulk copy global -> shared (16-byte aligned ends, bytes a multiple of 16),
+// completion counted on the mbarrier's transaction bytes
+__device__ __forceinline__ void bulk_load_u32(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_3d_u32(unsigned dst, const void* map, int c0, int c1, int c2,
                                                 unsigned bar) {
     asm volatile(

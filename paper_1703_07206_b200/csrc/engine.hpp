@@ -19,6 +19,10 @@
 #include "internal.hpp"
 #include "transport.hpp"
 
+namespace sgmlb {
+struct HostStager;
+}
+
 // ---- opaque C-ABI objects ----------------------------------------------
 struct sgml_ctx {
     int device = 0;
@@ -39,6 +43,8 @@ struct sgml_ctx {
     std::recursive_mutex mu;
     // multi-GPU clique this context belongs to (z-slab solves); null: single GPU
     std::unique_ptr<sgmlb::Transport> tp;
+    // pinned ring + memcpy workers for pageable host transfers (hoststage.cpp)
+    sgmlb::HostStager* stager = nullptr;
 };
 
 struct sgml_field {
@@ -86,6 +92,13 @@ RelaxConst relax_const(int dim, int level, double h, double a, double safety, bo
                        int compact = 0);
 double* dalloc(size_t count);
 void dfree(double* p);
+
+// host <-> device copies at pinned speed for pageable host buffers
+// (hoststage.cpp); call with the context lock held.  copy_h2d returns once
+// the source is consumed, copy_d2h once the destination holds the data.
+void copy_h2d(sgml_ctx* ctx, void* dst, const void* src, size_t bytes);
+void copy_d2h(sgml_ctx* ctx, void* dst, const void* src, size_t bytes);
+void destroy_stager(HostStager* st);
 
 // serial Kahan trapezoid mean over a host copy (kernels.cpp:367-386)
 double trapezoid_mean_host(sgml_ctx* ctx, const sgml_grid& g, const double* dfield);

@@ -66,7 +66,8 @@ def launch_list(n, out, problem, count=None):
 
 
 def base(name):
-    return name.split("<")[0].split("(")[0].strip().split(" ")[-1]
+    """k_relax_tma from 'void unnamed>::k_relax_tma<3, 0, ...>(...)'."""
+    return name.split("<")[0].split("(")[0].strip().split(" ")[-1].split("::")[-1]
 
 
 def pick(launches, name_part, nth=0, largest=True):
@@ -90,6 +91,8 @@ def pick(launches, name_part, nth=0, largest=True):
 def summarize(rep, target, label, out):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(raw.splitlines()))
+    if len(r) < 3:
+        raise SystemExit(f"{label}: no kernel captured in {rep}")
     h, u, v = r[0], r[1], r[2]
     name = v[h.index("Kernel Name")]
     grid = v[h.index("launch__grid_size")].replace(",", "") if "launch__grid_size" in h else "?"
@@ -122,20 +125,27 @@ def main():
     ap.add_argument("--n", type=int, default=9)
     ap.add_argument("--out", default="gpurun_out/r02")
     ap.add_argument("--only", default="")
+    ap.add_argument("--reps", default="/tmp/ncu_reps", help="where the .ncu-rep files go (large)")
     args = ap.parse_args()
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+    os.makedirs(args.reps, exist_ok=True)
     launches, _ = launch_list(args.n, args.out, "poisson")
-    sig_launches, _ = launch_list(args.n, args.out, "capacitor", count=1500)  # (cycle 0 is enough)
+    sig_launches = []
+    if not args.only or "sigma" in args.only:
+        sig_launches, _ = launch_list(args.n, args.out, "capacitor", count=1500)  # (cycle 0 is enough)
     T = [  # label, name part, nth, largest, launch list
-        ("relax0", "k_relax_tma<3, false, false, 0, false, false>", 0, True, launches, "poisson"),
-        ("relax1", "k_relax_tma<3, false, false, 0, true, false>", 0, True, launches, "poisson"),
-        ("residual", "k_relax_tma<3, false, false, 1, true, false>", 0, True, launches, "poisson"),
-        ("mat0_c8", "k_materialize4<3, 2, false>", 0, True, launches, "poisson"),
-        ("mat0_c4", "k_materialize4<3, 2, false>", 4, True, launches, "poisson"),
-        ("mat0_c1", "k_materialize4<3, 2, false>", 7, True, launches, "poisson"),
+        ("relax0", "k_relax_tma<3, 0, 0, 0, 0, 0>", 0, True, launches, "poisson"),
+        ("relax1", "k_relax_tma<3, 0, 0, 0, 1, 0>", 0, True, launches, "poisson"),
+        ("residual", "k_relax_tma<3, 0, 0, 1, 1, 0>", 0, True, launches, "poisson"),
+        ("mat0_c8", "k_materialize4<3, 2, 0>", 0, True, launches, "poisson"),
+        ("mat0_c4", "k_materialize4<3, 2, 0>", 4, True, launches, "poisson"),
+        ("mat0_c1", "k_materialize4<3, 2, 0>", 7, True, launches, "poisson"),
+        ("matl0_c8", "k_materialize_l0<3>", 0, True, launches, "poisson"),
+        ("matl0_c4", "k_materialize_l0<3>", 4, True, launches, "poisson"),
+        ("matl0_c1", "k_materialize_l0<3>", 7, True, launches, "poisson"),
         ("pyramid01", "k_pyramid_ext<3>", 0, True, launches, "poisson"),
-        ("small", "k_relax_small<3, false, false>", 0, True, launches, "poisson"),
-        ("sigma_relax0", "k_relax_tma<3, true, false, 0, false, false>", 0, True, sig_launches, "capacitor"),
+        ("small", "k_relax_small<3, 0, 0>", 0, True, launches, "poisson"),
+        ("sigma_relax0", "k_relax_tma<3, 1, 0, 0, 0, 0>", 0, True, sig_launches, "capacitor"),
     ]
     for label, part, nth, largest, L, problem in T:
         if args.only and label not in args.only.split(","):
@@ -144,8 +154,8 @@ def main():
         if target is None:
             print(f"{label}: no launch matches {part!r}", flush=True)
             continue
-        rep = f"{args.out}_{label}"
-        run(["ncu", "--set", "full", "--import-source", "on", "--clock-control", "none", "-k", base(target["name"]),
+        rep = os.path.join(args.reps, f"{os.path.basename(args.out)}_{label}")
+        run(["ncu", "--set", "full", "--import-source", "on", "--clock-control", "none", "-k", "regex:" + base(target["name"]),
              "--launch-skip", str(ordinal), "--launch-count", "1", "-f", "-o", rep,
              sys.executable, PROF, str(args.n), "1", "compact", problem], stdout=subprocess.DEVNULL)
         summarize(rep + ".ncu-rep", target, label, args.out)
