@@ -377,6 +377,23 @@ __device__ __forceinline__ void store_ext(double* a, const ExtLay& L, int i, int
     if (j == 1 || j == N - 2 || (DIM == 3 && (kg == 1 || kg == N - 2))) store_mirrors<DIM>(a, L, i, j, k, v);
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// The engine launches its cycle kernels with programmatic stream
+// serialization (internal.hpp launch_pdl): a kernel may then begin while its
+// predecessor in the stream is still running and must wait for it (grid
+// completion + memory flush) before touching any data.  Grids of at most
+// kPdlEarly CTAs also let THEIR successor begin at once (its CTAs park in
+// pdl_wait), so chains of small launches -- the coarse levels -- overlap
+// their launch latency; large grids trigger implicitly at completion so
+// parked successors never take SM slots from their waves.  Both are no-ops
+// for a plain launch.
+constexpr unsigned kPdlEarly = 296;
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (gridDim.x * gridDim.y * gridDim.z <= kPdlEarly) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
 // ---- mbarrier / TMA (sm_90+; used on sm_100a) ------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);

@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
     // single visit adding more than kMaxChain increments, n_r > kMaxChain + 1)
     // reads the rest from global memory
     __shared__ ChainEntry sch[kMaxChain];
+    pdl_begin();
     const int tid = threadIdx.x + MBX * threadIdx.y;
     const int nsh = min(nchain, kMaxChain);
     for (int c = tid; c < nsh; c += MBX * MBY) sch[c] = chain[c];
@@ -314,6 +315,7 @@ __device__ __forceinline__ double axw2(int o) { return o == 0 ? 0.5 : 0.25; }
 template <int DIM>
 __global__ void __launch_bounds__(128) k_pyramid_ext(const double* __restrict__ in, ExtLay Lin,
                                                      double* __restrict__ out, ExtLay Lout, int kb) {
+    pdl_begin();
     const int Nout = Lout.N;
     // output plane: local kb + blockIdx.z, global + Lout.z0; input plane 2 * global
     const int I = blockIdx.x * 32 + threadIdx.x, J = blockIdx.y * 4 + threadIdx.y;
@@ -361,6 +363,7 @@ __global__ void __launch_bounds__(128) k_gather_ext(const double* __restrict__ e
 // arrays: the x / y faces of the own planes, the z faces where they are own.
 template <int DIM>
 __global__ void __launch_bounds__(128) k_dirichlet_faces(double* a, ExtLay L, BcDev bc, int zero, int mirrors) {
+    pdl_begin();
     const int N = L.N;
     const int p = blockIdx.x * 32 + threadIdx.x, q = blockIdx.y * 4 + threadIdx.y, f = blockIdx.z;
     if (p >= N || (DIM == 2 && q > 0) || bc.neu[f]) return;
@@ -388,6 +391,7 @@ __global__ void __launch_bounds__(128) k_dirichlet_faces(double* a, ExtLay L, Bc
 // gridDim.z)) <- in at the level-0-relative positions << shift
 __global__ void __launch_bounds__(128) k_sample_ext(const double* __restrict__ in, ExtLay Lin,
                                                     double* __restrict__ out, ExtLay Lout, int shift, int kb) {
+    pdl_begin();
     const int I = blockIdx.x * 32 + threadIdx.x, J = blockIdx.y * 4 + threadIdx.y;
     const int K = kb + (int)blockIdx.z;
     if (I >= Lout.N || J >= Lout.N) return;
@@ -464,10 +468,9 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
     const int xtail = (!bc.neu[1] && (Nw - 1) % MV == 0) ? 1 : 0;
     const int threads_x = xtail ? (Nw - 1) / MV : (Nw + MV - 1) / MV, D = (Nw - 1) / NC;
     const dim3 grid((threads_x + MBX - 1) / MBX, (D + MBY) / MBY, dim == 3 ? ke - kb : 1);
-#define SGML_MAT(DD, CC, GG)                                                                     \
-    k_materialize4<DD, CC, GG><<<grid, dim3(MBX, MBY), 0, s>>>(out, Lw, w, base, L0, wb, base_zero, ufine, \
-                                                               Lf, frel, chain, nchain, bc, homogeneous, flag, xtail, \
-                                                               dim == 3 ? kb : 0)
+#define SGML_MAT(DD, CC, GG)                                                                              \
+    launch_pdl(k_materialize4<DD, CC, GG>, grid, dim3(MBX, MBY), 0, s, out, Lw, w, base, L0, wb, base_zero, ufine, \
+               Lf, frel, chain, nchain, bc, homogeneous, flag, xtail, dim == 3 ? kb : 0)
     if (dim == 2) {
         if (diag) SGML_MAT(2, NC, true);
         else SGML_MAT(2, NC, false);
@@ -481,14 +484,14 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
 void launch_pyramid_ext(int dim, const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout,
                         cudaStream_t s, int kb, int ke) {
     if (dim == 2) {
-        k_pyramid_ext<2><<<ext_grid(2, Lout), dim3(32, 4), 0, s>>>(in, Lin, out, Lout, 0);
+        launch_pdl(k_pyramid_ext<2>, ext_grid(2, Lout), dim3(32, 4), 0, s, in, Lin, out, Lout, 0);
         return;
     }
     if (ke < 0) ke = Lout.Nz;
     if (ke <= kb) return;
     dim3 g = ext_grid(3, Lout);
     g.z = ke - kb;
-    k_pyramid_ext<3><<<g, dim3(32, 4), 0, s>>>(in, Lin, out, Lout, kb);
+    launch_pdl(k_pyramid_ext<3>, g, dim3(32, 4), 0, s, in, Lin, out, Lout, kb);
 }
 
 void launch_scatter_ext(int dim, const double* dense, double* ext, const ExtLay& L, cudaStream_t s) {
@@ -505,9 +508,11 @@ void launch_dirichlet_faces(int dim, double* a, const ExtLay& L, const BcDev& bc
                             bool mirrors, cudaStream_t s) {
     const int N = L.N;
     if (dim == 2)
-        k_dirichlet_faces<2><<<dim3((N + 31) / 32, 1, 4), dim3(32, 4), 0, s>>>(a, L, bc, zero ? 1 : 0, mirrors ? 1 : 0);
+        launch_pdl(k_dirichlet_faces<2>, dim3((N + 31) / 32, 1, 4), dim3(32, 4), 0, s, a, L, bc, zero ? 1 : 0,
+                   mirrors ? 1 : 0);
     else
-        k_dirichlet_faces<3><<<dim3((N + 31) / 32, (N + 3) / 4, 6), dim3(32, 4), 0, s>>>(a, L, bc, zero ? 1 : 0, mirrors ? 1 : 0);
+        launch_pdl(k_dirichlet_faces<3>, dim3((N + 31) / 32, (N + 3) / 4, 6), dim3(32, 4), 0, s, a, L, bc, zero ? 1 : 0,
+                   mirrors ? 1 : 0);
 }
 
 void launch_sample_ext(const double* in, const ExtLay& Lin, double* out, const ExtLay& Lout, int shift, int kb,
@@ -515,7 +520,7 @@ void launch_sample_ext(const double* in, const ExtLay& Lin, double* out, const E
     if (ke <= kb) return;
     dim3 g = ext_grid(3, Lout);
     g.z = ke - kb;
-    k_sample_ext<<<g, dim3(32, 4), 0, s>>>(in, Lin, out, Lout, shift, kb);
+    launch_pdl(k_sample_ext, g, dim3(32, 4), 0, s, in, Lin, out, Lout, shift, kb);
 }
 
 void launch_dtau_ext(int dim, const double* sig, const ExtLay& L, double* dt, const RelaxConst& rc, cudaStream_t s) {

@@ -29,6 +29,8 @@
 // are summed as planes arrive (see the march); the window roles alternate
 // with period 2, so the march is unrolled two steps and no register moves
 // are issued.
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -149,6 +151,7 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
         }
         mbar_fence_init();
     }
+    pdl_begin();  // the predecessor's outputs are complete from here on
     __syncthreads();
 
     const unsigned a_full = smem_u32(&R.full[0]), a_empty = smem_u32(&R.empty[0]);
@@ -513,8 +516,8 @@ void launch_k(dim3 grid, dim3 block, cudaStream_t s, const TmaSet& tm, double* u
                              cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
         configured = true;
     }
-    k_relax_tma<DIM, SIG, HAS_A, MODE, DUO, CMP><<<grid, block, bytes, s>>>(tm.u, tm.g, tm.s, tm.t, uo, duo, L,
-                                                                            lo, hi, zb, rc, slot, flag, pass_slot);
+    launch_pdl(k_relax_tma<DIM, SIG, HAS_A, MODE, DUO, CMP>, grid, block, bytes, s, tm.u, tm.g, tm.s, tm.t, uo, duo, L,
+               lo, hi, zb, rc, slot, flag, pass_slot);
 }
 
 template <int DIM, bool SIG, bool HAS_A, int MODE, bool DUO>
@@ -587,6 +590,7 @@ void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, c
 template <int DIM, bool SIG, bool HAS_A>
 __global__ void __launch_bounds__(kSmallThreads) k_relax_small(SmallPasses sp, ExtLay L, int3 lo, int3 hi,
                                                                RelaxConst rc, int* flag) {
+    pdl_begin();
     const int nx = hi.x - lo.x + 1, ny = hi.y - lo.y + 1, nz = DIM == 3 ? hi.z - lo.z + 1 : 1;
     const int total = nx * ny * nz;
     const ptrdiff_t sy = L.Px, sz = DIM == 3 ? (ptrdiff_t)L.plane : 0;
@@ -647,6 +651,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_relax_small(SmallPasses sp, E
 
 // planes per CTA: long marches amortise the 2-plane prologue, short ones
 // give small levels enough CTAs (about two waves of 148 SMs x 2)
+bool pdl_enabled() {
+    static const bool on = std::getenv("SGML_NO_PDL") == nullptr;
+    return on;
+}
+
 int relax_tiled_zb(int dim, int cols, int nz) {
     const int target = 2 * 148 * (dim == 3 ? 2 : 4);
     int zb = dim == 3 ? 64 : 128;
@@ -674,7 +683,7 @@ void launch_relax_small(int dim, bool sig, const SmallPasses& sp, const ExtLay& 
                         const RelaxConst& rc, int* flag, cudaStream_t s) {
     const int3 lo = make_int3(rg.lo[0], rg.lo[1], rg.lo[2]);
     const int3 hi = make_int3(rg.hi[0], rg.hi[1], rg.hi[2]);
-#define SGML_SMALL(DD, SS, AA) k_relax_small<DD, SS, AA><<<1, kSmallThreads, 0, s>>>(sp, L, lo, hi, rc, flag)
+#define SGML_SMALL(DD, SS, AA) launch_pdl(k_relax_small<DD, SS, AA>, dim3(1), dim3(kSmallThreads), 0, s, sp, L, lo, hi, rc, flag)
     if (dim == 2) {
         if (sig) { if (rc.has_a) SGML_SMALL(2, true, true); else SGML_SMALL(2, true, false); }
         else { if (rc.has_a) SGML_SMALL(2, false, true); else SGML_SMALL(2, false, false); }
