@@ -239,6 +239,24 @@ int sgml_single_cycle(sgml_ctx* ctx, sgml_field* state_u, const sgml_field* sour
                       double normalization, const sgml_solver_opts* opts, sgml_report* rep,
                       uint64_t* work);
 
+/* single_cycle with the reference's full SolveState semantics
+ * (cycle.cpp:76-111): the state's four buffers (u, u_prev, du, du_prev) and
+ * *level are read and written exactly as the reference does (the cycle
+ * starts from the caller's state.u; du / du_prev reset at every level change;
+ * each pass swaps the buffers, which here swaps the fields' device storage),
+ * an arbitrary schedule (nsteps steps: kind 0 restrict_source / 1 relax,
+ * level, count) and caller-supplied sigma levels (sigma_levels[v] for every
+ * level a step relaxes, or NULL for sigma == 1).  Runs the literal full-grid
+ * kernels pass by pass; a failing pass stops the cycle there, with the trace
+ * samples and work units of the steps before it recorded and the state as
+ * the reference leaves it, and returns SGML_EBADSTEP / SGML_ENONFINITE. */
+int sgml_single_cycle_state(sgml_ctx* ctx, sgml_field* u, sgml_field* u_prev, sgml_field* du,
+                            sgml_field* du_prev, int* level, const sgml_field* source,
+                            sgml_field* const* sigma_levels, double a, const sgml_bc* bc, int homogeneous,
+                            const int* step_kinds, const int* step_levels, const int* step_counts, int nsteps,
+                            double safety, int cycle_index, double normalization, sgml_report* rep,
+                            uint64_t* work);
+
 /* Preallocated engine for repeated solves on one grid/problem shape. */
 int sgml_solver_create(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, double a,
                        const sgml_field* sigma_or_null, const sgml_solver_cfg* cfg,

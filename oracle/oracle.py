@@ -148,6 +148,9 @@ def _load_ref():
     lib.ref_deformation_setup.argtypes = [_D, C.c_int, C.c_double, C.c_int, _D, _D, _D]
     lib.ref_write_field_vtk.argtypes = [G, _D, C.c_char_p, C.c_char_p]
     lib.ref_write_vector_vtk.argtypes = [G, _D, C.c_char_p, C.c_char_p]
+    lib.ref_single_cycle_state.argtypes = [G, B, _D, _D, _D, _D, C.POINTER(C.c_int), _D, _D, C.c_int, C.c_double,
+                                           C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                           C.c_int, C.c_double, C.c_int, C.c_double, C.POINTER(Report), _U64P]
     lib.ref_session_create.argtypes = [G, B, _D, _D, C.c_double, C.c_int, C.c_double]
     lib.ref_session_create.restype = C.c_void_p
     lib.ref_session_destroy.argtypes = [C.c_void_p]
@@ -358,6 +361,30 @@ def ref_problem(name: str, n: int):
         raise ValueError(name)
     bc = make_bc(list(kinds), list(vals))
     return g, bc, f, (sig if rc == 3 else None), a.value
+
+
+def ref_single_cycle_state(g: Grid, bc: Bc, u, u_prev, du, du_prev, level, source, sigma_levels, a, homogeneous,
+                           steps, safety, cycle_index, normalization, work=0):
+    """The reference's single_cycle on an arbitrary state / schedule / sigma
+    levels; returns (status, u, u_prev, du, du_prev, level, trace, work)."""
+    lib = ref_lib()
+    arrs = [np.ascontiguousarray(x, np.float64).reshape(-1).copy() for x in (u, u_prev, du, du_prev)]
+    lv = None if sigma_levels is None else np.ascontiguousarray(sigma_levels, np.float64).reshape(-1)
+    nl = 0 if sigma_levels is None else len(sigma_levels)
+    n = len(steps)
+    kinds = (C.c_int * max(n, 1))(*[s[0] for s in steps])
+    levels = (C.c_int * max(n, 1))(*[s[1] for s in steps])
+    counts = (C.c_int * max(n, 1))(*[s[2] for s in steps])
+    lev = C.c_int(level)
+    w = C.c_uint64(work)
+    rep, rows, trace = _report()
+    src = np.ascontiguousarray(source, np.float64).reshape(-1)
+    st = lib.ref_single_cycle_state(C.byref(g), C.byref(bc), *[_ptr(x) for x in arrs], C.byref(lev), _ptr(src),
+                                    _ptr(lv), nl, a, int(homogeneous), kinds, levels, counts, n, safety, cycle_index,
+                                    normalization, C.byref(rep), C.byref(w))
+    tr = [(trace[i].cycle, trace[i].pass_, trace[i].level, trace[i].value)
+          for i in range(min(rep.n_trace, rep.trace_cap))]
+    return st, arrs[0], arrs[1], arrs[2], arrs[3], lev.value, tr, w.value
 
 
 class RefSession:

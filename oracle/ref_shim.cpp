@@ -154,6 +154,51 @@ int ref_single_cycle(const og_grid* g, const og_bc* bc, double* u_out, const dou
     return status;
 }
 
+// single_cycle with an arbitrary state, schedule and sigma levels (the
+// reference's full SolveState semantics; cycle.cpp:76-111)
+int ref_single_cycle_state(const og_grid* g, const og_bc* bc, double* u, double* u_prev, double* du,
+                           double* du_prev, int* level, const double* source, const double* sigma_levels,
+                           int nlevels, double a, int homogeneous, const int* kinds, const int* levels,
+                           const int* counts, int nsteps, double safety, int cycle_index, double normalization,
+                           og_report* rep, uint64_t* work) {
+    const R::Grid gr = grid_of(g);
+    R::SolveState st(gr);
+    std::memcpy(st.u.data(), u, gr.total * sizeof(double));
+    std::memcpy(st.u_prev.data(), u_prev, gr.total * sizeof(double));
+    std::memcpy(st.du.data(), du, gr.total * sizeof(double));
+    std::memcpy(st.du_prev.data(), du_prev, gr.total * sizeof(double));
+    st.level = *level;
+    std::vector<R::Field> lv;
+    for (int v = 0; sigma_levels && v < nlevels; ++v) lv.push_back(to_field(gr, sigma_levels + (size_t)v * gr.total));
+    R::CycleSchedule sch;
+    sch.n = gr.n;
+    for (int i = 0; i < nsteps; ++i)
+        sch.steps.push_back({kinds[i] == 0 ? R::ScheduleStep::Kind::restrict_source : R::ScheduleStep::Kind::relax,
+                             levels[i], counts[i]});
+    R::SolveReport report;
+    std::uint64_t w = *work;
+    int status = 0;
+    try {
+        R::single_cycle(st, to_field(gr, source), lv, a, to_bc(bc), homogeneous != 0, sch, safety, cycle_index,
+                        normalization, report, w);
+    } catch (const R::kernel_error& e) {
+        status = std::strstr(e.what(), "step") ? OG_BADSTEP : OG_NONFINITE;
+    }
+    *work = w;
+    from_field(st.u, u);
+    from_field(st.u_prev, u_prev);
+    from_field(st.du, du);
+    from_field(st.du_prev, du_prev);
+    *level = st.level;
+    rep->n_trace = 0;
+    for (const auto& smp : report.trace) {
+        if (rep->n_trace < rep->trace_cap)
+            rep->trace[rep->n_trace] = og_sample{smp.cycle, smp.pass, smp.level, 0, smp.value};
+        rep->n_trace++;
+    }
+    return status;
+}
+
 int ref_solve(const og_grid* g, const og_bc* bc, const double* f, const double* sigma, double a,
               int n_r, double tol, int max_cycles, double safety, double* u_out, og_report* rep) {
     const R::Grid gr = grid_of(g);

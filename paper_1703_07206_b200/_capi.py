@@ -100,6 +100,10 @@ _SIGNATURES = {
     "sgml_single_cycle": ([_P, _P, _P, C.POINTER(_P), C.c_double, C.POINTER(Bc), C.c_int, C.c_int,
                            C.c_double, C.c_int, C.c_double, C.POINTER(SolverOpts), C.POINTER(Report),
                            _U64P], C.c_int),
+    "sgml_single_cycle_state": ([_P, _P, _P, _P, _P, C.POINTER(C.c_int), _P, C.POINTER(_P), C.c_double,
+                                 C.POINTER(Bc), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                 C.POINTER(C.c_int), C.c_int, C.c_double, C.c_int, C.c_double, C.POINTER(Report),
+                                 _U64P], C.c_int),
     "sgml_solver_create": ([_P, C.c_int, C.c_int, C.POINTER(Bc), C.c_double, _P,
                             C.POINTER(SolverCfg), C.POINTER(SolverOpts), C.POINTER(_P)], C.c_int),
     "sgml_solver_destroy": ([_P], C.c_int),

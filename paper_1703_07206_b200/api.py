@@ -25,7 +25,7 @@ __all__ = [
     "max_abs", "trapezoid_mean", "zero_mean_projection", "apply_boundary", "ScheduleStep",
     "CycleSchedule", "build_schedule", "closed_form_work_units", "schedule_work_units",
     "SolverConfig", "SolverOptions", "DiagSample", "CycleRecord", "SolveReport", "ProblemSpec",
-    "SolveResult", "single_cycle", "solve", "solve_many", "Solver", "restrict_sigma_levels", "pure_neumann_pin",
+    "SolveResult", "single_cycle", "single_cycle_state", "solve", "solve_many", "Solver", "restrict_sigma_levels", "pure_neumann_pin",
     "kernel_error", "LocalGroup", "nccl_unique_id", "slab_plan",
 ]
 
@@ -721,6 +721,37 @@ def single_cycle(state: SolveState, source: Field, sigma_levels: Sequence[Field]
                                       float(normalization), C.byref(opts), C.byref(rb.c), C.byref(w)))
     finally:
         work.value = w.value
+        report.trace.extend(rb.to_report().trace)
+
+
+def single_cycle_state(state: SolveState, source: Field, sigma_levels: Sequence[Field], a: float,
+                       bc: BoundarySpec, homogeneous: bool, schedule: CycleSchedule, safety: float,
+                       cycle_index: int, normalization: float, report: SolveReport, work: _Work) -> None:
+    """cycle.cpp:76-111 with the reference's full SolveState semantics (the C++
+    drop-in's single_cycle): the cycle starts from state.u, runs the
+    schedule's own steps with the given sigma levels (one per level, or none),
+    and leaves u, u_prev, du, du_prev and level as the reference does, also
+    when a pass raises kernel_error (the literal kernels, pass by pass)."""
+    n = len(schedule.steps)
+    kinds = (C.c_int * max(n, 1))(*[int(st.kind) for st in schedule.steps])
+    levels = (C.c_int * max(n, 1))(*[int(st.level) for st in schedule.steps])
+    counts = (C.c_int * max(n, 1))(*[int(st.count) for st in schedule.steps])
+    passes = sum(int(st.count) for st in schedule.steps if int(st.kind) == 1)
+    rb = _ReportBuffers(rows_cap=1, trace_cap=max(passes, 1))
+    lv = None
+    if sigma_levels:
+        lv = (C.c_void_p * len(sigma_levels))(*[f.handle.value for f in sigma_levels])
+    level = C.c_int(state.level)
+    w = C.c_uint64(work.value)
+    try:
+        check(lib().sgml_single_cycle_state(source.ctx.handle, state.u.handle, state.u_prev.handle, state.du.handle,
+                                            state.du_prev.handle, C.byref(level), source.handle, lv, float(a),
+                                            C.byref(bc.to_c()), int(bool(homogeneous)), kinds, levels, counts, n,
+                                            float(safety), int(cycle_index), float(normalization), C.byref(rb.c),
+                                            C.byref(w)))
+    finally:
+        work.value = w.value
+        state.level = level.value
         report.trace.extend(rb.to_report().trace)
 
 

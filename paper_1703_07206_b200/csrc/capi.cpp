@@ -537,6 +537,90 @@ int sgml_single_cycle(sgml_ctx* ctx, sgml_field* state_u, const sgml_field* sour
     });
 }
 
+int sgml_single_cycle_state(sgml_ctx* ctx, sgml_field* u, sgml_field* u_prev, sgml_field* du,
+                            sgml_field* du_prev, int* level, const sgml_field* source,
+                            sgml_field* const* sigma_levels, double a, const sgml_bc* bc, int homogeneous,
+                            const int* step_kinds, const int* step_levels, const int* step_counts, int nsteps,
+                            double safety, int cycle_index, double normalization, sgml_report* rep,
+                            uint64_t* work) {
+    return guarded([&] {
+        require(ctx && u && u_prev && du && du_prev && level && source && bc && rep && work, SGML_EINVAL,
+                "single_cycle: null argument");
+        require(nsteps >= 0 && (nsteps == 0 || (step_kinds && step_levels && step_counts)), SGML_EINVAL,
+                "single_cycle: bad schedule");
+        const sgml_field* others[4] = {u_prev, du, du_prev, source};
+        for (const sgml_field* f : others) same_grid(u, f, "single_cycle: grid mismatch");
+        const sgml_grid& g = u->grid;
+        for (int i = 0; i < nsteps; ++i)
+            require(step_levels[i] >= 0 && step_levels[i] <= g.n && step_counts[i] >= 0, SGML_EINVAL,
+                    "single_cycle: bad schedule step");
+        activate(ctx);
+        CtxLock lk(ctx->mu);
+        const cudaStream_t s = ctx->stream;
+        const BcDev b = to_dev(*bc);
+        // cycle.cpp:83-84: g and scratch start zeroed every cycle
+        DevBuf gbuf(g.total * sizeof(double)), sbuf(g.total * sizeof(double));
+        double* gd = gbuf.d();
+        double* sd = sbuf.d();
+        SGML_CUDA(cudaMemsetAsync(gd, 0, g.total * sizeof(double), s));
+        SGML_CUDA(cudaMemsetAsync(sd, 0, g.total * sizeof(double), s));
+        int pass_index = 0, current = -1;
+        const double inv_norm = normalization > 0.0 ? 1.0 / normalization : 1.0;
+        for (int i = 0; i < nsteps; ++i) {
+            const int v = step_levels[i];
+            if (step_kinds[i] == 0) {
+                // restriction_into(source, v, bc, g, scratch, &work) (kernels.cpp:305-325)
+                if (v == 0) {
+                    SGML_CUDA(cudaMemcpyAsync(gd, source->d, g.total * sizeof(double), cudaMemcpyDeviceToDevice, s));
+                } else {
+                    const double* src = source->d;
+                    double* dst = (v % 2 == 1) ? gd : sd;
+                    for (int m = 0; m < v; ++m) {
+                        launch_restrict_pass(g.dim, src, dst, g.N, 1 << m, b, s);
+                        src = dst;
+                        dst = (dst == gd) ? sd : gd;
+                    }
+                    *work += (uint64_t)v;
+                    pass_index += v;
+                }
+                continue;
+            }
+            if (v != current) {  // SolveState::reset_level
+                SGML_CUDA(cudaMemsetAsync(du->d, 0, g.total * sizeof(double), s));
+                SGML_CUDA(cudaMemsetAsync(du_prev->d, 0, g.total * sizeof(double), s));
+                *level = v;
+                current = v;
+            }
+            const sgml_field* sig = sigma_levels ? sigma_levels[v] : nullptr;
+            if (sig) same_grid(u, sig, "single_cycle: sigma level grid mismatch");
+            const RelaxConst rc = relax_const(g.dim, v, g.h, a, safety, homogeneous != 0);
+            for (int c = 0; c < step_counts[i]; ++c) {
+                std::swap(u->d, u_prev->d);  // SolveState::swap_buffers
+                std::swap(du->d, du_prev->d);
+                SGML_CUDA(cudaMemsetAsync(ctx->d_slots, 0, sizeof(unsigned long long), s));
+                SGML_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), s));
+                launch_relax_literal(g.dim, sig != nullptr, u->d, du->d, u_prev->d, du_prev->d, gd,
+                                     sig ? sig->d : nullptr, g.N, v, rc, b, ctx->d_slots, ctx->d_flags, 0, s);
+                SGML_CUDA(cudaGetLastError());
+                SGML_CUDA(cudaMemcpyAsync(ctx->h_slots, ctx->d_slots, sizeof(unsigned long long),
+                                          cudaMemcpyDeviceToHost, s));
+                SGML_CUDA(cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+                SGML_CUDA(cudaStreamSynchronize(s));
+                // kernels.cpp:343-346: the pass throws before its work unit and sample
+                if (!(safety > 0.0)) fail(SGML_EBADSTEP, "relaxation_interpolation: non-positive pseudo-time step");
+                if (ctx->h_flags[0]) fail(SGML_ENONFINITE, "relaxation_interpolation: non-finite value produced");
+                *work += 1;
+                if (rep->n_trace < rep->trace_cap)
+                    rep->trace[rep->n_trace] =
+                        sgml_diag_sample{cycle_index, pass_index, v, 0, slot_to_double(ctx->h_slots[0]) * inv_norm};
+                rep->n_trace++;
+                ++pass_index;
+            }
+        }
+        SGML_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
 int sgml_solver_create(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, double a,
                        const sgml_field* sigma, const sgml_solver_cfg* cfg,
                        const sgml_solver_opts* opts, sgml_solver** out) {

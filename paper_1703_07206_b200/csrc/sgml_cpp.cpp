@@ -201,29 +201,52 @@ int l1_hook(void* user, int, const sgml_field* u_total, double* l1) {
 
 }  // namespace
 
+// cycle.cpp:76-111 with the reference's full SolveState semantics: the caller's
+// state (all four buffers and the level) goes in and comes back as the
+// reference leaves it, the schedule's own steps and the caller's sigma levels
+// are used (sgml_single_cycle_state: literal full-grid kernels, pass by pass)
 void single_cycle(SolveState& state, const Field& source, const std::vector<Field>& sigma_levels, double a,
                   const BoundarySpec& bc, bool homogeneous, const CycleSchedule& schedule, double safety,
                   int cycle_index, double normalization, SolveReport& report, std::uint64_t& work_units) {
     const Grid& g = source.grid();
-    Dev su(g), src(source);
+    Dev u(state.u), up(state.u_prev), du(state.du), dup(state.du_prev), src(source);
     std::vector<std::unique_ptr<Dev>> lv;
     std::vector<sgml_field*> lvp;
     for (const Field& f : sigma_levels) {
         lv.push_back(std::make_unique<Dev>(f));
         lvp.push_back(lv.back()->f);
     }
+    std::vector<int> kinds, levels, counts;
+    std::size_t passes = 0;
+    for (const ScheduleStep& st : schedule.steps) {
+        if (st.kind == ScheduleStep::Kind::relax && !lvp.empty() && static_cast<std::size_t>(st.level) >= lvp.size())
+            throw std::out_of_range("single_cycle: no sigma level for a relax step");
+        kinds.push_back(st.kind == ScheduleStep::Kind::restrict_source ? 0 : 1);
+        levels.push_back(st.level);
+        counts.push_back(st.count);
+        if (st.kind == ScheduleStep::Kind::relax) passes += static_cast<std::size_t>(st.count);
+    }
     const sgml_bc b = to_c(bc);
-    std::vector<sgml_diag_sample> trace(relax_passes(g.n, schedule.n_r));
+    std::vector<sgml_diag_sample> trace(std::max<std::size_t>(passes, 1));
     sgml_report rep{};
     rep.trace = trace.data();
     rep.trace_cap = static_cast<int64_t>(trace.size());
-    const int st = sgml_single_cycle(context(), su.f, src.f, lvp.empty() ? nullptr : lvp.data(), a, &b,
-                                     homogeneous ? 1 : 0, schedule.n_r, safety, cycle_index, normalization,
-                                     nullptr, &rep, &work_units);
+    int level = state.level;
+    const int st = sgml_single_cycle_state(context(), u.f, up.f, du.f, dup.f, &level, src.f,
+                                           lvp.empty() ? nullptr : lvp.data(), a, &b, homogeneous ? 1 : 0,
+                                           kinds.data(), levels.data(), counts.data(), static_cast<int>(kinds.size()),
+                                           safety, cycle_index, normalization, &rep, &work_units);
     for (int64_t t = 0; t < std::min<int64_t>(rep.n_trace, rep.trace_cap); ++t)
         report.trace.push_back(DiagSample{trace[t].cycle, trace[t].pass, trace[t].level, trace[t].value});
+    // the state as the reference leaves it (also when a pass throws)
+    if (st == SGML_OK || st == SGML_EBADSTEP || st == SGML_ENONFINITE) {
+        u.to(state.u);
+        up.to(state.u_prev);
+        du.to(state.du);
+        dup.to(state.du_prev);
+        state.level = level;
+    }
     check(st);
-    su.to(state.u);
 }
 
 SolveResult solve(const ProblemSpec& problem, const SolverConfig& config) {
