@@ -86,6 +86,10 @@ typedef struct {
     int small_levels; /* 0 (default): a visit of a small level array (<= 6144 relaxed
                        nodes) runs all its passes in one CTA; -1: one TMA launch per
                        pass on every level (same bits either way) */
+    int replicate_n;  /* z-slab solves: levels whose arrays hold at most this many nodes
+                       per axis are replicated on every rank instead of exchanging
+                       halos (0: SGML_REPLICATE_N = 65; levels also replicate once a
+                       rank would hold fewer than 2 planes) */
 } sgml_solver_opts;
 
 enum { SGML_STENCIL_RADIAL = 0, SGML_STENCIL_COMPACT = 1 };
@@ -186,6 +190,9 @@ int sgml_ctx_clique(sgml_ctx* ctx, int* nranks, int* rank);
  * owns level-v planes [z0 >> v, (z0 >> v) + nz_v) with nz_v = (nz - last) >> v
  * + last, last = (rank == nranks - 1); level-0 planes [*z0, *z0 + *nz) */
 int sgml_slab_plan(int n, int nranks, int rank, int* vrep, int* z0, int* nz);
+/* the same with an explicit replicate_n (sgml_solver_opts; 0: the default) */
+int sgml_slab_plan_ex(int n, int nranks, int rank, int replicate_n, int* vrep, int* z0, int* nz);
+#define SGML_REPLICATE_N 65
 
 /* ---- grid / schedule (host logic; no device needed) --------------------- */
 int sgml_make_grid(int dim, int n, sgml_grid* out);                      /* grid.cpp:10-23 */

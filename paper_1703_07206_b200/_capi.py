@@ -33,7 +33,8 @@ class SolverCfg(C.Structure):
 
 class SolverOpts(C.Structure):
     _fields_ = [("engine", C.c_int), ("use_graph", C.c_int), ("timing", C.c_int),
-                ("timing_classes", C.c_int), ("stencil", C.c_int), ("small_levels", C.c_int)]
+                ("timing_classes", C.c_int), ("stencil", C.c_int), ("small_levels", C.c_int),
+                ("replicate_n", C.c_int)]
 
 
 class CycleRecord(C.Structure):
@@ -119,6 +120,8 @@ _SIGNATURES = {
     "sgml_local_group_destroy": ([_P], C.c_int),
     "sgml_ctx_join_local": ([_P, _P, C.c_int], C.c_int),
     "sgml_ctx_clique": ([_P, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+    "sgml_slab_plan_ex": ([C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                           C.POINTER(C.c_int)], C.c_int),
     "sgml_slab_plan": ([C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
                         C.POINTER(C.c_int)], C.c_int),
     "sgml_axis_derivative": ([_P, C.c_int, _P], C.c_int),

@@ -220,11 +220,12 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def slab_plan(n: int, nranks: int, rank: int) -> tuple[int, int, int]:
+def slab_plan(n: int, nranks: int, rank: int, replicate_n: int = 0) -> tuple[int, int, int]:
     """(vrep, z0, nz): levels < vrep are z-slabs; `rank` owns level-0 planes
-    [z0, z0 + nz) of the 2^n + 1 (host only)."""
+    [z0, z0 + nz) of the 2^n + 1 (host only).  replicate_n as in
+    SolverOptions (0: levels of <= 65 nodes per axis are replicated)."""
     v, z0, nz = C.c_int(), C.c_int(), C.c_int()
-    check(lib().sgml_slab_plan(n, nranks, rank, C.byref(v), C.byref(z0), C.byref(nz)))
+    check(lib().sgml_slab_plan_ex(n, nranks, rank, int(replicate_n), C.byref(v), C.byref(z0), C.byref(nz)))
     return v.value, z0.value, nz.value
 
 
@@ -475,13 +476,15 @@ class SolverOptions:
     timing_classes: int = 0     # 0: time every kernel class; else a mask of 1 << class index
     stencil: str = "radial"     # "radial" (the reference's) or "compact" 5/7-point (no reference)
     small_levels: bool = True   # one CTA per visit of a small level array (else one launch per pass)
+    replicate_n: int = 0        # z-slab solves: replicate levels of <= this many nodes per axis (0: 65)
 
     def to_c(self) -> _capi.SolverOpts:
         if self.stencil not in ("radial", "compact"):
             raise ValueError("stencil must be 'radial' or 'compact'")
         return _capi.SolverOpts(0 if self.engine == "compact" else 1, 1 if self.use_graph else -1,
                                 int(self.timing), int(self.timing_classes),
-                                0 if self.stencil == "radial" else 1, 0 if self.small_levels else -1)
+                                0 if self.stencil == "radial" else 1, 0 if self.small_levels else -1,
+                                int(self.replicate_n))
 
 
 @dataclass

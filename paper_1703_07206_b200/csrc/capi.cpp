@@ -154,6 +154,10 @@ int sgml_ctx_clique(sgml_ctx* ctx, int* nranks, int* rank) {
 }
 
 int sgml_slab_plan(int n, int nranks, int rank, int* vrep, int* z0, int* nz) {
+    return sgml_slab_plan_ex(n, nranks, rank, 0, vrep, z0, nz);
+}
+
+int sgml_slab_plan_ex(int n, int nranks, int rank, int replicate_n, int* vrep, int* z0, int* nz) {
     return guarded([&] {
         require(vrep && z0 && nz, SGML_EINVAL, "slab_plan: null argument");
         require(n >= 1 && n <= 13, SGML_EINVAL, "slab_plan: n must lie in [1, 13]");
@@ -163,10 +167,7 @@ int sgml_slab_plan(int n, int nranks, int rank, int* vrep, int* z0, int* nz) {
                 "slab_plan: too many ranks for this grid (>= 2 planes each)");
         require(rank >= 0 && rank < nranks, SGML_EINVAL, "slab_plan: bad rank");
         const int t0 = (1 << n) / nranks;
-        int v = 0;
-        if (nranks > 1)
-            while ((t0 >> v) >= 2) ++v;
-        *vrep = v;
+        *vrep = slab_vrep(n, nranks, replicate_n);
         *z0 = rank * t0;
         *nz = t0 + (rank == nranks - 1 ? 1 : 0);
     });

@@ -87,6 +87,16 @@ int relax_count(int n, int n_r, int v1) {
     return (int)std::min<long long>(n_r, doubling);
 }
 
+int slab_vrep(int n, int nranks, int replicate_n) {
+    if (nranks <= 1) return 0;
+    const int t0 = (1 << n) / nranks, rn = replicate_n > 0 ? replicate_n : SGML_REPLICATE_N;
+    int v = 0;
+    // replicated coarse levels cost a redundant pass on every rank; slab
+    // levels cost a halo exchange (latency) per producer
+    while ((t0 >> v) >= 2 && (1 << (n - v)) + 1 > rn) ++v;
+    return v;
+}
+
 // kernels.cpp:182-188 and the sigma == 1 step (see RelaxConst)
 RelaxConst relax_const(int dim, int level, double h, double a, double safety, bool homogeneous, int compact) {
     RelaxConst rc{};
@@ -369,8 +379,12 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
         if (nrk & (nrk - 1)) fail(SGML_EINVAL, "solve: the number of ranks must be a power of two");
         if (nrk > (1 << (n - 1))) fail(SGML_EINVAL, "solve: too many ranks for this grid (>= 2 planes each)");
         T0 = (1 << n) / nrk;  // level-0 planes per rank (the last rank also owns plane N-1)
-        vrep = 0;
-        while ((T0 >> vrep) >= 2) ++vrep;  // levels v < vrep hold >= 2 planes per rank
+        vrep = slab_vrep(n, nrk, opts.replicate_n);  // levels v < vrep are z-slabs
+        // the transfer stream of the overlapped halo exchanges (created here,
+        // not inside a graph capture)
+        SGML_CUDA(cudaStreamCreateWithFlags(&hx_stream, cudaStreamNonBlocking));
+        SGML_CUDA(cudaEventCreateWithFlags(&hx_ready, cudaEventDisableTiming));
+        SGML_CUDA(cudaEventCreateWithFlags(&hx_done, cudaEventDisableTiming));
     }
 
     if (compact()) {
@@ -538,13 +552,7 @@ void sgml_solver::halo(double* a, int v) {
 // interior planes (SGML_NO_HALO_OVERLAP=1: exchange after the whole pass)
 bool sgml_solver::overlap_halos(int v) {
     static const bool off = std::getenv("SGML_NO_HALO_OVERLAP") != nullptr;
-    if (off || !dist(v) || rng[v].hi[2] - rng[v].lo[2] < 2) return false;
-    if (!hx_stream) {
-        SGML_CUDA(cudaStreamCreateWithFlags(&hx_stream, cudaStreamNonBlocking));
-        SGML_CUDA(cudaEventCreateWithFlags(&hx_ready, cudaEventDisableTiming));
-        SGML_CUDA(cudaEventCreateWithFlags(&hx_done, cudaEventDisableTiming));
-    }
-    return true;
+    return !off && dist(v) && hx_stream && rng[v].hi[2] - rng[v].lo[2] >= 2;
 }
 
 // a replicated level array whose planes were produced rank by rank (own
@@ -778,9 +786,13 @@ bool sgml_solver::small_visit(int v, const double* in, int c, const double* p0, 
     return true;
 }
 
+// Single-GPU solves replay each cycle from a CUDA graph; z-slab solves too
+// when the transport's exchanges are stream-ordered (NCCL: the halo
+// send/recv and the plane broadcasts become graph nodes between the kernels).
 bool sgml_solver::use_graphs() const {
     static const int off = std::getenv("SGML_NO_GRAPHS") ? 1 : 0;
-    return compact() && nrk == 1 && !off && opts.use_graph >= 0 && debug_sync <= 0 && !diag_mode;
+    const bool clique_ok = nrk == 1 || (tp && tp->graph_capturable() && !slab_graphs_off);
+    return compact() && clique_ok && !off && opts.use_graph >= 0 && debug_sync <= 0 && !diag_mode;
 }
 
 const double* sgml_solver::cycle_graph(bool homogeneous) {
@@ -815,10 +827,31 @@ const double* sgml_solver::cycle_graph(bool homogeneous) {
         throw;
     }
     capturing = nullptr;
-    SGML_CUDA(cudaStreamEndCapture(s, &graph));
-    const cudaError_t ie = cudaGraphInstantiate(&G.exec, graph, 0);
-    cudaGraphDestroy(graph);
-    SGML_CUDA(ie);
+    cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    if (ce == cudaSuccess) {
+        ce = cudaGraphInstantiate(&G.exec, graph, 0);
+        cudaGraphDestroy(graph);
+    }
+    if (nrk > 1) {
+        // a z-slab clique captures together: every rank must replay (or none),
+        // or the ranks' exchanges would not pair up
+        h_flag[6] = ce != cudaSuccess ? 1 : 0;
+        (void)cudaGetLastError();
+        SGML_CUDA(cudaMemcpyAsync(d_flag + 6, h_flag + 6, sizeof(int), cudaMemcpyHostToDevice, s));
+        tp->allreduce_max_i32(d_flag + 6, 1, s);
+        SGML_CUDA(cudaMemcpyAsync(h_flag + 6, d_flag + 6, sizeof(int), cudaMemcpyDeviceToHost, s));
+        SGML_CUDA(cudaStreamSynchronize(s));
+        if (h_flag[6]) {
+            if (G.exec) cudaGraphExecDestroy(G.exec);
+            G.exec = nullptr;
+            slab_graphs_off = true;  // this solver runs its cycles eagerly from now on
+            fstate = G.pre;
+            spans.resize(s0);
+            launches = l0;
+            return cycle_compact(homogeneous);
+        }
+    }
+    SGML_CUDA(ce);
     G.post = fstate;
     G.out = e;
     G.nlaunch = launches - l0;

@@ -88,6 +88,10 @@ BcDev to_dev(const sgml_bc& bc);
 bool any_dirichlet(const sgml_bc& bc, int dim);
 sgml_grid make_grid_or_throw(int dim, int n);
 int relax_count(int n, int n_r, int v1);
+// first replicated level of a z-slab solve on nranks ranks:
+// levels v < vrep are z-slabs while a rank holds >= 2 planes of them and their
+// arrays have more than replicate_n (0: SGML_REPLICATE_N) nodes per axis
+int slab_vrep(int n, int nranks, int replicate_n);
 RelaxConst relax_const(int dim, int level, double h, double a, double safety, bool homogeneous,
                        int compact = 0);
 double* dalloc(size_t count);
@@ -222,6 +226,7 @@ struct sgml_solver {
     };
     CycleGraph graphs[2];                 // by homogeneous
     CycleGraph* capturing = nullptr;
+    bool slab_graphs_off = false;         // a z-slab capture failed on some rank: eager cycles
     bool use_graphs() const;
     bool small_visit(int v, const double* in, int c, const double* p0, const double* p1, bool homogeneous) const;
     const double* cycle_graph(bool homogeneous);

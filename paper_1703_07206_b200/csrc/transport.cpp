@@ -193,6 +193,8 @@ public:
     void allreduce_max_i32(int* d, int n, cudaStream_t s) override {
         SGML_NCCL(nccl().AllReduce(d, d, (size_t)n, ncclInt32, ncclMax, comm_, s));
     }
+    // NCCL send/recv/broadcast are graph-capturable (SGML_NO_SLAB_GRAPHS=1: eager)
+    bool graph_capturable() const override { return std::getenv("SGML_NO_SLAB_GRAPHS") == nullptr; }
 
 private:
     ncclComm_t comm_ = nullptr;

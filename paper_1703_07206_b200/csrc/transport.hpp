@@ -45,6 +45,9 @@ public:
     // element-wise max over ranks (non-negative doubles as u64, or flags)
     virtual void allreduce_max_u64(unsigned long long* d, int n, cudaStream_t s) = 0;
     virtual void allreduce_max_i32(int* d, int n, cudaStream_t s) = 0;
+    // every exchange is stream-ordered device work (no host synchronisation),
+    // so a cycle with its exchanges can be captured into a CUDA graph
+    virtual bool graph_capturable() const { return false; }
 };
 
 // ---- in-process ranks ------------------------------------------------------

@@ -37,15 +37,15 @@ def join_torch_clique(ctx: Context) -> tuple[int, int]:
     return n, r
 
 
-def plan_table(n: int, nranks: int) -> list[tuple[int, int, int]]:
+def plan_table(n: int, nranks: int, replicate_n: int = 0) -> list[tuple[int, int, int]]:
     """slab_plan of every rank: [(vrep, z0, nz)] (host only)."""
-    return [slab_plan(n, nranks, r) for r in range(nranks)]
+    return [slab_plan(n, nranks, r, replicate_n) for r in range(nranks)]
 
 
-def check_plan(n: int, nranks: int) -> None:
+def check_plan(n: int, nranks: int, replicate_n: int = 0) -> None:
     """The per-rank plans tile every distributed level exactly once and agree
     on the replicated levels (raises AssertionError otherwise)."""
-    table = plan_table(n, nranks)
+    table = plan_table(n, nranks, replicate_n)
     vreps = {t[0] for t in table}
     assert len(vreps) == 1, "ranks disagree on the replicated levels"
     vrep = vreps.pop()

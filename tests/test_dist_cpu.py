@@ -55,6 +55,15 @@ def test_two_gloo_ranks_share_id_and_plan():
         D.check_plan(n, 2)
 
 
+@pytest.mark.parametrize("replicate_n", [0, 3])
 @pytest.mark.parametrize("n,nranks", [(3, 4), (4, 8), (9, 2), (9, 8), (10, 8), (13, 4096)])
-def test_slab_plans_tile_every_level(n, nranks):
-    D.check_plan(n, nranks)
+def test_slab_plans_tile_every_level(n, nranks, replicate_n):
+    D.check_plan(n, nranks, replicate_n)
+
+
+@pytest.mark.parametrize("n,nranks,rn,vrep", [
+    (10, 8, 0, 4),   # 1025^3 on 8 ranks: levels 0..3 (1025..129) slabs, 65^3 and coarser replicated
+    (10, 8, 3, 7),   # replicate only where a rank would hold < 2 planes
+    (9, 2, 0, 3), (6, 2, 0, 0), (9, 8, 129, 2)])
+def test_replicated_levels_start_at_65_nodes(n, nranks, rn, vrep):
+    assert S.slab_plan(n, nranks, 0, rn)[0] == vrep

@@ -22,7 +22,9 @@ def sbc_of(b):
     return S.BoundarySpec([S.FaceBc(S.BcKind(b.kind[f]), b.value[f]) for f in range(6)])
 
 
-def solve_clique(name, n, nranks, n_r=2, max_cycles=40, stencil="radial"):
+def solve_clique(name, n, nranks, n_r=2, max_cycles=40, stencil="radial", replicate_n=3):
+    # replicate_n = 3: the small test grids keep z-slab levels down to 2 planes
+    # per rank (the default replicates every level of <= 65 nodes per axis)
     g, b, f, s, a = K.solve_problem(name, n)
     group = S.LocalGroup(nranks)
     out, err = [None] * nranks, [None] * nranks
@@ -34,7 +36,7 @@ def solve_clique(name, n, nranks, n_r=2, max_cycles=40, stencil="radial"):
             assert ctx.clique() == (nranks, r)
             prob = S.ProblemSpec(sgrid(g), f, bc=sbc_of(b), sigma=s, a=a)
             out[r] = S.solve(prob, S.SolverConfig(n_r=n_r, tol=1e-10, max_cycles=max_cycles, safety=0.9),
-                             S.SolverOptions(stencil=stencil), ctx=ctx)
+                             S.SolverOptions(stencil=stencil, replicate_n=replicate_n), ctx=ctx)
         except Exception as exc:  # surfaced below
             err[r] = exc
 
@@ -99,8 +101,9 @@ def test_slab_solve_compact_stencil(name, n):
 
 
 @pytest.mark.timeout(900)
-@pytest.mark.parametrize("name,n,nranks", [("poisson3d", 7, 4), ("capacitor_low", 6, 2)])
-def test_slab_solve_larger_equals_single_gpu(name, n, nranks):
+@pytest.mark.parametrize("name,n,nranks,rn", [("poisson3d", 7, 4, 3), ("capacitor_low", 6, 2, 3),
+                                              ("poisson3d", 7, 2, 0), ("capacitor_high", 7, 4, 0)])
+def test_slab_solve_larger_equals_single_gpu(name, n, nranks, rn):
     # 129^3 / 65^3: deeper slab levels and replicated coarse levels; compared with
     # the single-GPU solve (pinned to the reference elsewhere), every rank bit for bit
     g, b, f, s, a = K.solve_problem(name, n)
@@ -114,7 +117,7 @@ def test_slab_solve_larger_equals_single_gpu(name, n, nranks):
         try:
             ctx = S.Context(0)
             ctx.join_local(group, r)
-            out[r] = S.solve(prob, cfg, ctx=ctx)
+            out[r] = S.solve(prob, cfg, S.SolverOptions(replicate_n=rn), ctx=ctx)
         except Exception as exc:  # surfaced below
             err[r] = exc
 
