@@ -770,6 +770,7 @@ bool sgml_solver::small_visit(int v, const double* in, int c, const double* p0, 
     long long nodes = 1;
     for (int ax = 0; ax < g.dim; ++ax) nodes *= (long long)(rng[v].hi[ax] - rng[v].lo[ax] + 1);
     if (nodes <= 0 || nodes > kSmallNodes) return false;
+    if (ext_size(g.dim, Lv[v]) > (uint64_t)kSmallMaxExt) return false;  // (staged whole in shared memory)
     if (all_neumann) return true;
     const int want = face_want(homogeneous);
     const double* cur = in;

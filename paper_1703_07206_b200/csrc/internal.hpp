@@ -99,6 +99,10 @@ struct NodeRange {
 constexpr int kSmallThreads = 512;
 constexpr int kSmallNodes = 6144;
 constexpr int kSmallMaxPasses = 16;
+// the one-CTA visit stages three whole level arrays in shared memory; the
+// largest small array is 3D N = 17 (20 x 19 x 19 doubles) or 2D N = 65 (68 x 67)
+constexpr int kSmallMaxExt = 20 * 19 * 19;
+constexpr int kSmallSmem = 3 * kSmallMaxExt * 8;
 struct SmallPasses {
     const double* in[kSmallMaxPasses];
     double* out[kSmallMaxPasses];

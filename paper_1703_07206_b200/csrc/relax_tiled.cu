@@ -585,17 +585,33 @@ void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, c
 // kernel per pass).  Same arithmetic as the reference's relax branch
 // (kernels.cpp:94-137) on the ghost-extended array (mirror ghosts in memory),
 // with the edge terms unfused (identical bits whenever the fused form is
-// exact); passes are separated by __syncthreads.
+// exact).  The visit runs out of shared memory: the input array, the first
+// output array (its Dirichlet faces are resident, engine face states) and
+// the source are staged whole (<= 3 x 58 KB); pass p reads one staged array
+// and writes the other (with its mirror ghosts), so only the first touch of
+// each array waits for L2; every pass output and du also go to global memory
+// as before.  Passes are separated by barriers.
 // ---------------------------------------------------------------------------
 template <int DIM, bool SIG, bool HAS_A>
 __global__ void __launch_bounds__(kSmallThreads) k_relax_small(SmallPasses sp, ExtLay L, int3 lo, int3 hi,
-                                                               RelaxConst rc, int* flag) {
+                                                               RelaxConst rc, int* flag, int next) {
     pdl_begin();
+    extern __shared__ __align__(16) double sm[];
+    double* X = sm;             // pass input of even passes (the visit's input array)
+    double* Y = sm + next;      // first output array
+    double* G = sm + 2 * next;  // source
+    for (int e = threadIdx.x; e < next; e += blockDim.x) {
+        X[e] = sp.in[0][e];
+        Y[e] = sp.out[0][e];
+        G[e] = sp.g[e];
+    }
+    __syncthreads();
     const int nx = hi.x - lo.x + 1, ny = hi.y - lo.y + 1, nz = DIM == 3 ? hi.z - lo.z + 1 : 1;
     const int total = nx * ny * nz;
     const ptrdiff_t sy = L.Px, sz = DIM == 3 ? (ptrdiff_t)L.plane : 0;
     for (int p = 0; p < sp.count; ++p) {
-        const double* __restrict__ u = sp.in[p];
+        const double* __restrict__ u = (p & 1) ? Y : X;
+        double* __restrict__ so = (p & 1) ? X : Y;
         double* __restrict__ o = sp.out[p];
         double* __restrict__ du = sp.du[p];
         double dmax = 0.0;
@@ -620,7 +636,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_relax_small(SmallPasses sp, E
                         acc = acc + stencil_t<SIG>(sbar, u[pos + d], uc, l2);
                     }
             const double op = (acc * rc.pref) * rc.inv_s2;
-            const double gc = sp.g[pos];
+            const double gc = G[pos];
             const double diag = HAS_A ? fabs((op + rc.a * uc) - gc) : fabs(op - gc);
             double value;
             if (SIG) {
@@ -638,6 +654,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_relax_small(SmallPasses sp, E
             const unsigned ex = (unsigned)__double2hiint(value) & 0x7ff00000u;
             bad |= ex == 0x7ff00000u;
             tiny |= ex < 0x03600000u;
+            store_ext<DIM>(so, L, i, j, k, value);
             store_ext<DIM>(o, L, i, j, k, value);
             if (du) du[pos] = value - uc;
         }
@@ -683,7 +700,17 @@ void launch_relax_small(int dim, bool sig, const SmallPasses& sp, const ExtLay& 
                         const RelaxConst& rc, int* flag, cudaStream_t s) {
     const int3 lo = make_int3(rg.lo[0], rg.lo[1], rg.lo[2]);
     const int3 hi = make_int3(rg.hi[0], rg.hi[1], rg.hi[2]);
-#define SGML_SMALL(DD, SS, AA) launch_pdl(k_relax_small<DD, SS, AA>, dim3(1), dim3(kSmallThreads), 0, s, sp, L, lo, hi, rc, flag)
+    const int next = (int)ext_size(dim, L);  // doubles per staged array
+    const size_t bytes = 3 * (size_t)next * sizeof(double);
+#define SGML_SMALL(DD, SS, AA)                                                                                   \
+    do {                                                                                                        \
+        static bool configured = false;                                                                         \
+        if (!configured) {                                                                                      \
+            cudaFuncSetAttribute(k_relax_small<DD, SS, AA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallSmem); \
+            configured = true;                                                                                  \
+        }                                                                                                       \
+        launch_pdl(k_relax_small<DD, SS, AA>, dim3(1), dim3(kSmallThreads), bytes, s, sp, L, lo, hi, rc, flag, next); \
+    } while (0)
     if (dim == 2) {
         if (sig) { if (rc.has_a) SGML_SMALL(2, true, true); else SGML_SMALL(2, true, false); }
         else { if (rc.has_a) SGML_SMALL(2, false, true); else SGML_SMALL(2, false, false); }
