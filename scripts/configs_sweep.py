@@ -84,6 +84,8 @@ CONFIGS = [
     ("C4 3D trifoil psi_z 513^3", "trifoil_z", 9, None),
     ("3D Poisson 513^3 (bench workload)", "poisson3d", 9, None),
     ("3D Poisson 1025^3 (north-star size, 1 GPU)", "poisson3d", 10, None),
+    ("C5 3D capacitor high 257^3 (sigma)", "capacitor_high", 8, None),
+    ("C5 3D capacitor low 257^3 (sigma)", "capacitor_low", 8, None),
     ("C5 3D capacitor high 1025^3 (sigma)", "capacitor_high", 10, 7),
     ("C5 3D capacitor low 1025^3 (sigma)", "capacitor_low", 10, 7),
 ]
