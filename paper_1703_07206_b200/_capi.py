@@ -34,7 +34,7 @@ class SolverCfg(C.Structure):
 class SolverOpts(C.Structure):
     _fields_ = [("engine", C.c_int), ("use_graph", C.c_int), ("timing", C.c_int),
                 ("timing_classes", C.c_int), ("stencil", C.c_int), ("small_levels", C.c_int),
-                ("replicate_n", C.c_int)]
+                ("cluster_levels", C.c_int), ("replicate_n", C.c_int)]
 
 
 class CycleRecord(C.Structure):

@@ -476,6 +476,7 @@ class SolverOptions:
     timing_classes: int = 0     # 0: time every kernel class; else a mask of 1 << class index
     stencil: str = "radial"     # "radial" (the reference's) or "compact" 5/7-point (no reference)
     small_levels: bool = True   # one CTA per visit of a small level array (else one launch per pass)
+    cluster_levels: bool = True  # small-level operations batched into cluster launches (single GPU)
     replicate_n: int = 0        # z-slab solves: replicate levels of <= this many nodes per axis (0: 65)
 
     def to_c(self) -> _capi.SolverOpts:
@@ -484,7 +485,7 @@ class SolverOptions:
         return _capi.SolverOpts(0 if self.engine == "compact" else 1, 1 if self.use_graph else -1,
                                 int(self.timing), int(self.timing_classes),
                                 0 if self.stencil == "radial" else 1, 0 if self.small_levels else -1,
-                                int(self.replicate_n))
+                                0 if self.cluster_levels else -1, int(self.replicate_n))
 
 
 @dataclass

@@ -398,6 +398,18 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
                 Lv[v] = make_ext(dim, Nl[v]);
             }
         }
+        // the small-level interpreter's levels: arrays of at most kClusterNodes
+        // nodes (3D <= 17^3, 2D <= 65^2; measured: with larger levels the 16
+        // SMs of one cluster run them slower than full-GPU kernels do).
+        // SGML_KOP_NODES overrides the bound (A/B and the parity suite).
+        kop_ok.assign(n, 0);
+        const char* kn = std::getenv("SGML_KOP_NODES");
+        const double kop_max = kn ? std::atof(kn) : (double)kClusterNodes;
+        for (int v = 0; v < n; ++v) {
+            double nodes = 1.0;
+            for (int d = 0; d < dim; ++d) nodes *= Nl[v];
+            kop_ok[v] = nodes <= kop_max ? 1 : 0;
+        }
         // nodes off the Dirichlet faces, per level (local z indices); face values
         rng.assign(n, NodeRange{});
         for (int v = 0; v < n; ++v)
@@ -525,9 +537,17 @@ void sgml_solver::set_faces(double* p, int level, int st) {
     // DU arrays: data nodes only (their ghost cells stay 0, the past-the-end
     // corner reads of the interpolation)
     const bool mirrors = std::find(du_bufs.begin(), du_bufs.end(), p) == du_bufs.end();
-    launch(SGML_CLASS_OTHER, [&] {
-        launch_dirichlet_faces(g.dim, p, Lv[level], bc, st == FS_ZERO, mirrors, ctx->stream);
-    });
+    if (kop_level(level)) {
+        KOp op{};
+        op.kind = KOP_FACES;
+        op.level = level;
+        op.fc = KOpFaces{p, Lv[level], st == FS_ZERO ? 1 : 0, mirrors ? 1 : 0};
+        record(op);
+    } else {
+        launch(SGML_CLASS_OTHER, [&] {
+            launch_dirichlet_faces(g.dim, p, Lv[level], bc, st == FS_ZERO, mirrors, ctx->stream);
+        });
+    }
     fstate[p] = st;
 }
 
@@ -598,8 +618,33 @@ void sgml_solver::pyramid_step(const double* in, int m, double* out) {
         own_planes(m + 1, rank, kb, cnt);
         launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid_ext(dim, in, Lv[m], out, Lv[m + 1], s, kb, kb + cnt); });
         gather_level(out, m + 1);
+    } else if (kop_level(m + 1)) {
+        KOp op{};
+        op.kind = KOP_PYRAMID;
+        op.level = m + 1;
+        op.py = KOpPyramid{in, out, Lv[m], Lv[m + 1]};
+        record(op);
     } else {
         launch(SGML_CLASS_PYRAMID, [&] { launch_pyramid_ext(dim, in, Lv[m], out, Lv[m + 1], s); });
+    }
+}
+
+// the recorded small-level operations as one cluster launch per batch
+void sgml_solver::flush_kops() {
+    if (kops.empty()) return;
+    std::vector<KOp> ops;
+    ops.swap(kops);
+    if (!kop_batch) kop_batch = std::make_unique<KOpBatch>();  // (~29 KB: passed by value as kernel parameters)
+    KOpBatch& b = *kop_batch;
+    b.bc = bc;
+    b.flag = d_flag;
+    b.homogeneous = cyc_homog ? 1 : 0;
+    b.sig = has_sigma ? 1 : 0;
+    for (int v = 0; v < g.n && v < 14; ++v) b.rc[v] = relax_const(g.dim, v, g.h, a, cfg.safety, cyc_homog, opts.stencil);
+    for (size_t i0 = 0; i0 < ops.size(); i0 += kMaxKOps) {
+        b.count = (int)std::min<size_t>(kMaxKOps, ops.size() - i0);
+        std::copy(ops.begin() + (long)i0, ops.begin() + (long)i0 + b.count, b.op);
+        launch(SGML_CLASS_RELAX_COARSE, [&] { launch_kop_batch(g.dim, b, ctx->stream); });
     }
 }
 
@@ -867,6 +912,12 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
     const uint64_t E0 = ext_size(dim, Lv[0]);
     unsigned long long* diag = d_cycle;
     int* flag = d_flag;
+    // operations on small level arrays are recorded and run as cluster batches
+    // (interp.cu; single GPU, outside failure re-runs)
+    static const bool no_kops = std::getenv("SGML_NO_CLUSTER_LEVELS") != nullptr;
+    flush_kops();
+    kops_cycle = !no_kops && opts.cluster_levels >= 0 && nrk == 1 && !diag_mode;
+    cyc_homog = homogeneous;
 
     // a non-finite Dirichlet value makes the first pass throw
     // (kernels.cpp:228, 343-346); the kernels never write face nodes
@@ -905,9 +956,76 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
             halo(dst, w);
         }
     };
+    // a materialisation into level w: recorded for small levels, else launched
+    // (z-slab levels with their halo exchange)
+    auto materialize = [&](double* dst, int w, const double* bp, const ExtLay& bl, int wb, const double* uf,
+                           const ExtLay& Lf, int frel, const ChainEntry* ch, int count) {
+        if (kop_level(w)) {
+            KOp op{};
+            op.kind = KOP_MATERIALIZE;
+            op.level = w;
+            KOpMaterialize& m = op.mt;
+            m.out = dst;
+            m.base = bp;
+            m.ufine = uf;
+            m.chain = ch;
+            m.Lw = Lv[w];
+            m.L0 = bl;
+            m.Lf = Lf;
+            m.w = w;
+            m.wb = wb;
+            m.base_zero = base_zero ? 1 : 0;
+            m.frel = frel;
+            m.nchain = count;
+            materialize_grid(dim, Lv[w], bc, m.gx, m.gy, m.gz, m.xtail);
+            record(op);
+            return;
+        }
+        mat_halo(dst, w, [&](int kb, int ke) {
+            launch(SGML_CLASS_MATERIALIZE, [&] {
+                launch_materialize4(dim, dst, Lv[w], w, bp, bl, wb, base_zero, uf, Lf, frel, ch, count, bc,
+                                    homogeneous, flag, diag_mode, s, kb, ke);
+            });
+        });
+    };
     auto relax_level = [&](int v, double* in, int c, double* p0, double* p1) -> double* {
         const RelaxConst rc = relax_const(dim, v, g.h, a, cfg.safety, homogeneous, opts.stencil);
         double* cur = in;
+        if (kop_level(v)) {  // recorded passes (small-level interpreter)
+            for (int p = 1; p <= c; ++p) {
+                double* out = cur == p0 ? p1 : p0;
+                double* duo = (v > 0 && p < c) ? DU[v][p - 1] : nullptr;
+                const int want = face_want(homogeneous), ins = faces_of(cur);
+                set_faces(out, v, want);
+                if (duo) {
+                    if (ins == want) set_faces(duo, v, FS_ZERO);
+                    else if (ins == FS_ZERO && want == FS_BVAL) set_faces(duo, v, FS_BVAL);
+                    else fail(SGML_ELOGIC, "relax: input faces out of step");
+                }
+                KOp op{};
+                op.kind = KOP_RELAX;
+                op.level = v;
+                KOpRelax& x = op.rx;
+                x.in = cur;
+                x.out = out;
+                x.du = duo;
+                x.g = gsrc(v);
+                x.sig = has_sigma ? S[v] : nullptr;
+                x.dt = has_sigma ? DT[v] : nullptr;
+                x.slot = diag + slot;
+                x.L = Lv[v];
+                for (int d = 0; d < 3; ++d) {
+                    x.lo[d] = rng[v].lo[d];
+                    x.hi[d] = rng[v].hi[d];
+                }
+                x.pass_slot = slot;
+                record(op);
+                ++slot;
+                cur = out;
+                first = false;
+            }
+            return cur;
+        }
         // small level array, faces already what every pass needs: all c
         // passes in one CTA (one launch instead of c)
         if (small_visit(v, in, c, p0, p1, homogeneous)) {
@@ -1006,18 +1124,22 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
         for (int v = v1; v >= 1; --v) {
             double* in = U[v][0];
             if (first) {
-                SGML_CUDA(cudaMemsetAsync(in, 0, ext_size(dim, Lv[v]) * sizeof(double), s));
+                if (kop_level(v)) {
+                    KOp op{};
+                    op.kind = KOP_MEMSET;
+                    op.level = v;
+                    op.ms = KOpMemset{in, (long long)ext_size(dim, Lv[v])};
+                    record(op);
+                } else {
+                    flush_kops();
+                    SGML_CUDA(cudaMemsetAsync(in, 0, ext_size(dim, Lv[v]) * sizeof(double), s));
+                }
                 fstate[in] = FS_ZERO;
             } else {
                 if (count > 0 && count + (c - 1) > kMaxChain) {
                     // fold the pending increments into a full-grid base
                     const ChainEntry* ch = chain_at();
-                    mat_halo(other, 0, [&](int kb, int ke) {
-                        launch(SGML_CLASS_MATERIALIZE, [&] {
-                            launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lv[v + 1],
-                                                v + 1, ch, count, bc, homogeneous, flag, diag_mode, s, kb, ke);
-                        });
-                    });
+                    materialize(other, 0, base, Lv[0], 0, ufinal, Lv[v + 1], v + 1, ch, count);
                     fstate[other] = face_want(homogeneous);
                     bs_valid = false;
                     std::swap(base, other);
@@ -1032,12 +1154,7 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
                 ExtLay bl;
                 int wb;
                 base_src(v, bp, bl, wb);
-                mat_halo(in, v, [&](int kb, int ke) {
-                    launch(SGML_CLASS_MATERIALIZE, [&] {
-                        launch_materialize4(dim, in, Lv[v], v, bp, bl, wb, base_zero, ufinal, Lf, 1, ch, count,
-                                            bc, homogeneous, flag, diag_mode, s, kb, ke);
-                    });
-                });
+                materialize(in, v, bp, bl, wb, ufinal, Lf, 1, ch, count);
                 fstate[in] = face_want(homogeneous);
             }
             ufinal = relax_level(v, in, c, U[v][0], U[v][1]);
@@ -1046,18 +1163,22 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
         // level 0 visit of this tooth
         double* in0;
         if (first) {
-            SGML_CUDA(cudaMemsetAsync(base, 0, E0 * sizeof(double), s));
+            if (kop_level(0)) {
+                KOp op{};
+                op.kind = KOP_MEMSET;
+                op.level = 0;
+                op.ms = KOpMemset{base, (long long)E0};
+                record(op);
+            } else {
+                flush_kops();
+                SGML_CUDA(cudaMemsetAsync(base, 0, E0 * sizeof(double), s));
+            }
             fstate[base] = FS_ZERO;
             in0 = base;
         } else if (v1 >= 1) {
             const ChainEntry* ch = chain_at();
             const ExtLay Lf = n > 1 ? Lv[1] : Lv[0];
-            mat_halo(other, 0, [&](int kb, int ke) {
-                launch(SGML_CLASS_MATERIALIZE, [&] {
-                    launch_materialize4(dim, other, Lv[0], 0, base, Lv[0], 0, base_zero, ufinal, Lf, 1, ch, count,
-                                        bc, homogeneous, flag, diag_mode, s, kb, ke);
-                });
-            });
+            materialize(other, 0, base, Lv[0], 0, ufinal, Lf, 1, ch, count);
             fstate[other] = face_want(homogeneous);
             in0 = other;
         } else {
@@ -1070,6 +1191,8 @@ const double* sgml_solver::cycle_compact(bool homogeneous) {
     }
     // tail Relax(0, min(n_r, 2^n))
     base = relax_level(0, base, relax_count(n, cfg.n_r, 0), A, B);
+    flush_kops();
+    kops_cycle = false;
     return base;
 }
 

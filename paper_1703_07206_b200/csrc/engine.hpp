@@ -192,6 +192,7 @@ struct sgml_solver {
     void check_launch(int cls);
     template <typename F>
     void launch(int cls, F&& fn) {
+        flush_kops();  // recorded small-level operations run before anything launched after them
         ++launches;
         if (debug_sync < 0) debug_sync = std::getenv("SGML_DEBUG_SYNC") ? 1 : 0;
         if (debug_sync) {
@@ -229,6 +230,17 @@ struct sgml_solver {
     bool slab_graphs_off = false;         // a z-slab capture failed on some rank: eager cycles
     bool use_graphs() const;
     bool small_visit(int v, const double* in, int c, const double* p0, const double* p1, bool homogeneous) const;
+    // small-level interpreter (interp.cu): operations on level arrays of at
+    // most kClusterNodes nodes are recorded during a cycle and run by one cluster
+    // launch per batch (single GPU, compact engine, outside failure re-runs)
+    std::vector<sgmlb::KOp> kops;
+    bool kops_cycle = false;   // this cycle records small-level operations
+    bool cyc_homog = false;    // the cycle's homogeneous flag (relaxation constants of a batch)
+    bool kop_level(int v) const { return kops_cycle && v < (int)kop_ok.size() && kop_ok[v]; }
+    std::vector<char> kop_ok;  // level v's array is small enough
+    std::unique_ptr<sgmlb::KOpBatch> kop_batch;
+    void flush_kops();
+    void record(const sgmlb::KOp& op) { kops.push_back(op); }
     const double* cycle_graph(bool homogeneous);
     cudaEvent_t next_event();
     void harvest_spans();  // call after a stream synchronize

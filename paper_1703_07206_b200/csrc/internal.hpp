@@ -147,6 +147,79 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
                          const ExtLay& L0, int wb, bool base_zero, const double* ufine, const ExtLay& Lf,
                          int frel, const ChainEntry* chain, int nchain, const BcDev& bc,
                          bool homogeneous, int* flag, bool diag, cudaStream_t s, int kb = 0, int ke = -1);
+// ---- small-level interpreter (interp.cu) -------------------------------------
+// The operations of a cycle on small level arrays (coarse levels of large
+// grids; whole cycles of small ones) recorded by the engine and executed
+// in order by ONE launch of a thread-block cluster, with a cluster barrier
+// between operations, instead of one kernel each.  Same per-node arithmetic
+// as the kernels they replace.
+enum KOpKind : int { KOP_MEMSET = 0, KOP_FACES = 1, KOP_PYRAMID = 2, KOP_MATERIALIZE = 3, KOP_RELAX = 4 };
+struct KOpMemset {
+    double* p;
+    long long count;
+};
+struct KOpFaces {  // k_dirichlet_faces
+    double* a;
+    ExtLay L;
+    int zero, mirrors;
+};
+struct KOpPyramid {  // k_pyramid_ext: level m -> m + 1
+    const double* in;
+    double* out;
+    ExtLay Lin, Lout;
+};
+struct KOpMaterialize {  // k_materialize4 (no diagnostic mode)
+    double* out;
+    const double* base;
+    const double* ufine;
+    const ChainEntry* chain;
+    ExtLay Lw, L0, Lf;
+    int w, wb, base_zero, frel, nchain, xtail, gx, gy, gz;
+};
+struct KOpRelax {  // one relaxation pass over a level array (k_relax_small's per-node arithmetic)
+    const double* in;
+    double* out;
+    double* du;
+    const double* g;
+    const double* sig;
+    const double* dt;
+    unsigned long long* slot;
+    ExtLay L;
+    int lo[3], hi[3];
+    int pass_slot;
+};
+struct KOp {
+    int kind;
+    int level;
+    union {
+        KOpMemset ms;
+        KOpFaces fc;
+        KOpPyramid py;
+        KOpMaterialize mt;
+        KOpRelax rx;
+    };
+};
+// one launch: the operations share the cycle's boundary set, relaxation
+// constants per level and flags; kernel parameters are limited to 32 KB
+constexpr int kMaxKOps = 160;
+struct KOpBatch {
+    BcDev bc;
+    int* flag;
+    int homogeneous;
+    int count;
+    int sig;
+    RelaxConst rc[14];  // per level
+    KOp op[kMaxKOps];
+};
+// level arrays of at most this many nodes are interpreted
+constexpr int kClusterNodes = 5000;
+// cluster of CTAs that runs a batch (16 where the device allows it, else 8)
+int interp_cluster_size();
+// the launch geometry launch_materialize4 uses for a whole level array
+// (virtual grid of the interpreter's materialisation)
+void materialize_grid(int dim, const ExtLay& Lw, const BcDev& bc, int& gx, int& gy, int& gz, int& xtail);
+void launch_kop_batch(int dim, const KOpBatch& b, cudaStream_t s);
+
 // per-node pseudo-time step of the sigma relaxation at every node of a level
 // array (own planes), from the level's sigma (with ghosts / halos)
 void launch_dtau_ext(int dim, const double* sig, const ExtLay& L, double* dt, const RelaxConst& rc, cudaStream_t s);

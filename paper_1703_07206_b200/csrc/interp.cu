@@ -1,0 +1,259 @@
+// interp.cu — the small-level interpreter: one thread-block cluster runs a
+// batch of recorded level-array operations (internal.hpp KOp) in order, with
+// a cluster barrier (release / acquire) between operations.
+//
+// Why: on a small level array an operation is a few microseconds of work and
+// its kernel is launch- and latency-bound (a C1 129^2 cycle is 70 such
+// kernels).  A cluster of 16 CTAs x 512 threads keeps the arrays hot in L2
+// and replaces each launch by a hardware barrier.  Measured (B200): an
+// interpreted operation costs ~2 us (L2 round trips + the barrier), so the
+// engine interprets the levels of <= kClusterNodes nodes (3D <= 17^3, 2D <=
+// 65^2), where that beats a kernel; larger levels run faster as full-GPU
+// kernels than on the 16 SMs of one cluster (C1 129^2: 4.35 -> 4.11 ms,
+// 3D 65^3: 6.39 -> 5.72 ms per solve; SGML_KOP_NODES for A/B).
+//
+// Per-node arithmetic is exactly that of the kernels the operations replace:
+// relaxation passes follow k_relax_small (the reference's relax branch,
+// kernels.cpp:94-137, edge terms unfused), materialisations run
+// k_materialize4's body (level_ops.cuh), pyramid steps and Dirichlet faces
+// follow k_pyramid_ext and k_dirichlet_faces.  Data written by an earlier
+// operation of the batch is read with coherent loads (never .nc).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+#include "internal.hpp"
+#include "level_ops.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace sgmlb {
+
+namespace {
+
+constexpr int kIThreads = 512;  // threads per CTA (4 virtual 128-thread blocks)
+
+__device__ __forceinline__ double axw(int o) { return o == 0 ? 0.5 : 0.25; }
+
+template <int DIM>
+__device__ void op_faces(const KOpFaces& o, const BcDev& bc, long long gtid, long long gthreads) {
+    const ExtLay& L = o.L;
+    const int N = L.N;
+    const long long per_face = (long long)N * (DIM == 3 ? N : 1);
+    for (long long e = gtid; e < per_face * 2 * DIM; e += gthreads) {
+        const int f = (int)(e / per_face);
+        const long long r = e - (long long)f * per_face;
+        const int p = (int)(r % N), q = (int)(r / N);
+        if (bc.neu[f]) continue;
+        const int side = (f & 1) ? N - 1 : 0;
+        int i, j, kg = 0;
+        if (DIM == 2) {
+            if (f < 2) { i = side; j = p; }
+            else { i = p; j = side; }
+        } else if (f < 4) {
+            if (q >= L.Nz) continue;
+            kg = q + L.z0;
+            if (f < 2) { i = side; j = p; }
+            else { i = p; j = side; }
+        } else {
+            if (side < L.z0 || side >= L.z0 + L.Nz) continue;
+            i = p; j = q; kg = side;
+        }
+        const double v = o.zero ? 0.0 : dirichlet_value<DIM>(bc, N, i, j, kg);
+        const int k = DIM == 3 ? kg - L.z0 : 0;
+        if (o.mirrors) store_ext<DIM>(o.a, L, i, j, k, v);
+        else o.a[eix<DIM>(L, i, j, k)] = v;
+    }
+}
+
+template <int DIM>
+__device__ void op_pyramid(const KOpPyramid& o, long long gtid, long long gthreads) {
+    const ExtLay &Lin = o.Lin, &Lout = o.Lout;
+    const int Nout = Lout.N;
+    const long long total = (long long)Nout * Nout * (DIM == 3 ? Lout.Nz : 1);
+    const ptrdiff_t sy = Lin.Px, sz = (ptrdiff_t)Lin.Px * Lin.Ne;
+    for (long long e = gtid; e < total; e += gthreads) {
+        const int I = (int)(e % Nout), J = (int)((e / Nout) % Nout), K = DIM == 3 ? (int)(e / ((long long)Nout * Nout)) : 0;
+        const int Kin = DIM == 3 ? 2 * (K + Lout.z0) - Lin.z0 : 0;
+        const double* c = o.in + eix<DIM>(Lin, 2 * I, 2 * J, Kin);
+        double acc = 0.0;
+#pragma unroll
+        for (int r = (DIM == 3 ? -1 : 0); r <= (DIM == 3 ? 1 : 0); ++r)
+#pragma unroll
+            for (int q = -1; q <= 1; ++q)
+#pragma unroll
+                for (int p = -1; p <= 1; ++p) {
+                    const double w = DIM == 3 ? (axw(p) * axw(q)) * axw(r) : axw(p) * axw(q);
+                    acc = acc + w * c[r * sz + q * sy + p];
+                }
+        store_ext<DIM>(o.out, Lout, I, J, K, acc);
+    }
+}
+
+// one relaxation pass (k_relax_small's per-node arithmetic); diag max and
+// the flags through the CTA, then atomics
+template <int DIM, bool SIG, bool HAS_A>
+__device__ void op_relax(const KOpRelax& o, const RelaxConst& rc, int* flag, long long gtid, long long gthreads) {
+    const ExtLay& L = o.L;
+    const int nx = o.hi[0] - o.lo[0] + 1, ny = o.hi[1] - o.lo[1] + 1, nz = DIM == 3 ? o.hi[2] - o.lo[2] + 1 : 1;
+    const long long total = (nx > 0 && ny > 0 && nz > 0) ? (long long)nx * ny * nz : 0;
+    const ptrdiff_t sy = L.Px, sz = DIM == 3 ? (ptrdiff_t)L.plane : 0;
+    const double* __restrict__ u = o.in;
+    double dmax = 0.0;
+    int bad = 0, tiny = 0;
+    for (long long e = gtid; e < total; e += gthreads) {
+        const int i = o.lo[0] + (int)(e % nx), j = o.lo[1] + (int)((e / nx) % ny);
+        const int k = DIM == 3 ? o.lo[2] + (int)(e / ((long long)nx * ny)) : 0;
+        const ptrdiff_t pos = eix<DIM>(L, i, j, k);
+        const double uc = u[pos];
+        const double sc = SIG ? o.sig[pos] : 1.0;
+        double acc = 0.0;
+#pragma unroll
+        for (int r = (DIM == 3 ? -1 : 0); r <= (DIM == 3 ? 1 : 0); ++r)
+#pragma unroll
+            for (int q = -1; q <= 1; ++q)
+#pragma unroll
+                for (int pp = -1; pp <= 1; ++pp) {
+                    if (r == 0 && q == 0 && pp == 0) continue;
+                    const int l2 = r * r + q * q + pp * pp;
+                    if (stencil_skip(rc.compact, l2)) continue;
+                    const ptrdiff_t d = r * sz + q * sy + pp;
+                    const double sbar = SIG ? 0.5 * (o.sig[pos + d] + sc) : 1.0;
+                    acc = acc + stencil_t<SIG>(sbar, u[pos + d], uc, l2);
+                }
+        const double op = (acc * rc.pref) * rc.inv_s2;
+        const double gc = o.g[pos];
+        const double diag = HAS_A ? fabs((op + rc.a * uc) - gc) : fabs(op - gc);
+        double value;
+        if (SIG) {
+            const double dtau = o.dt[pos];
+            if (!(dtau > 0.0)) value = __longlong_as_double(0x7ff8000000000000LL);
+            else {
+                const double num = uc + dtau * (op - gc);
+                value = HAS_A ? num / (1.0 - dtau * rc.a) : num;
+            }
+        } else {
+            const double num = uc + rc.dtau1 * (op - gc);
+            value = HAS_A ? num / rc.denom1 : num;
+        }
+        dmax = dmax < diag ? diag : dmax;
+        const unsigned ex = (unsigned)__double2hiint(value) & 0x7ff00000u;
+        bad |= ex == 0x7ff00000u;
+        tiny |= ex < 0x03600000u;
+        store_ext<DIM>(o.out, L, i, j, k, value);
+        if (o.du) o.du[pos] = value - uc;
+    }
+    block_max_commit(dmax, o.slot);
+    block_bad_commit(bad, flag, o.pass_slot);
+    block_or_commit(tiny, flag + 1);
+}
+
+__device__ __forceinline__ void cluster_barrier() {
+    __threadfence();
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(kIThreads, 1) k_kop_batch(const __grid_constant__ KOpBatch b) {
+    __shared__ ChainEntry sch[kMaxChain];
+    pdl_begin();
+    const unsigned crank = cg::this_cluster().block_rank();
+    const unsigned csize = cg::this_cluster().num_blocks();
+    const long long gthreads = (long long)csize * kIThreads;
+    const long long gtid = (long long)crank * kIThreads + threadIdx.x;
+    const int sub = threadIdx.x / (MBX * MBY);                  // virtual 128-thread block of this CTA
+    const int vtx = threadIdx.x % MBX, vty = (threadIdx.x / MBX) % MBY;
+    const int vstride = (int)csize * (kIThreads / (MBX * MBY));
+    for (int i = 0; i < b.count; ++i) {
+        const KOp& op = b.op[i];
+        switch (op.kind) {
+            case KOP_MEMSET:
+                for (long long e = gtid; e < op.ms.count; e += gthreads) op.ms.p[e] = 0.0;
+                break;
+            case KOP_FACES:
+                op_faces<DIM>(op.fc, b.bc, gtid, gthreads);
+                break;
+            case KOP_PYRAMID:
+                op_pyramid<DIM>(op.py, gtid, gthreads);
+                break;
+            case KOP_MATERIALIZE: {
+                const KOpMaterialize& m = op.mt;
+                const int nsh = min(m.nchain, kMaxChain);
+                for (int c = threadIdx.x; c < nsh; c += kIThreads) sch[c] = m.chain[c];
+                __syncthreads();
+                const int nvb = m.gx * m.gy * m.gz;
+                for (int vb = (int)crank * (kIThreads / (MBX * MBY)) + sub; vb < nvb; vb += vstride) {
+                    const int bx = vb % m.gx, by = (vb / m.gx) % m.gy, bz = vb / (m.gx * m.gy);
+                    mat4_body<DIM, 2, false, false>(m.out, m.Lw, m.w, m.base, m.L0, m.wb, m.base_zero, m.ufine,
+                                                    m.Lf, m.frel, m.chain, m.nchain, sch, b.bc, b.homogeneous,
+                                                    b.flag, m.xtail, 0, bx, by, bz, vtx, vty);
+                }
+                __syncthreads();  // sch is reused by the next materialisation
+                break;
+            }
+            case KOP_RELAX: {
+                const RelaxConst& rc = b.rc[op.level];
+                if (b.sig) {
+                    if (rc.has_a) op_relax<DIM, true, true>(op.rx, rc, b.flag, gtid, gthreads);
+                    else op_relax<DIM, true, false>(op.rx, rc, b.flag, gtid, gthreads);
+                } else {
+                    if (rc.has_a) op_relax<DIM, false, true>(op.rx, rc, b.flag, gtid, gthreads);
+                    else op_relax<DIM, false, false>(op.rx, rc, b.flag, gtid, gthreads);
+                }
+                break;
+            }
+            default:
+                break;
+        }
+        cluster_barrier();
+    }
+}
+
+int g_cluster = 0;
+
+}  // namespace
+
+int interp_cluster_size() {
+    if (g_cluster) return g_cluster;
+    int best = 8;
+    if (cudaFuncSetAttribute(k_kop_batch<3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+        cudaFuncSetAttribute(k_kop_batch<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(16);
+        cfg.blockDim = dim3(kIThreads);
+        cudaLaunchAttribute a[1];
+        a[0].id = cudaLaunchAttributeClusterDimension;
+        a[0].val.clusterDim.x = 16;
+        a[0].val.clusterDim.y = 1;
+        a[0].val.clusterDim.z = 1;
+        cfg.attrs = a;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_kop_batch<3>, &cfg) == cudaSuccess && n > 0) best = 16;
+    }
+    (void)cudaGetLastError();
+    g_cluster = best;
+    return best;
+}
+
+void launch_kop_batch(int dim, const KOpBatch& b, cudaStream_t s) {
+    const int cs = interp_cluster_size();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kIThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute a[2];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = cs;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    a[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = a;
+    cfg.numAttrs = 2;
+    if (dim == 2) cudaLaunchKernelEx(&cfg, k_kop_batch<2>, b);
+    else cudaLaunchKernelEx(&cfg, k_kop_batch<3>, b);
+}
+
+}  // namespace sgmlb

@@ -31,13 +31,22 @@ def dev(g, arr):
 
 
 # engine variants: the compact engine with and without the one-CTA
-# small-level path (SolverOptions.small_levels), and the literal engine
-ENGINES = ["compact", "compact-nosmall", "literal"]
+# small-level path (SolverOptions.small_levels) and the small-level cluster
+# interpreter (cluster_levels; "compact-kopall": interpreted up to 65^3-node
+# levels, SGML_KOP_NODES), and the literal engine
+ENGINES = ["compact", "compact-nosmall", "compact-nocluster", "compact-kopall", "literal"]
+
+
+@pytest.fixture(autouse=True)
+def _kop_env(request, monkeypatch):
+    if "compact-kopall" in request.node.name:
+        monkeypatch.setenv("SGML_KOP_NODES", str(65 ** 3))
 
 
 def opts(engine):
     return S.SolverOptions(engine="literal" if engine == "literal" else "compact",
-                           small_levels=engine != "compact-nosmall")
+                           small_levels=engine != "compact-nosmall",
+                           cluster_levels=engine not in ("compact-nosmall", "compact-nocluster"))
 
 
 @pytest.fixture(scope="module", autouse=True)
