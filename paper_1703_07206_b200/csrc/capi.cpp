@@ -720,7 +720,6 @@ int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f
         require(ctx && bc && f_host && cfg && rep, SGML_EINVAL, "solve: null argument");
         const sgml_grid g = make_grid_or_throw(dim, n);
         activate(ctx);
-        const cudaStream_t s = ctx->stream;
         check_solve_args(cfg);
         sgml_solver_opts o{};
         if (opts) o = *opts;
@@ -730,7 +729,7 @@ int sgml_solve(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* f
         copy_h2d(ctx, sv->fin, f_host, bytes);  // (pageable sources at pinned speed)
         sv->run(sv->fin, nullptr, rep);
         if (u_host_out) copy_d2h(ctx, u_host_out, sv->result(), bytes);
-        SGML_CUDA(cudaStreamSynchronize(s));
+        SGML_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
 
