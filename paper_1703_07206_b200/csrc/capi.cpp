@@ -669,7 +669,6 @@ namespace {
 sgml_solver* cached_solver(sgml_ctx* ctx, int dim, int n, const sgml_bc* bc, const double* sigma_host, double a,
                            const sgml_solver_cfg* cfg, const sgml_solver_opts& o) {
     const sgml_grid g = make_grid_or_throw(dim, n);
-    const cudaStream_t s = ctx->stream;
     std::string key(reinterpret_cast<const char*>(&g), sizeof g);
     key.append(reinterpret_cast<const char*>(bc), sizeof *bc);
     key.append(reinterpret_cast<const char*>(&a), sizeof a);
