@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
     k_materialize4(double* __restrict__ out, ExtLay Lw, int w, const double* __restrict__ base,
                    ExtLay L0, int wb, int base_zero, const double* __restrict__ ufine, ExtLay Lf, int frel,
                    const ChainEntry* __restrict__ chain, int nchain, BcDev bc, int homogeneous,
-                   int* flag, int xtail, int k0) {
+                   int* flag, int xtail, int k0, int kz, int ke) {
     // the first kMaxChain entries sit in shared memory; a longer chain (a
     // single visit adding more than kMaxChain increments, n_r > kMaxChain + 1)
     // reads the rest from global memory
@@ -54,9 +54,13 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
     const int nsh = min(nchain, kMaxChain);
     for (int c = tid; c < nsh; c += MBX * MBY) sch[c] = chain[c];
     __syncthreads();
-    mat4_body<DIM, NC, DIAG, true>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, frel, chain, nchain, sch, bc,
-                                   homogeneous, flag, xtail, k0, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x,
-                                   threadIdx.y);
+    // kz planes per CTA (one chain copy, fewer CTA launches: 513^3 level 0
+    // 101 -> 95 ms per solve at kz = 4; prefetching the next plane's base
+    // values did not pay)
+    for (int bz = blockIdx.z * kz; bz < min(blockIdx.z * kz + kz, ke); ++bz)
+        mat4_body<DIM, NC, DIAG, true>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, frel, chain, nchain, sch, bc,
+                                       homogeneous, flag, xtail, k0, blockIdx.x, blockIdx.y, bz, threadIdx.x,
+                                       threadIdx.y);
 }
 
 // ---------------------------------------------------------------------------
@@ -234,10 +238,13 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
     // and the last group writes the face node (xtail)
     const int xtail = (!bc.neu[1] && (Nw - 1) % MV == 0) ? 1 : 0;
     const int threads_x = xtail ? (Nw - 1) / MV : (Nw + MV - 1) / MV, D = (Nw - 1) / NC;
-    const dim3 grid((threads_x + MBX - 1) / MBX, (D + MBY) / MBY, dim == 3 ? ke - kb : 1);
+    const int gx = (threads_x + MBX - 1) / MBX, gy = (D + MBY) / MBY, nzp = dim == 3 ? ke - kb : 1;
+    // 4 planes per CTA where that still leaves ~10 CTAs per SM (large levels)
+    const int kz = (long long)gx * gy * nzp >= 4LL * 148 * 5 * 2 ? 4 : 1;
+    const dim3 grid(gx, gy, (nzp + kz - 1) / kz);
 #define SGML_MAT(DD, CC, GG)                                                                              \
     launch_pdl(k_materialize4<DD, CC, GG>, grid, dim3(MBX, MBY), 0, s, out, Lw, w, base, L0, wb, base_zero, ufine, \
-               Lf, frel, chain, nchain, bc, homogeneous, flag, xtail, dim == 3 ? kb : 0)
+               Lf, frel, chain, nchain, bc, homogeneous, flag, xtail, dim == 3 ? kb : 0, kz, nzp)
     if (dim == 2) {
         if (diag) SGML_MAT(2, NC, true);
         else SGML_MAT(2, NC, false);

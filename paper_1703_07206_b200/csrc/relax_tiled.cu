@@ -666,16 +666,20 @@ __global__ void __launch_bounds__(kSmallThreads) k_relax_small(SmallPasses sp, E
 }
 }  // namespace
 
-// planes per CTA: long marches amortise the 2-plane prologue, short ones
-// give small levels enough CTAs (about two waves of 148 SMs x 2)
 bool pdl_enabled() {
     static const bool on = std::getenv("SGML_NO_PDL") == nullptr;
     return on;
 }
 
+// planes per CTA: long marches amortise the 2-plane prologue, short ones
+// give small levels enough CTAs (about two waves of 148 SMs x 2)
+
 int relax_tiled_zb(int dim, int cols, int nz) {
     const int target = 2 * 148 * (dim == 3 ? 2 : 4);
-    int zb = dim == 3 ? 64 : 128;
+    // 3D: 24 planes per CTA (513^3 level-0 pass measured over 8..64: 16-24
+    // best, 0.69 ms; 64: 0.72-0.75 ms — shorter marches spread the ring
+    // fills of the two co-resident CTAs better and shrink the tail wave)
+    int zb = dim == 3 ? 24 : 128;
     while (zb > 4 && (long long)cols * ((nz + zb - 1) / zb) < target) zb >>= 1;
     return zb;
 }
