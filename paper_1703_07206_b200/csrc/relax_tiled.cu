@@ -29,6 +29,7 @@
 // are summed as planes arrive (see the march); the window roles alternate
 // with period 2, so the march is unrolled two steps and no register moves
 // are issued.
+#include <algorithm>
 #include <cstdlib>
 
 #include <cuda.h>
@@ -672,15 +673,16 @@ bool pdl_enabled() {
 }
 
 // planes per CTA: long marches amortise the 2-plane prologue, short ones
-// give small levels enough CTAs (about two waves of 148 SMs x 2)
-
+// give small levels enough CTAs (2D: about two waves of 148 SMs x 4; 3D:
+// about four waves of 148 x 2 — 257^3 passes then march 12 planes, ~1 ms per
+// 513^3 solve faster than 24)
 int relax_tiled_zb(int dim, int cols, int nz) {
-    const int target = 2 * 148 * (dim == 3 ? 2 : 4);
+    const int target = (dim == 3 ? 4 : 2) * 148 * (dim == 3 ? 2 : 4);
     // 3D: 24 planes per CTA (513^3 level-0 pass measured over 8..64: 16-24
     // best, 0.69 ms; 64: 0.72-0.75 ms — shorter marches spread the ring
     // fills of the two co-resident CTAs better and shrink the tail wave)
     int zb = dim == 3 ? 24 : 128;
-    while (zb > 4 && (long long)cols * ((nz + zb - 1) / zb) < target) zb >>= 1;
+    while (zb > 4 && (long long)cols * ((nz + zb - 1) / zb) < target) zb = std::max(4, zb / 2);
     return zb;
 }
 
