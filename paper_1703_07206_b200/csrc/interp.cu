@@ -36,13 +36,13 @@ constexpr int kIThreads = 512;  // threads per CTA (4 virtual 128-thread blocks)
 __device__ __forceinline__ double axw(int o) { return o == 0 ? 0.5 : 0.25; }
 
 template <int DIM>
-__device__ void op_faces(const KOpFaces& o, const BcDev& bc, long long gtid, long long gthreads) {
+__device__ void op_faces(const KOpFaces& o, const BcDev& bc, int gtid, int gthreads) {
     const ExtLay& L = o.L;
     const int N = L.N;
-    const long long per_face = (long long)N * (DIM == 3 ? N : 1);
-    for (long long e = gtid; e < per_face * 2 * DIM; e += gthreads) {
+    const int per_face = N * (DIM == 3 ? N : 1);
+    for (int e = gtid; e < per_face * 2 * DIM; e += gthreads) {
         const int f = (int)(e / per_face);
-        const long long r = e - (long long)f * per_face;
+        const int r = e - f * per_face;
         const int p = (int)(r % N), q = (int)(r / N);
         if (bc.neu[f]) continue;
         const int side = (f & 1) ? N - 1 : 0;
@@ -67,13 +67,13 @@ __device__ void op_faces(const KOpFaces& o, const BcDev& bc, long long gtid, lon
 }
 
 template <int DIM>
-__device__ void op_pyramid(const KOpPyramid& o, long long gtid, long long gthreads) {
+__device__ void op_pyramid(const KOpPyramid& o, int gtid, int gthreads) {
     const ExtLay &Lin = o.Lin, &Lout = o.Lout;
     const int Nout = Lout.N;
-    const long long total = (long long)Nout * Nout * (DIM == 3 ? Lout.Nz : 1);
+    const int total = Nout * Nout * (DIM == 3 ? Lout.Nz : 1);
     const ptrdiff_t sy = Lin.Px, sz = (ptrdiff_t)Lin.Px * Lin.Ne;
-    for (long long e = gtid; e < total; e += gthreads) {
-        const int I = (int)(e % Nout), J = (int)((e / Nout) % Nout), K = DIM == 3 ? (int)(e / ((long long)Nout * Nout)) : 0;
+    for (int e = gtid; e < total; e += gthreads) {
+        const int I = e % Nout, J = (e / Nout) % Nout, K = DIM == 3 ? e / (Nout * Nout) : 0;
         const int Kin = DIM == 3 ? 2 * (K + Lout.z0) - Lin.z0 : 0;
         const double* c = o.in + eix<DIM>(Lin, 2 * I, 2 * J, Kin);
         double acc = 0.0;
@@ -93,17 +93,17 @@ __device__ void op_pyramid(const KOpPyramid& o, long long gtid, long long gthrea
 // one relaxation pass (k_relax_small's per-node arithmetic); diag max and
 // the flags through the CTA, then atomics
 template <int DIM, bool SIG, bool HAS_A>
-__device__ void op_relax(const KOpRelax& o, const RelaxConst& rc, int* flag, long long gtid, long long gthreads) {
+__device__ void op_relax(const KOpRelax& o, const RelaxConst& rc, int* flag, int gtid, int gthreads) {
     const ExtLay& L = o.L;
     const int nx = o.hi[0] - o.lo[0] + 1, ny = o.hi[1] - o.lo[1] + 1, nz = DIM == 3 ? o.hi[2] - o.lo[2] + 1 : 1;
-    const long long total = (nx > 0 && ny > 0 && nz > 0) ? (long long)nx * ny * nz : 0;
+    const int total = (nx > 0 && ny > 0 && nz > 0) ? nx * ny * nz : 0;
     const ptrdiff_t sy = L.Px, sz = DIM == 3 ? (ptrdiff_t)L.plane : 0;
     const double* __restrict__ u = o.in;
     double dmax = 0.0;
     int bad = 0, tiny = 0;
-    for (long long e = gtid; e < total; e += gthreads) {
-        const int i = o.lo[0] + (int)(e % nx), j = o.lo[1] + (int)((e / nx) % ny);
-        const int k = DIM == 3 ? o.lo[2] + (int)(e / ((long long)nx * ny)) : 0;
+    for (int e = gtid; e < total; e += gthreads) {
+        const int i = o.lo[0] + e % nx, j = o.lo[1] + (e / nx) % ny;
+        const int k = DIM == 3 ? o.lo[2] + e / (nx * ny) : 0;
         const ptrdiff_t pos = eix<DIM>(L, i, j, k);
         const double uc = u[pos];
         const double sc = SIG ? o.sig[pos] : 1.0;
@@ -143,9 +143,10 @@ __device__ void op_relax(const KOpRelax& o, const RelaxConst& rc, int* flag, lon
         store_ext<DIM>(o.out, L, i, j, k, value);
         if (o.du) o.du[pos] = value - uc;
     }
+    // (the flags are rare: warp-level atomics, no block barrier)
+    warp_bad_commit(bad, flag, o.pass_slot);
+    warp_or_commit(tiny, flag + 1);
     block_max_commit(dmax, o.slot);
-    block_bad_commit(bad, flag, o.pass_slot);
-    block_or_commit(tiny, flag + 1);
 }
 
 // (release / acquire at cluster scope orders the operations' global-memory
@@ -162,8 +163,9 @@ __global__ void __launch_bounds__(kIThreads, 1) k_kop_batch(const __grid_constan
     pdl_begin();
     const unsigned crank = cg::this_cluster().block_rank();
     const unsigned csize = cg::this_cluster().num_blocks();
-    const long long gthreads = (long long)csize * kIThreads;
-    const long long gtid = (long long)crank * kIThreads + threadIdx.x;
+    // (interpreted level arrays hold far fewer than 2^31 elements)
+    const int gthreads = (int)csize * kIThreads;
+    const int gtid = (int)crank * kIThreads + threadIdx.x;
     const int sub = threadIdx.x / (MBX * MBY);                  // virtual 128-thread block of this CTA
     const int vtx = threadIdx.x % MBX, vty = (threadIdx.x / MBX) % MBY;
     const int vstride = (int)csize * (kIThreads / (MBX * MBY));
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(kIThreads, 1) k_kop_batch(const __grid_constan
         const KOp& op = b.op[i];
         switch (op.kind) {
             case KOP_MEMSET:
-                for (long long e = gtid; e < op.ms.count; e += gthreads) op.ms.p[e] = 0.0;
+                for (int e = gtid; e < (int)op.ms.count; e += gthreads) op.ms.p[e] = 0.0;
                 break;
             case KOP_FACES:
                 op_faces<DIM>(op.fc, b.bc, gtid, gthreads);
