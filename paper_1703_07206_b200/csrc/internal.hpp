@@ -211,8 +211,10 @@ struct KOpBatch {
     RelaxConst rc[14];  // per level
     KOp op[kMaxKOps];
 };
-// level arrays of at most this many nodes are interpreted
+// level arrays of at most this many nodes are interpreted (and a 2D level 0
+// of at most kClusterNodes2D0)
 constexpr int kClusterNodes = 5000;
+constexpr int kClusterNodes2D0 = 129 * 129;
 // cluster of CTAs that runs a batch (16 where the device allows it, else 8)
 int interp_cluster_size();
 // the launch geometry launch_materialize4 uses for a whole level array
