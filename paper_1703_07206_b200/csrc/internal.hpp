@@ -87,7 +87,7 @@ struct TmaSet {
 // TMA box shapes of the relaxation tiles: u/sigma box (tile + halo) and
 // g/r/u_tot box (tile), {x, y, plane}.
 void tile_boxes(int dim, unsigned* box_u, unsigned* box_g);
-int relax_tiled_zb(int dim, int cols, int nz);
+int relax_tiled_zb(int dim, int cols, int nz, int per_sm);
 
 // Box of data nodes a relaxation / residual launch covers: every node not on
 // a Dirichlet face (those keep their face value, resident in the buffers).

@@ -559,7 +559,7 @@ void launch_mode(int dim, bool sig, const TmaSet& tm, double* uo, double* duo, c
     const int nxt = dim == 3 ? rg.hi[0] - (rg.lo[0] & ~1) + 1 : nx;
     const int tilesx = dim == 3 ? (nxt + Tile<3>::NX - 1) / Tile<3>::NX : (nxt + Tile<2>::NX - 1) / Tile<2>::NX;
     const int cols = dim == 3 ? tilesx * ((ny + Tile<3>::ROWS - 1) / Tile<3>::ROWS) : tilesx;
-    const int zb = relax_tiled_zb(dim, cols, dim == 3 ? nz : ny);
+    const int zb = relax_tiled_zb(dim, cols, dim == 3 ? nz : ny, dim == 3 ? (sig ? 1 : 2) : 4);
     dim3 grid, block;
     if (dim == 3) {
         using TL = Tile<3>;
@@ -673,11 +673,12 @@ bool pdl_enabled() {
 }
 
 // planes per CTA: long marches amortise the 2-plane prologue, short ones
-// give small levels enough CTAs (2D: about two waves of 148 SMs x 4; 3D:
-// about four waves of 148 x 2 — 257^3 passes then march 12 planes, ~1 ms per
-// 513^3 solve faster than 24)
-int relax_tiled_zb(int dim, int cols, int nz) {
-    const int target = (dim == 3 ? 4 : 2) * 148 * (dim == 3 ? 2 : 4);
+// give small levels enough CTAs (2D: about two waves of 148 SMs x 4 CTAs;
+// 3D: about four waves of 148 x per_sm — 257^3 passes then march 12 planes,
+// ~1 ms per 513^3 solve faster than 24; the sigma kernel, one CTA per SM,
+// keeps 24 there)
+int relax_tiled_zb(int dim, int cols, int nz, int per_sm) {
+    const int target = (dim == 3 ? 4 : 2) * 148 * per_sm;
     // 3D: 24 planes per CTA (513^3 level-0 pass measured over 8..64: 16-24
     // best, 0.69 ms; 64: 0.72-0.75 ms — shorter marches spread the ring
     // fills of the two co-resident CTAs better and shrink the tail wave)
