@@ -135,3 +135,17 @@ def test_slab_solve_larger_equals_single_gpu(name, n, nranks, rn):
             [(r.cycle, r.work_units, r.residual, r.diag_min) for r in one.report.rows]
         assert [t.value for t in res.report.trace] == [t.value for t in one.report.trace]
         assert K.bits_equal(res.u, one.u)
+
+
+def test_nccl_clique_of_one_rank_solves_like_the_single_gpu():
+    """The NCCL transport on the hardware this suite gets (one GPU): the
+    runtime-loaded libnccl forms a one-rank clique and a solve through it is
+    the single-GPU solve (multi-rank NCCL runs need one process per GPU)."""
+    g, b, f, s, a = K.solve_problem("poisson3d", 4)
+    ctx = S.Context(0)
+    ctx.join_nccl(1, 0, S.nccl_unique_id())
+    assert ctx.clique() == (1, 0)
+    prob = S.ProblemSpec(sgrid(g), f, bc=sbc_of(b), sigma=s, a=a)
+    res = S.solve(prob, S.SolverConfig(n_r=2, tol=1e-10, max_cycles=40, safety=0.9), ctx=ctx)
+    ref = O.solve(g, b, f, s, a, n_r=2, tol=1e-10, max_cycles=40)
+    check_same(res, ref)
