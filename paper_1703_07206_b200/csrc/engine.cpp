@@ -645,6 +645,12 @@ void sgml_solver::flush_kops() {
     b.homogeneous = cyc_homog ? 1 : 0;
     b.sig = has_sigma ? 1 : 0;
     for (int v = 0; v < g.n && v < 14; ++v) b.rc[v] = relax_const(g.dim, v, g.h, a, cfg.safety, cyc_homog, opts.stencil);
+    static const bool no_solo = std::getenv("SGML_NO_SOLO_OPS") != nullptr;
+    for (KOp& op : ops) {
+        double nodes = 1.0;
+        for (int d = 0; d < g.dim; ++d) nodes *= Nl[op.level];
+        op.solo = !no_solo && g.dim == 2 && nodes <= kSoloNodes ? 1 : 0;
+    }
     for (size_t i0 = 0; i0 < ops.size(); i0 += kMaxKOps) {
         b.count = (int)std::min<size_t>(kMaxKOps, ops.size() - i0);
         std::copy(ops.begin() + (long)i0, ops.begin() + (long)i0 + b.count, b.op);

@@ -191,6 +191,7 @@ struct KOpRelax {  // one relaxation pass over a level array (k_relax_small's pe
 struct KOp {
     int kind;
     int level;
+    int solo;  // run by the batch's first CTA alone (small arrays, see interp.cu)
     union {
         KOpMemset ms;
         KOpFaces fc;
@@ -211,9 +212,15 @@ struct KOpBatch {
     RelaxConst rc[14];  // per level
     KOp op[kMaxKOps];
 };
+static_assert(sizeof(KOpBatch) <= 32000, "KOpBatch travels as kernel parameters (32 KB)");
 // level arrays of at most this many nodes are interpreted (and a 2D level 0
 // of at most kClusterNodes2D0)
 constexpr int kClusterNodes = 5000;
+// interpreted 2D operations on level arrays of at most this many nodes run
+// on one CTA of the cluster (<= 17^2: at most one node per thread; C1 129^2
+// 4.13 -> 3.99 ms per solve; 3D levels <= 5^3 gained nothing, <= 9^3 and 2D
+// <= 33^2 lost — several nodes per thread, each round an L2 round trip)
+constexpr int kSoloNodes = 512;
 constexpr int kClusterNodes2D0 = 129 * 129;
 // cluster of CTAs that runs a batch (16 where the device allows it, else 8)
 int interp_cluster_size();

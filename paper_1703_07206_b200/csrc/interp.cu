@@ -157,60 +157,79 @@ __device__ __forceinline__ void cluster_barrier() {
                  "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// one recorded operation, by the threads gtid < gthreads (materialisations:
+// virtual 128-thread blocks vb0, vb0 + vstride, ...)
+template <int DIM>
+__device__ __forceinline__ void run_op(const KOpBatch& b, const KOp& op, ChainEntry* sch, int gtid, int gthreads,
+                                       int vb0, int vstride, int vtx, int vty) {
+    switch (op.kind) {
+        case KOP_MEMSET:
+            for (int e = gtid; e < (int)op.ms.count; e += gthreads) op.ms.p[e] = 0.0;
+            break;
+        case KOP_FACES:
+            op_faces<DIM>(op.fc, b.bc, gtid, gthreads);
+            break;
+        case KOP_PYRAMID:
+            op_pyramid<DIM>(op.py, gtid, gthreads);
+            break;
+        case KOP_MATERIALIZE: {
+            const KOpMaterialize& m = op.mt;
+            const int nsh = min(m.nchain, kMaxChain);
+            for (int c = threadIdx.x; c < nsh; c += kIThreads) sch[c] = m.chain[c];
+            __syncthreads();
+            const int nvb = m.gx * m.gy * m.gz;
+            for (int vb = vb0; vb < nvb; vb += vstride) {
+                const int bx = vb % m.gx, by = (vb / m.gx) % m.gy, bz = vb / (m.gx * m.gy);
+                mat4_body<DIM, 2, false, false>(m.out, m.Lw, m.w, m.base, m.L0, m.wb, m.base_zero, m.ufine, m.Lf,
+                                                m.frel, m.chain, m.nchain, sch, b.bc, b.homogeneous, b.flag,
+                                                m.xtail, 0, bx, by, bz, vtx, vty);
+            }
+            __syncthreads();  // sch is reused by the next materialisation
+            break;
+        }
+        case KOP_RELAX: {
+            const RelaxConst& rc = b.rc[op.level];
+            if (b.sig) {
+                if (rc.has_a) op_relax<DIM, true, true>(op.rx, rc, b.flag, gtid, gthreads);
+                else op_relax<DIM, true, false>(op.rx, rc, b.flag, gtid, gthreads);
+            } else {
+                if (rc.has_a) op_relax<DIM, false, true>(op.rx, rc, b.flag, gtid, gthreads);
+                else op_relax<DIM, false, false>(op.rx, rc, b.flag, gtid, gthreads);
+            }
+            break;
+        }
+        default:
+            break;
+    }
+}
+
 template <int DIM>
 __global__ void __launch_bounds__(kIThreads, 1) k_kop_batch(const __grid_constant__ KOpBatch b) {
     __shared__ ChainEntry sch[kMaxChain];
     pdl_begin();
-    const unsigned crank = cg::this_cluster().block_rank();
-    const unsigned csize = cg::this_cluster().num_blocks();
     // (interpreted level arrays hold far fewer than 2^31 elements)
-    const int gthreads = (int)csize * kIThreads;
-    const int gtid = (int)crank * kIThreads + threadIdx.x;
-    const int sub = threadIdx.x / (MBX * MBY);                  // virtual 128-thread block of this CTA
+    const int crank = (int)cg::this_cluster().block_rank();
+    const int csize = (int)cg::this_cluster().num_blocks();
+    constexpr int VB = kIThreads / (MBX * MBY);  // virtual 128-thread blocks per CTA
+    const int sub = threadIdx.x / (MBX * MBY);
     const int vtx = threadIdx.x % MBX, vty = (threadIdx.x / MBX) % MBY;
-    const int vstride = (int)csize * (kIThreads / (MBX * MBY));
     for (int i = 0; i < b.count; ++i) {
         const KOp& op = b.op[i];
-        switch (op.kind) {
-            case KOP_MEMSET:
-                for (int e = gtid; e < (int)op.ms.count; e += gthreads) op.ms.p[e] = 0.0;
-                break;
-            case KOP_FACES:
-                op_faces<DIM>(op.fc, b.bc, gtid, gthreads);
-                break;
-            case KOP_PYRAMID:
-                op_pyramid<DIM>(op.py, gtid, gthreads);
-                break;
-            case KOP_MATERIALIZE: {
-                const KOpMaterialize& m = op.mt;
-                const int nsh = min(m.nchain, kMaxChain);
-                for (int c = threadIdx.x; c < nsh; c += kIThreads) sch[c] = m.chain[c];
-                __syncthreads();
-                const int nvb = m.gx * m.gy * m.gz;
-                for (int vb = (int)crank * (kIThreads / (MBX * MBY)) + sub; vb < nvb; vb += vstride) {
-                    const int bx = vb % m.gx, by = (vb / m.gx) % m.gy, bz = vb / (m.gx * m.gy);
-                    mat4_body<DIM, 2, false, false>(m.out, m.Lw, m.w, m.base, m.L0, m.wb, m.base_zero, m.ufine,
-                                                    m.Lf, m.frel, m.chain, m.nchain, sch, b.bc, b.homogeneous,
-                                                    b.flag, m.xtail, 0, bx, by, bz, vtx, vty);
-                }
-                __syncthreads();  // sch is reused by the next materialisation
-                break;
-            }
-            case KOP_RELAX: {
-                const RelaxConst& rc = b.rc[op.level];
-                if (b.sig) {
-                    if (rc.has_a) op_relax<DIM, true, true>(op.rx, rc, b.flag, gtid, gthreads);
-                    else op_relax<DIM, true, false>(op.rx, rc, b.flag, gtid, gthreads);
-                } else {
-                    if (rc.has_a) op_relax<DIM, false, true>(op.rx, rc, b.flag, gtid, gthreads);
-                    else op_relax<DIM, false, false>(op.rx, rc, b.flag, gtid, gthreads);
-                }
-                break;
-            }
-            default:
-                break;
+        // Solo operations (arrays of <= kSoloNodes nodes) run on CTA 0 alone,
+        // consecutive ones separated by __syncthreads (CTA-scope ordering of
+        // its global-memory accesses) instead of a cluster barrier each; a
+        // cluster barrier closes the run.  Saves the barrier and the wait for
+        // L2 store acknowledgements per operation where the work is a few
+        // hundred nodes.
+        const bool solo = op.solo != 0;
+        if (!solo) run_op<DIM>(b, op, sch, crank * kIThreads + threadIdx.x, csize * kIThreads, crank * VB + sub,
+                               csize * VB, vtx, vty);
+        else if (crank == 0) run_op<DIM>(b, op, sch, threadIdx.x, kIThreads, sub, VB, vtx, vty);
+        if (solo && i + 1 < b.count && b.op[i + 1].solo) {
+            if (crank == 0) __syncthreads();
+        } else {
+            cluster_barrier();
         }
-        cluster_barrier();
     }
 }
 
