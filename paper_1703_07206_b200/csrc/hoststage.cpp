@@ -46,7 +46,8 @@ public:
     }
     void run(char* dst, const char* src, size_t bytes) {
         const int parts = (int)workers_.size() + 1;
-        const size_t per = (bytes / parts + 63) & ~size_t(63);
+        // (rounded up: a chunk of fewer bytes than parts still gets copied)
+        const size_t per = ((bytes + parts - 1) / parts + 63) & ~size_t(63);
         {
             std::lock_guard<std::mutex> lk(mu_);
             dst_ = dst;
