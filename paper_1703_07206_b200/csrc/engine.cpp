@@ -764,7 +764,17 @@ double sgml_solver::max_abs_r(const double* f_dense) {
 }
 
 // u_tot += e; r -= A(e) + a e; r = 0 on Dirichlet; max|r| into d_cycle[n_slots]
-void sgml_solver::residual(const double* e) {
+// The recurrence can run before the host has seen the cycle's kernel-error
+// flag (one host synchronisation per cycle instead of two) when it changes
+// nothing but r, u_tot and the max|r| slot — the faces it would set are in
+// place (every homogeneous cycle of a problem with Dirichlet faces) — and the
+// kernel itself skips the update on a failed cycle (guarded).
+bool sgml_solver::residual_guardable(const double* e) const {
+    static const bool off = std::getenv("SGML_NO_GUARDED_RESIDUAL") != nullptr;
+    return !off && compact() && !all_neumann && faces_of(r) == FS_ZERO && faces_of(e) == FS_ZERO;
+}
+
+void sgml_solver::residual(const double* e, bool guarded) {
     const int dim = g.dim;
     const cudaStream_t s = ctx->stream;
     unsigned long long* d_rmax = d_cycle + n_slots;
@@ -785,7 +795,9 @@ void sgml_solver::residual(const double* e) {
         tm.g = gmap(r);
         tm.s = has_sigma ? umap(S[0]) : tm.u;
         tm.t = gmap(utot);
-        launch(SGML_CLASS_RESIDUAL, [&] { launch_residual_tma(dim, has_sigma, tm, r, utot, Lv[0], rng[0], rc0, d_rmax, d_flag, s); });
+        launch(SGML_CLASS_RESIDUAL, [&] {
+            launch_residual_tma(dim, has_sigma, tm, r, utot, Lv[0], rng[0], rc0, d_rmax, d_flag, guarded, s);
+        });
         halo(r, 0);  // the next cycle's pyramid reads r across the slab faces
     } else {
         const double inv_h2 = 1.0 / (g.h * g.h);
@@ -1371,16 +1383,16 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
         SGML_CUDA(cudaMemsetAsync(d_cycle, 0, (n_slots + 1) * sizeof(unsigned long long), s));
         reset_fail_flags();
         const double* e = use_graphs() ? cycle_graph(homogeneous) : cycle(homogeneous);
-        // kernel_error check before the recurrence touches u_tot and r
+        // kernel_error check before the recurrence touches u_tot and r (or,
+        // guarded, the recurrence skips itself on a failed cycle)
         if (nrk > 1) tp->allreduce_max_i32(d_flag, 1, s);
-        SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-        SGML_CUDA(cudaStreamSynchronize(s));
         static const bool dbg_flags = std::getenv("SGML_DEBUG_FLAGS") != nullptr;
-        if (dbg_flags) std::fprintf(stderr, "sgml: cycle %d flags %d %d %d %d\n", cyc, h_flag[0], h_flag[1], h_flag[2], h_flag[3]);
-        if (h_flag[0]) {
-            // the reference throws at the first failing pass: the trace keeps
-            // the samples of the passes before it, the cycle gets no row
-            // (cycle.cpp:98-107, 182-190)
+        // the reference throws at the first failing pass: the trace keeps the
+        // samples of the passes before it, the cycle gets no row
+        // (cycle.cpp:98-107, 182-190)
+        auto failed = [&] {
+            if (dbg_flags) std::fprintf(stderr, "sgml: cycle %d flags %d %d %d %d\n", cyc, h_flag[0], h_flag[1], h_flag[2], h_flag[3]);
+            if (!h_flag[0]) return false;
             const int fail_slot = first_failing_pass(homogeneous);
             const double inv_norm = !norm_pending && norm > 0.0 ? 1.0 / norm : 1.0;
             for (int p = 0; p < fail_slot && p < n_slots; ++p) {
@@ -1392,16 +1404,24 @@ void sgml_solver::run(const double* f, double* u_out, sgml_report* rep) {
             }
             rep->nan_detected = 1;
             rep->converged = 0;
-            break;
+            return true;
+        };
+        const bool guarded = residual_guardable(e);
+        if (!guarded) {
+            SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+            SGML_CUDA(cudaStreamSynchronize(s));
+            if (failed()) break;
         }
-        residual(e);
+        residual(e, guarded);
         SGML_CUDA(cudaGetLastError());
         // per-pass diag maxima and max|r| over the ranks (max is order-free:
         // bit-identical to the single-GPU values)
         if (nrk > 1) tp->allreduce_max_u64(d_cycle, n_slots + 1, s);
+        if (guarded) SGML_CUDA(cudaMemcpyAsync(h_flag, d_flag, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaMemcpyAsync(h_cycle, d_cycle, (n_slots + 1) * sizeof(unsigned long long),
                                   cudaMemcpyDeviceToHost, s));
         SGML_CUDA(cudaStreamSynchronize(s));
+        if (guarded && failed()) break;
         if (opts.timing) harvest_spans();
 
         const double inv_norm = !norm_pending && norm > 0.0 ? 1.0 / norm : 1.0;

@@ -258,7 +258,8 @@ struct sgml_solver {
     void load_source(const double* f_dense);            // r <- f
     void zero_mean_r();                                  // zero_mean_projection(r)
     double max_abs_r(const double* f_dense);             // max |r| (data nodes)
-    void residual(const double* e);                      // fused recurrence step
+    void residual(const double* e, bool guarded = false);  // fused recurrence step
+    bool residual_guardable(const double* e) const;
     void reset_fail_flags();
     int first_failing_pass(bool homogeneous);            // after a failed cycle
     const double* dense_view(const double* engine_field);  // dense device view

@@ -127,10 +127,11 @@ void launch_relax_tma(int dim, bool sig, const TmaSet& tm, double* uo, double* d
 // Residual recurrence at level 0 over the range: r -= A(e) + a e (tm.u = e,
 // tm.g = r, r written with mirror ghosts), u_tot += e (tm.t / utot,
 // nullable), max|r| into rmax_slot; reads flag[1] as the relaxation pass.
-// rc = relax_const(level 0).
+// rc = relax_const(level 0).  guarded: nothing happens when flag[0] (a failed
+// cycle) is set.
 void launch_residual_tma(int dim, bool sig, const TmaSet& tm, double* r, double* utot,
                          const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
-                         unsigned long long* rmax_slot, int* flag, cudaStream_t s);
+                         unsigned long long* rmax_slot, int* flag, bool guarded, cudaStream_t s);
 // Dirichlet-face nodes of an extended level array <- 0 (zero) or their face
 // value (the reference's lowest-face-id rule), with their mirror ghost cells
 // unless `mirrors` is false (DU arrays keep all-zero ghosts).

@@ -153,6 +153,10 @@ __global__ void __launch_bounds__(Tile<DIM>::THREADS, DIM == 3 ? (SIG ? 1 : 2) :
         mbar_fence_init();
     }
     pdl_begin();  // the predecessor's outputs are complete from here on
+    // guarded residual (pass_slot < 0): a failed cycle (flag[0], written only
+    // by the cycle's passes, never by this kernel) leaves r and u_tot as they
+    // are, so the host checks the failure after the recurrence
+    if (RESID && pass_slot < 0 && *(const volatile int*)flag) return;
     __syncthreads();
 
     const unsigned a_full = smem_u32(&R.full[0]), a_empty = smem_u32(&R.empty[0]);
@@ -730,8 +734,8 @@ void launch_relax_small(int dim, bool sig, const SmallPasses& sp, const ExtLay& 
 
 void launch_residual_tma(int dim, bool sig, const TmaSet& tm, double* r, double* utot,
                          const ExtLay& L, const NodeRange& rg, const RelaxConst& rc,
-                         unsigned long long* rmax_slot, int* flag, cudaStream_t s) {
-    launch_mode<MODE_RESID>(dim, sig, tm, r, utot, L, rg, rc, rmax_slot, flag, 0, s);
+                         unsigned long long* rmax_slot, int* flag, bool guarded, cudaStream_t s) {
+    launch_mode<MODE_RESID>(dim, sig, tm, r, utot, L, rg, rc, rmax_slot, flag, guarded ? -1 : 0, s);
 }
 
 }  // namespace sgmlb
