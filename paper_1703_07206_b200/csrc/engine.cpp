@@ -475,6 +475,7 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
         }
         for (int v = 1; v < n; ++v)
             for (double* d : DU[v]) du_bufs.push_back(d);
+        h_chain = entries;
         if (!entries.empty()) {
             SGML_CUDA(cudaMalloc((void**)&d_chain, entries.size() * sizeof(ChainEntry)));
             SGML_CUDA(cudaMemcpy(d_chain, entries.data(), entries.size() * sizeof(ChainEntry),
@@ -644,6 +645,8 @@ void sgml_solver::flush_kops() {
     b.flag = d_flag;
     b.homogeneous = cyc_homog ? 1 : 0;
     b.sig = has_sigma ? 1 : 0;
+    b.chains = d_chain && h_chain.size() <= (size_t)kMaxChain ? d_chain : nullptr;
+    b.nchains = b.chains ? (int)h_chain.size() : 0;
     for (int v = 0; v < g.n && v < 14; ++v) b.rc[v] = relax_const(g.dim, v, g.h, a, cfg.safety, cyc_homog, opts.stencil);
     static const bool no_solo = std::getenv("SGML_NO_SOLO_OPS") != nullptr;
     for (KOp& op : ops) {

@@ -146,6 +146,7 @@ struct sgml_solver {
     std::vector<std::array<double*, 2>> U;    // U[v][0..1], v >= 1
     std::vector<std::vector<double*>> DU;     // DU[v][k]
     sgmlb::ChainEntry* d_chain = nullptr;     // per-tooth pending-increment lists
+    std::vector<sgmlb::ChainEntry> h_chain;   // (host copy)
     std::vector<int> tooth_off;               // offset of tooth v1's list in d_chain
     std::vector<const double*> du_bufs;       // DU arrays (faces without mirror ghosts)
     // TMA descriptors per buffer: window box (tile + halo) and tile box

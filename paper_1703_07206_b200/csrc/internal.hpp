@@ -210,6 +210,10 @@ struct KOpBatch {
     int homogeneous;
     int count;
     int sig;
+    // the solver's whole pending-increment table when it has at most
+    // kMaxChain entries (copied to shared memory once per batch), else null
+    const ChainEntry* chains;
+    int nchains;
     RelaxConst rc[14];  // per level
     KOp op[kMaxKOps];
 };

@@ -174,17 +174,22 @@ __device__ __forceinline__ void run_op(const KOpBatch& b, const KOp& op, ChainEn
             break;
         case KOP_MATERIALIZE: {
             const KOpMaterialize& m = op.mt;
-            const int nsh = min(m.nchain, kMaxChain);
-            for (int c = threadIdx.x; c < nsh; c += kIThreads) sch[c] = m.chain[c];
-            __syncthreads();
+            // the batch's copy of the whole increment table, or this chain's
+            const ChainEntry* ch = m.nchain > 0 && b.chains ? sch + (m.chain - b.chains) : sch;
+            if (!b.chains) {
+                const int nsh = min(m.nchain, kMaxChain);
+                for (int c = threadIdx.x; c < nsh; c += kIThreads) sch[c] = m.chain[c];
+                __syncthreads();
+                ch = sch;
+            }
             const int nvb = m.gx * m.gy * m.gz;
             for (int vb = vb0; vb < nvb; vb += vstride) {
                 const int bx = vb % m.gx, by = (vb / m.gx) % m.gy, bz = vb / (m.gx * m.gy);
                 mat4_body<DIM, 2, false, false>(m.out, m.Lw, m.w, m.base, m.L0, m.wb, m.base_zero, m.ufine, m.Lf,
-                                                m.frel, m.chain, m.nchain, sch, b.bc, b.homogeneous, b.flag,
+                                                m.frel, m.chain, m.nchain, ch, b.bc, b.homogeneous, b.flag,
                                                 m.xtail, 0, bx, by, bz, vtx, vty);
             }
-            __syncthreads();  // sch is reused by the next materialisation
+            if (!b.chains) __syncthreads();  // sch is reused by the next materialisation
             break;
         }
         case KOP_RELAX: {
@@ -207,6 +212,10 @@ template <int DIM>
 __global__ void __launch_bounds__(kIThreads, 1) k_kop_batch(const __grid_constant__ KOpBatch b) {
     __shared__ ChainEntry sch[kMaxChain];
     pdl_begin();
+    if (b.chains) {  // (static per solver: one copy serves every materialisation)
+        for (int c = threadIdx.x; c < b.nchains; c += kIThreads) sch[c] = b.chains[c];
+        __syncthreads();
+    }
     // (interpreted level arrays hold far fewer than 2^31 elements)
     const int crank = (int)cg::this_cluster().block_rank();
     const int csize = (int)cg::this_cluster().num_blocks();
