@@ -71,7 +71,7 @@ def problem(case: str):
 CASES = [
     "deformation_circle@11", "deformation_mixed_x@11", "deformation_mixed_y@11",
     "capacitor_high@7", "capacitor_low@7", "capacitor_high@8", "capacitor_low@8",
-    "trifoil_x@9", "trifoil_y@9", "trifoil_z@9", "poisson3d@9",
+    "trifoil_x@9", "trifoil_y@9", "trifoil_z@9", "poisson3d@9", "poisson3d@8",
 ]
 # tests/golden/solves.json: the tests/cases.py solves that run the TMA
 # relaxation kernels with sigma / a / Neumann / mixed faces (SOLVE_CASES_LARGE)

@@ -36,7 +36,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LARGE_JSON = os.path.join(HERE, "golden", "large.json")
 CASES = ["capacitor_high@7", "capacitor_low@7", "capacitor_high@8", "capacitor_low@8",
          "deformation_circle@11", "deformation_mixed_x@11", "deformation_mixed_y@11",
-         "trifoil_x@9", "trifoil_y@9", "trifoil_z@9", "poisson3d@9"]
+         "trifoil_x@9", "trifoil_y@9", "trifoil_z@9", "poisson3d@9", "poisson3d@8"]
 CFG = S.SolverConfig(n_r=2, tol=1e-10, max_cycles=60, safety=0.9)
 
 
