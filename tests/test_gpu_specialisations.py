@@ -143,3 +143,35 @@ def test_solve_long_chains_bitwise():
                   S.SolverConfig(n_r=100, tol=1e-10, max_cycles=6, safety=0.9))
     assert [(r.cycle, r.work_units, r.residual, r.diag_min) for r in res.report.rows] == ref.rows
     assert K.bits_equal(res.u, ref.u)
+
+
+# Tiny lattices (N = 3, 5, 9): one interior node, levels that exist only as
+# faces, a single level, every boundary mix, sigma and a, on each engine path
+# (compact with and without the interpreter and small-level visits, literal).
+TINY_ENGINES = {
+    "compact": dict(),
+    "compact-nointerp": dict(cluster_levels=False),
+    "compact-nosmall-nointerp": dict(cluster_levels=False, small_levels=False),
+    "literal": dict(engine="literal"),
+}
+
+
+@pytest.mark.parametrize("engine", list(TINY_ENGINES))
+@pytest.mark.parametrize("a", [0.0, 0.3])
+@pytest.mark.parametrize("sig", [False, True])
+@pytest.mark.parametrize("dim,n,bcn", [(d, n, b) for d, ns in ((2, (1, 2, 3)), (3, (1, 2, 3)))
+                                       for n in ns for b in BCS[d]])
+def test_tiny_lattices_bitwise(dim, n, bcn, sig, a, engine):
+    g = O.make_grid(dim, n)
+    b = K.bc(bcn)
+    f = O.fill("sinsin2d" if dim == 2 else "poisson3d", g)
+    s = K.sigma_field(g, 57 + dim) if sig else None
+    ref = O.solve(g, b, f, s, a, n_r=2, tol=1e-10, max_cycles=25)
+    res = S.solve(S.ProblemSpec(S.make_grid(dim, n), f, bc=sbc_of(b), sigma=s, a=a),
+                  S.SolverConfig(n_r=2, tol=1e-10, max_cycles=25, safety=0.9),
+                  S.SolverOptions(**TINY_ENGINES[engine]))
+    rep = res.report
+    assert (rep.converged, rep.nan_detected, rep.stagnated) == (ref.converged, ref.nan_detected, ref.stagnated)
+    assert [(r.cycle, r.work_units, r.residual, r.diag_min) for r in rep.rows] == ref.rows
+    assert [(t.cycle, t.pass_, t.level, t.value) for t in rep.trace] == ref.trace
+    assert K.bits_equal(res.u, ref.u)
