@@ -175,3 +175,26 @@ def test_tiny_lattices_bitwise(dim, n, bcn, sig, a, engine):
     assert [(r.cycle, r.work_units, r.residual, r.diag_min) for r in rep.rows] == ref.rows
     assert [(t.cycle, t.pass_, t.level, t.value) for t in rep.trace] == ref.trace
     assert K.bits_equal(res.u, ref.u)
+
+
+# Other relaxation counts and safety factors where the TMA kernels carry the
+# large levels (2D 129^2, 3D 33^3); tol 1e-12 with max_cycles 6 also exits
+# on the cycle cap.
+@pytest.mark.parametrize("n_r,safety,tol,max_cycles", [(1, 0.9, 1e-10, 40), (3, 0.9, 1e-10, 40),
+                                                        (4, 0.6, 1e-10, 40), (2, 1.0, 1e-12, 6)])
+@pytest.mark.parametrize("sig", [False, True])
+@pytest.mark.parametrize("dim,n,bcn", [(2, 7, "mixed_x"), (3, 5, "dir_distinct"), (3, 5, "neumann")])
+def test_relax_counts_and_safety_bitwise(dim, n, bcn, sig, n_r, safety, tol, max_cycles):
+    g = O.make_grid(dim, n)
+    b = K.bc(bcn)
+    f = O.fill("sinsin2d" if dim == 2 else "poisson3d", g)
+    s = K.sigma_field(g, 57 + dim) if sig else None
+    a = 0.25 if bcn == "neumann" else 0.0
+    ref = O.solve(g, b, f, s, a, n_r=n_r, tol=tol, max_cycles=max_cycles, safety=safety)
+    res = S.solve(S.ProblemSpec(S.make_grid(dim, n), f, bc=sbc_of(b), sigma=s, a=a),
+                  S.SolverConfig(n_r=n_r, tol=tol, max_cycles=max_cycles, safety=safety))
+    rep = res.report
+    assert (rep.converged, rep.nan_detected, rep.stagnated) == (ref.converged, ref.nan_detected, ref.stagnated)
+    assert [(r.cycle, r.work_units, r.residual, r.diag_min) for r in rep.rows] == ref.rows
+    assert [(t.cycle, t.pass_, t.level, t.value) for t in rep.trace] == ref.trace
+    assert K.bits_equal(res.u, ref.u)
