@@ -149,3 +149,14 @@ def test_nccl_clique_of_one_rank_solves_like_the_single_gpu():
     res = S.solve(prob, S.SolverConfig(n_r=2, tol=1e-10, max_cycles=40, safety=0.9), ctx=ctx)
     ref = O.solve(g, b, f, s, a, n_r=2, tol=1e-10, max_cycles=40)
     check_same(res, ref)
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("nranks", [2, 4])
+@pytest.mark.parametrize("name", ["poisson3d", "capacitor_high", "neumann3d_a"])
+def test_slab_solve_65_cubed_bitwise(name, nranks):
+    # 65^3 on 2 / 4 ranks: the slab levels run the TMA kernels (interpreter
+    # and small-level paths off the slabs), with the halo / compute overlap
+    out, ref = solve_clique(name, 6, nranks)
+    for res in out:
+        check_same(res, ref)
