@@ -5,6 +5,7 @@ solve does (all reductions are maxima, so the decomposition cannot change a
 bit).  The NCCL transport shares this code path; only the plane copies differ."""
 import threading
 
+import numpy as np
 import pytest
 
 import cases as K
@@ -160,3 +161,64 @@ def test_slab_solve_65_cubed_bitwise(name, nranks):
     out, ref = solve_clique(name, 6, nranks)
     for res in out:
         check_same(res, ref)
+
+
+@pytest.mark.timeout(900)
+def test_slab_solve_129_cubed_eight_ranks_bitwise():
+    # 129^3 on 8 ranks (16 level-0 planes each), default replication (levels
+    # of <= 65 nodes per axis replicated): the configuration the multi-GPU
+    # bench runs, scaled down
+    out, ref = solve_clique("poisson3d", 7, 8, replicate_n=0)
+    for res in out:
+        check_same(res, ref)
+
+
+@pytest.mark.timeout(1800)
+def test_slab_solve_bench_config_eight_ranks_matches_reference_golden():
+    # The multi-GPU bench's exact configuration (513^3 Poisson to 1e-10 on 8
+    # ranks, default replication) on 8 in-process ranks: every rank's report
+    # and solution equal the UNMODIFIED reference's full solve
+    # (tests/golden/large.json, make_golden_large.py) bit for bit.
+    import hashlib
+    import json
+    import os
+    gold_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "large.json")
+    gold = json.load(open(gold_path)).get("poisson3d@9")
+    if gold is None:
+        pytest.skip("tests/golden/large.json lacks poisson3d@9")
+
+    def digest(a):
+        return hashlib.sha256(K.canon(np.asarray(a, np.float64)).tobytes()).hexdigest()
+
+    g = S.make_grid(3, 9)
+    f = S.poisson3d_source(g).numpy()
+    assert digest(f) == gold["f"]
+    nranks = 8
+    group = S.LocalGroup(nranks)
+    out, err = [None] * nranks, [None] * nranks
+
+    def run(r):
+        try:
+            ctx = S.Context(0)
+            ctx.join_local(group, r)
+            prob = S.ProblemSpec(g, f, bc=S.BoundarySpec.all_dirichlet(0.0))
+            out[r] = S.solve(prob, S.SolverConfig(n_r=2, tol=1e-10, max_cycles=60, safety=0.9), ctx=ctx)
+        except Exception as exc:  # surfaced below
+            err[r] = exc
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=1500)
+    assert all(not t.is_alive() for t in ts), "a rank hung"
+    for e in err:
+        if e is not None:
+            raise e
+    for res in out:
+        rep = res.report
+        assert [rep.converged, rep.nan_detected, rep.stagnated] == gold["flags"]
+        assert [[r.cycle, r.work_units, r.residual.hex(), r.diag_min.hex()] for r in rep.rows] == gold["rows"]
+        assert rep.normalization.hex() == gold["normalization"]
+        assert digest([t.value for t in rep.trace]) == gold["trace"]
+        assert digest(res.u) == gold["u"]
