@@ -222,3 +222,44 @@ def test_slab_solve_bench_config_eight_ranks_matches_reference_golden():
         assert rep.normalization.hex() == gold["normalization"]
         assert digest([t.value for t in rep.trace]) == gold["trace"]
         assert digest(res.u) == gold["u"]
+
+
+@pytest.mark.timeout(1800)
+def test_slab_solve_north_star_size_two_ranks_equals_single_gpu():
+    # 1025^3 Poisson (the north-star size): 2 in-process z-slab ranks give the
+    # single-GPU solve bit for bit (the 8-GPU target needs one GPU per rank;
+    # 8 in-process ranks of this size would not fit one B200)
+    g = S.make_grid(3, 10)
+    f = S.poisson3d_source(g).numpy()
+    cfg = S.SolverConfig(n_r=2, tol=1e-10, max_cycles=60, safety=0.9)
+    prob = S.ProblemSpec(g, f, bc=S.BoundarySpec.all_dirichlet(0.0))
+    ctx1 = S.Context(0)
+    one = S.solve(prob, cfg, ctx=ctx1)
+    ctx1.close()  # (frees the single-GPU solver before the ranks allocate)
+    nranks = 2
+    group = S.LocalGroup(nranks)
+    out, err = [None] * nranks, [None] * nranks
+
+    def run(r):
+        try:
+            ctx = S.Context(0)
+            ctx.join_local(group, r)
+            out[r] = S.solve(prob, cfg, ctx=ctx)
+            ctx.close()
+        except Exception as exc:  # surfaced below
+            err[r] = exc
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=1500)
+    assert all(not t.is_alive() for t in ts), "a rank hung"
+    for e in err:
+        if e is not None:
+            raise e
+    for res in out:
+        assert [(r.cycle, r.work_units, r.residual, r.diag_min) for r in res.report.rows] == \
+            [(r.cycle, r.work_units, r.residual, r.diag_min) for r in one.report.rows]
+        assert [t.value for t in res.report.trace] == [t.value for t in one.report.trace]
+        assert K.bits_equal(res.u, one.u)
