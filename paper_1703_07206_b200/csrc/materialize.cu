@@ -201,8 +201,7 @@ ExtLay make_ext(int dim, int N, int z0, int nz) {
     ExtLay L{};
     L.N = N;
     L.Ne = N + 2;
-    // pitch a multiple of 4 doubles: 32-byte aligned rows (TMA needs 16; the
-    // materialisation's 256-bit accesses start at data nodes 4m - 1)
+    // pitch a multiple of 4 doubles: 32-byte aligned rows (TMA needs 16)
     L.Px = (L.Ne + 3) / 4 * 4;
     L.Nz = dim == 3 ? (nz < 0 ? N : nz) : 1;
     L.z0 = dim == 3 ? z0 : 0;
