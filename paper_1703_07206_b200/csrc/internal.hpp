@@ -218,6 +218,7 @@ struct KOpBatch {
     KOp op[kMaxKOps];
 };
 static_assert(sizeof(KOpBatch) <= 32000, "KOpBatch travels as kernel parameters (32 KB)");
+static_assert(sizeof(KOp) % 8 == 0 && alignof(KOp) >= 8, "KOp is staged in 8-byte words");
 // level arrays of at most this many nodes are interpreted (and a 2D level 0
 // of at most kClusterNodes2D0)
 constexpr int kClusterNodes = 5000;

@@ -211,11 +211,20 @@ __device__ __forceinline__ void run_op(const KOpBatch& b, const KOp& op, ChainEn
 template <int DIM>
 __global__ void __launch_bounds__(kIThreads, 1) k_kop_batch(const __grid_constant__ KOpBatch b) {
     __shared__ ChainEntry sch[kMaxChain];
-    pdl_begin();
-    if (b.chains) {  // (static per solver: one copy serves every materialisation)
-        for (int c = threadIdx.x; c < b.nchains; c += kIThreads) sch[c] = b.chains[c];
-        __syncthreads();
+    // the recorded operations, staged once in shared memory: an operation's
+    // fields then cost a shared-memory read instead of a constant-cache miss
+    // (one L2 round trip) when the interpreter reaches it
+    __shared__ KOp sop[kMaxKOps];
+    {
+        const unsigned long long* src = reinterpret_cast<const unsigned long long*>(b.op);
+        unsigned long long* dst = reinterpret_cast<unsigned long long*>(sop);
+        const int words = b.count * (int)(sizeof(KOp) / sizeof(unsigned long long));
+        for (int t = threadIdx.x; t < words; t += kIThreads) dst[t] = src[t];
     }
+    pdl_begin();
+    if (b.chains)  // (static per solver: one copy serves every materialisation)
+        for (int c = threadIdx.x; c < b.nchains; c += kIThreads) sch[c] = b.chains[c];
+    __syncthreads();
     // (interpreted level arrays hold far fewer than 2^31 elements)
     const int crank = (int)cg::this_cluster().block_rank();
     const int csize = (int)cg::this_cluster().num_blocks();
@@ -223,7 +232,7 @@ __global__ void __launch_bounds__(kIThreads, 1) k_kop_batch(const __grid_constan
     const int sub = threadIdx.x / (MBX * MBY);
     const int vtx = threadIdx.x % MBX, vty = (threadIdx.x / MBX) % MBY;
     for (int i = 0; i < b.count; ++i) {
-        const KOp& op = b.op[i];
+        const KOp& op = sop[i];
         // Solo operations (arrays of <= kSoloNodes nodes) run on CTA 0 alone,
         // consecutive ones separated by __syncthreads (CTA-scope ordering of
         // its global-memory accesses) instead of a cluster barrier each; a
@@ -234,7 +243,7 @@ __global__ void __launch_bounds__(kIThreads, 1) k_kop_batch(const __grid_constan
         if (!solo) run_op<DIM>(b, op, sch, crank * kIThreads + threadIdx.x, csize * kIThreads, crank * VB + sub,
                                csize * VB, vtx, vty);
         else if (crank == 0) run_op<DIM>(b, op, sch, threadIdx.x, kIThreads, sub, VB, vtx, vty);
-        if (solo && i + 1 < b.count && b.op[i + 1].solo) {
+        if (solo && i + 1 < b.count && sop[i + 1].solo) {
             if (crank == 0) __syncthreads();
         } else {
             cluster_barrier();
