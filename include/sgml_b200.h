@@ -87,8 +87,8 @@ typedef struct {
                        nodes) runs all its passes in one CTA; -1: one TMA launch per
                        pass on every level (same bits either way) */
     int cluster_levels; /* 0 (default): operations on level arrays of <= 5000 nodes (3D
-                       <= 17^3, 2D <= 65^2; and level 0 of a 2D grid of <= 129^2) run
-                       as batches in one thread-block cluster launch each (single GPU);
+                       <= 17^3) and on 2D level arrays of <= 129^2 nodes run as batches
+                       in one thread-block cluster launch each (single GPU);
                        -1: one kernel per operation (same bits either way) */
     int replicate_n;  /* z-slab solves: levels whose arrays hold at most this many nodes
                        per axis are replicated on every rank instead of exchanging

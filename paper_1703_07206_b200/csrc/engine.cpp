@@ -402,17 +402,16 @@ void sgml_solver::build(sgml_ctx* c, int dim, int n, const sgml_bc& bcin, double
         // nodes (3D <= 17^3, 2D <= 65^2; measured: with larger levels the 16
         // SMs of one cluster run them slower than full-GPU kernels do).
         // SGML_KOP_NODES overrides the bound (A/B and the parity suite).
-        // A 2D grid of <= 129^2 nodes runs its level 0 interpreted too (the
-        // whole cycle but the residual in one batch per tooth: C1 129^2 3.99
-        // -> 3.85 ms per solve; a 129^2 level under a finer level 0 is faster
-        // as kernels).
+        // 2D levels of <= 129^2 nodes are interpreted too (C1 129^2: the whole
+        // cycle but the residual in one batch per tooth, 3.99 -> 3.85 ms per
+        // solve; 257^2: 3.89 -> 3.82 ms with its 129^2 level 1 interpreted).
         kop_ok.assign(n, 0);
         const char* kn = std::getenv("SGML_KOP_NODES");
         const double kop_max = kn ? std::atof(kn) : (double)kClusterNodes;
         for (int v = 0; v < n; ++v) {
             double nodes = 1.0;
             for (int d = 0; d < dim; ++d) nodes *= Nl[v];
-            kop_ok[v] = nodes <= kop_max || (!kn && dim == 2 && v == 0 && nodes <= kClusterNodes2D0) ? 1 : 0;
+            kop_ok[v] = nodes <= kop_max || (!kn && dim == 2 && nodes <= kClusterNodes2D) ? 1 : 0;
         }
         // nodes off the Dirichlet faces, per level (local z indices); face values
         rng.assign(n, NodeRange{});

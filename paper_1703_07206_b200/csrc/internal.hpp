@@ -219,15 +219,15 @@ struct KOpBatch {
 };
 static_assert(sizeof(KOpBatch) <= 32000, "KOpBatch travels as kernel parameters (32 KB)");
 static_assert(sizeof(KOp) % 8 == 0 && alignof(KOp) >= 8, "KOp is staged in 8-byte words");
-// level arrays of at most this many nodes are interpreted (and a 2D level 0
-// of at most kClusterNodes2D0)
+// level arrays of at most this many nodes are interpreted (2D: at most
+// kClusterNodes2D)
 constexpr int kClusterNodes = 5000;
+constexpr int kClusterNodes2D = 129 * 129;
 // interpreted 2D operations on level arrays of at most this many nodes run
 // on one CTA of the cluster (<= 17^2: at most one node per thread; C1 129^2
 // 4.13 -> 3.99 ms per solve; 3D levels <= 5^3 gained nothing, <= 9^3 and 2D
 // <= 33^2 lost — several nodes per thread, each round an L2 round trip)
 constexpr int kSoloNodes = 512;
-constexpr int kClusterNodes2D0 = 129 * 129;
 // cluster of CTAs that runs a batch (16 where the device allows it, else 8)
 int interp_cluster_size();
 // the launch geometry launch_materialize4 uses for a whole level array
