@@ -14,8 +14,10 @@
 //
 // Per-node arithmetic is exactly that of the kernels the operations replace:
 // relaxation passes follow k_relax_small (the reference's relax branch,
-// kernels.cpp:94-137, edge terms unfused), materialisations run
-// k_materialize4's body (level_ops.cuh), pyramid steps and Dirichlet faces
+// kernels.cpp:94-137, edge terms unfused), materialisations follow
+// k_materialize4 (one node per thread with every chain corner loaded up
+// front, op_mat_node; longer chains run its body, level_ops.cuh), pyramid
+// steps and Dirichlet faces
 // follow k_pyramid_ext and k_dirichlet_faces.  Data written by an earlier
 // operation of the batch is read with coherent loads (never .nc).
 #include <cooperative_groups.h>
