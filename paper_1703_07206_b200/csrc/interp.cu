@@ -162,91 +162,19 @@ __device__ __forceinline__ void cluster_barrier() {
 // A materialisation one node per thread (the interpreter's form: the
 // operation is latency-bound, so every corner of every chain entry is loaded
 // before any arithmetic — one L2 round trip for the whole chain instead of
-// one per entry).  Per node exactly k_materialize4's arithmetic
-// (level_ops.cuh mat4_body, materialize.cu): the Dirichlet value, the
-// level-(w + frel) value, or ((base + I_l0(du0)) + I_l1(du1)) + ... with
-// I_l = sum over r, q, p of ((wz * wy) * wx) * du (zero-weight rows in y / z
-// skipped, the p = 1 corner always added).  Chains of at most NodeChain::max.
-template <int DIM>
-struct NodeChain {
-    static constexpr int max = DIM == 3 ? 3 : 6;  // (all corners in registers)
-};
-
+// one per entry; mat_node, level_ops.cuh).  Chains of at most
+// NodeChain::max entries.
 template <int DIM>
 __device__ void op_mat_node(const KOpMaterialize& m, const ChainEntry* ch, const KOpBatch& b, int gtid,
                             int gthreads) {
-    constexpr int NCV = DIM == 3 ? 8 : 4;  // corner values per entry: [r][q][p]
     const ExtLay& Lw = m.Lw;
-    const int Nw = Lw.N, w = m.w, nz = DIM == 3 ? Lw.Nz : 1;
-    const int total = Nw * Nw * nz, bsh = w - m.wb, fmask = (1 << m.frel) - 1;
+    const int Nw = Lw.N, nz = DIM == 3 ? Lw.Nz : 1;
+    const int total = Nw * Nw * nz;
     int bad = 0, tiny = 0;
-    for (int e = gtid; e < total; e += gthreads) {
-        const int I = e % Nw, J = (e / Nw) % Nw, K = DIM == 3 ? e / (Nw * Nw) : 0;
-        const int Kg = DIM == 3 ? K + Lw.z0 : 0;
-        double value;
-        if (on_dirichlet<DIM>(b.bc, Nw, I, J, Kg)) {
-            value = b.homogeneous ? 0.0 : dirichlet_value<DIM>(b.bc, Nw, I, J, Kg);
-        } else if (m.ufine && ((I | J | Kg) & fmask) == 0) {
-            value = m.ufine[eix<DIM>(m.Lf, I >> m.frel, J >> m.frel, (Kg >> m.frel) - m.Lf.z0)];
-        } else {
-            const int x = I << w, y = J << w, z = Kg << w;
-            double val = m.base_zero ? 0.0 : m.base[eix<DIM>(m.L0, I << bsh, J << bsh, (z >> m.wb) - m.L0.z0)];
-            constexpr int MC = NodeChain<DIM>::max;
-            double cv[MC][NCV];
-#pragma unroll
-            for (int c = 0; c < MC; ++c) {
-                const bool in = c < m.nchain;
-                const ChainEntry& ce = ch[in ? c : 0];
-                const int l = ce.level, msk = (1 << l) - 1;
-                const int nq = (y & msk) ? 2 : 1, nr = (DIM == 3 && (z & msk)) ? 2 : 1;
-                const int sq = ce.L.Px, sr = DIM == 3 ? (int)ce.L.plane : 0;
-                const double* o = ce.du + eix<DIM>(ce.L, x >> l, y >> l, DIM == 3 ? (z >> l) - ce.L.z0 : 0);
-#pragma unroll
-                for (int r = 0; r < (DIM == 3 ? 2 : 1); ++r)
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const bool live = in && r < nr && q < nq;
-                        cv[c][(r * 2 + q) * 2] = live ? o[r * sr + q * sq] : 0.0;
-                        cv[c][(r * 2 + q) * 2 + 1] = live ? o[r * sr + q * sq + 1] : 0.0;
-                    }
-            }
-#pragma unroll
-            for (int c = 0; c < MC; ++c) {
-                if (c >= m.nchain) continue;
-                const ChainEntry& ce = ch[c];
-                const int l = ce.level, msk = (1 << l) - 1;
-                const double inv = __longlong_as_double((long long)(1023 - l) << 52);  // 2^-l, exact
-                const int iy = y & msk, iz = z & msk;
-                const double fy = (double)iy * inv, fz = (double)iz * inv;
-                const double wy[2] = {1.0 - fy, fy};
-                const double wz[2] = {1.0 - fz, fz};
-                const int nq = iy ? 2 : 1, nr = (DIM == 3 && iz) ? 2 : 1;
-                const double fx = (double)(x & msk) * inv, wx0 = 1.0 - fx;
-                double acc = 0.0;
-#pragma unroll
-                for (int r = 0; r < (DIM == 3 ? 2 : 1); ++r) {
-                    if (r >= nr) continue;
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        if (q >= nq) continue;
-                        const double wzy = DIM == 3 ? wz[r] * wy[q] : wy[q];
-                        const double w0 = wzy * wx0, w1 = wzy * fx;
-                        const double t0 = w0 * cv[c][(r * 2 + q) * 2];
-                        acc = (r == 0 && q == 0) ? t0 : acc + t0;
-                        acc = acc + w1 * cv[c][(r * 2 + q) * 2 + 1];
-                    }
-                }
-                val = val + acc;
-            }
-            value = val;
-        }
-        bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
-        {  // nonzero |value| < 2^-969 (see launch_relax_tma)
-            const unsigned key = ((unsigned)__double2hiint(value) & 0x7fffffffu) | (__double2loint(value) != 0 ? 1u : 0u);
-            tiny |= key - 1u < 0x035fffffu;
-        }
-        store_ext<DIM>(m.out, Lw, I, J, K, value);
-    }
+    for (int e = gtid; e < total; e += gthreads)
+        mat_node<DIM, NodeChain<DIM>::max, false>(m.out, Lw, m.w, m.base, m.L0, m.wb, m.base_zero, m.ufine, m.Lf,
+                                                  m.frel, ch, m.nchain, b.bc, b.homogeneous, e % Nw, (e / Nw) % Nw,
+                                                  DIM == 3 ? e / (Nw * Nw) : 0, bad, tiny);
     warp_or_commit(bad, b.flag);
     warp_or_commit(tiny, b.flag + 1);
 }

@@ -278,4 +278,90 @@ __device__ __forceinline__ void mat4_body(double* __restrict__ out, ExtLay Lw, i
     warp_or_commit(tiny, flag + 1);
 }
 
+// ---------------------------------------------------------------------------
+// One node of a materialisation (k_materialize4's arithmetic for a single
+// node): the Dirichlet value, the level-(w + frel) value, or
+// ((base + I_l0(du0)) + I_l1(du1)) + ... with I_l = sum over r, q, p of
+// ((wz * wy) * wx) * du (zero-weight rows in y / z skipped, the p = 1 corner
+// always added).  Every corner of every entry (at most MC) is loaded before
+// any arithmetic.  Node (I, J, K), K local; stores with the mirror ghosts and
+// folds the non-finite / tiny checks into bad / tiny.
+template <int DIM>
+struct NodeChain {
+    static constexpr int max = DIM == 3 ? 3 : 6;  // (all corners in registers)
+};
+
+template <int DIM, int MC, bool NCLD>
+__device__ __forceinline__ void mat_node(double* __restrict__ out, const ExtLay& Lw, int w,
+                                         const double* __restrict__ base, const ExtLay& L0, int wb, int base_zero,
+                                         const double* __restrict__ ufine, const ExtLay& Lf, int frel,
+                                         const ChainEntry* ch, int nchain, const BcDev& bc, int homogeneous, int I,
+                                         int J, int K, int& bad, int& tiny) {
+    constexpr int NCV = DIM == 3 ? 8 : 4;  // corner values per entry: [r][q][p]
+    const int Nw = Lw.N, Kg = DIM == 3 ? K + Lw.z0 : 0;
+    const int bsh = w - wb, fmask = (1 << frel) - 1;
+    double value;
+    if (on_dirichlet<DIM>(bc, Nw, I, J, Kg)) {
+        value = homogeneous ? 0.0 : dirichlet_value<DIM>(bc, Nw, I, J, Kg);
+    } else if (ufine && ((I | J | Kg) & fmask) == 0) {
+        value = ldx<NCLD>(ufine + eix<DIM>(Lf, I >> frel, J >> frel, (Kg >> frel) - Lf.z0));
+    } else {
+        const int x = I << w, y = J << w, z = Kg << w;
+        double val = base_zero ? 0.0 : ldx<NCLD>(base + eix<DIM>(L0, I << bsh, J << bsh, (z >> wb) - L0.z0));
+        double cv[MC][NCV];
+#pragma unroll
+        for (int c = 0; c < MC; ++c) {
+            const bool in = c < nchain;
+            const ChainEntry& ce = ch[in ? c : 0];
+            const int l = ce.level, msk = (1 << l) - 1;
+            const int nq = (y & msk) ? 2 : 1, nr = (DIM == 3 && (z & msk)) ? 2 : 1;
+            const int sq = ce.L.Px, sr = DIM == 3 ? (int)ce.L.plane : 0;
+            const double* o = ce.du + eix<DIM>(ce.L, x >> l, y >> l, DIM == 3 ? (z >> l) - ce.L.z0 : 0);
+#pragma unroll
+            for (int r = 0; r < (DIM == 3 ? 2 : 1); ++r)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const bool live = in && r < nr && q < nq;
+                    cv[c][(r * 2 + q) * 2] = live ? ldx<NCLD>(o + r * sr + q * sq) : 0.0;
+                    cv[c][(r * 2 + q) * 2 + 1] = live ? ldx<NCLD>(o + r * sr + q * sq + 1) : 0.0;
+                }
+        }
+#pragma unroll
+        for (int c = 0; c < MC; ++c) {
+            if (c >= nchain) continue;
+            const ChainEntry& ce = ch[c];
+            const int l = ce.level, msk = (1 << l) - 1;
+            const double inv = __longlong_as_double((long long)(1023 - l) << 52);  // 2^-l, exact
+            const int iy = y & msk, iz = z & msk;
+            const double fy = (double)iy * inv, fz = (double)iz * inv;
+            const double wy[2] = {1.0 - fy, fy};
+            const double wz[2] = {1.0 - fz, fz};
+            const int nq = iy ? 2 : 1, nr = (DIM == 3 && iz) ? 2 : 1;
+            const double fx = (double)(x & msk) * inv, wx0 = 1.0 - fx;
+            double acc = 0.0;
+#pragma unroll
+            for (int r = 0; r < (DIM == 3 ? 2 : 1); ++r) {
+                if (r >= nr) continue;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    if (q >= nq) continue;
+                    const double wzy = DIM == 3 ? wz[r] * wy[q] : wy[q];
+                    const double w0 = wzy * wx0, w1 = wzy * fx;
+                    const double t0 = w0 * cv[c][(r * 2 + q) * 2];
+                    acc = (r == 0 && q == 0) ? t0 : acc + t0;
+                    acc = acc + w1 * cv[c][(r * 2 + q) * 2 + 1];
+                }
+            }
+            val = val + acc;
+        }
+        value = val;
+    }
+    bad |= (__double_as_longlong(value) & 0x7ff0000000000000LL) == 0x7ff0000000000000LL;
+    {  // nonzero |value| < 2^-969 (see launch_relax_tma)
+        const unsigned key = ((unsigned)__double2hiint(value) & 0x7fffffffu) | (__double2loint(value) != 0 ? 1u : 0u);
+        tiny |= key - 1u < 0x035fffffu;
+    }
+    store_ext<DIM>(out, Lw, I, J, K, value);
+}
+
 }  // namespace sgmlb

@@ -28,6 +28,8 @@
 // last row 2H alone (its second copy is computed redundantly and dropped).
 // Threads whose nodes all lie on Dirichlet faces skip the chain.  Chain
 // descriptors sit in shared memory.
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include "device.cuh"
@@ -61,6 +63,32 @@ __global__ void __launch_bounds__(MBX* MBY, 5)
         mat4_body<DIM, NC, DIAG, true>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, frel, chain, nchain, sch, bc,
                                        homogeneous, flag, xtail, k0, blockIdx.x, blockIdx.y, bz, threadIdx.x,
                                        threadIdx.y);
+}
+
+// Short chains (at most kShortChain entries): one node per thread along x
+// (coalesced base loads and stores), every chain corner loaded up front
+// (level_ops.cuh mat_node) — the 4-node, 2-copy form above shares weights and
+// corners, which pays only once the chain arithmetic dominates.
+constexpr int kShortChain = 2;
+constexpr int kNodeX = 256;
+
+template <int DIM>
+__global__ void __launch_bounds__(kNodeX) k_mat_node(double* __restrict__ out, ExtLay Lw, int w,
+                                                     const double* __restrict__ base, ExtLay L0, int wb, int base_zero,
+                                                     const double* __restrict__ ufine, ExtLay Lf, int frel,
+                                                     const ChainEntry* __restrict__ chain, int nchain, BcDev bc,
+                                                     int homogeneous, int* flag, int k0) {
+    __shared__ ChainEntry sch[kShortChain];
+    pdl_begin();
+    if (threadIdx.x < nchain) sch[threadIdx.x] = chain[threadIdx.x];
+    __syncthreads();
+    const int I = blockIdx.x * kNodeX + threadIdx.x, J = blockIdx.y, K = DIM == 3 ? k0 + (int)blockIdx.z : 0;
+    int bad = 0, tiny = 0;
+    if (I < Lw.N)
+        mat_node<DIM, kShortChain, true>(out, Lw, w, base, L0, wb, base_zero, ufine, Lf, frel, sch, nchain, bc,
+                                         homogeneous, I, J, K, bad, tiny);
+    warp_or_commit(bad, flag);
+    warp_or_commit(tiny, flag + 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -229,6 +257,21 @@ void launch_materialize4(int dim, double* out, const ExtLay& Lw, int w, const do
     const int Nw = Lw.N;
     if (ke < 0) ke = Lw.Nz;
     if (dim == 3 && ke <= kb) return;
+    static const bool no_short = std::getenv("SGML_NO_SHORT_CHAINS") != nullptr;
+    // (small levels only: on 129^3 and larger the weight and corner sharing
+    // of the 4-node form wins even for one entry — 513^3 materialisations
+    // 92 -> 118 ms per solve with this form, 65^3 solve 5.21 -> 5.08 ms)
+    const double nodes = (double)Nw * Nw * (dim == 3 ? (double)Nw : 1.0);
+    if (!diag && !no_short && nchain <= kShortChain && nodes <= 300000.0) {
+        const dim3 grid((Nw + kNodeX - 1) / kNodeX, Nw, dim == 3 ? ke - kb : 1);
+        if (dim == 2)
+            launch_pdl(k_mat_node<2>, grid, dim3(kNodeX), 0, s, out, Lw, w, base, L0, wb, base_zero ? 1 : 0, ufine, Lf,
+                       frel, chain, nchain, bc, homogeneous ? 1 : 0, flag, 0);
+        else
+            launch_pdl(k_mat_node<3>, grid, dim3(kNodeX), 0, s, out, Lw, w, base, L0, wb, base_zero ? 1 : 0, ufine, Lf,
+                       frel, chain, nchain, bc, homogeneous ? 1 : 0, flag, kb);
+        return;
+    }
     // two copies (y and y + (Nw-1)/2): measured faster than one (occupancy
     // does not pay for the lost weight sharing) and than four (16 nodes per
     // thread cost occupancy)
