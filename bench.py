@@ -68,7 +68,9 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=9, help="grid exponent, N = 2^n + 1 (default 513^3)")
+    # (--grid-n: the spelling that survives torch.distributed.run's option
+    # matching, which reads a bare --n as an abbreviation of its own options)
+    p.add_argument("--n", "--grid-n", dest="n", type=int, default=9, help="grid exponent, N = 2^n + 1 (default 513^3)")
     p.add_argument("--engine", choices=["compact", "literal"], default="compact")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -543,6 +545,9 @@ def free_port() -> int:
 def launcher_cmd(gpus: int, argv) -> list:
     """The torch.distributed.run command that runs this script on `gpus` ranks
     of this node (one process per GPU)."""
+    # (a bare --n would be read by torch.distributed.run as one of its own
+    # options: pass it on as --grid-n)
+    argv = ["--grid-n" if a == "--n" else ("--grid-n=" + a[4:] if a.startswith("--n=") else a) for a in argv]
     return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
             "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
 
@@ -570,7 +575,9 @@ def main():
             print(f"bench.py: {world} ranks need {world} visible GPUs, found {visible_gpus()}",
                   file=sys.stderr, flush=True)
             sys.exit(2)
-    dist = Dist(world, rank, local)
+    # (the reference arm runs on rank 0's host cores alone and needs neither a
+    # GPU per rank nor a process group: the other ranks exit at once)
+    dist = Dist(world if args.impl == "ours" else 1, rank, local)
     try:
         line = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
         if line is not None:

@@ -35,6 +35,8 @@ def test_launcher_command_is_one_rank_per_gpu():
     assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
     assert cmd[-4:] == ["--gpus", "4", "--steps", "3"]
     assert cmd[-5].endswith("bench.py")
+    # a bare --n would be taken by torch.distributed.run itself
+    assert bench.launcher_cmd(2, ["--n", "7", "--n=6"])[-3:] == ["--grid-n", "7", "--grid-n=6"]
 
 
 @pytest.mark.parametrize("n,k", [(4, 1), (6, 5), (9, 20), (9, 200)])
@@ -81,6 +83,22 @@ def test_reference_arm_runs_one_full_cycle_of_the_same_problem():
     assert line["impl"] == "reference" and line["steps"] == 4 and line["value"] > 0
     assert line["config"]["n"] == 5 and line["cpu_baseline"]["cores"] == 2
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.skipif(O.ref_lib() is None, reason="reference build unavailable")
+def test_reference_arm_under_torchrun_prints_one_line_from_rank_0():
+    # the driver launches the reference arm like our own (torchrun, N ranks):
+    # rank 0 alone runs and prints; no GPU per rank, no process group needed
+    env = dict(os.environ, OMP_NUM_THREADS="2", CUDA_VISIBLE_DEVICES="")
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", f"--master-port={bench.free_port()}",
+                        os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--grid-n", "4",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=300, env=env)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [x for x in p.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
 
 
 @pytest.mark.skipif(O.ref_lib() is None, reason="reference build unavailable")
