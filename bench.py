@@ -224,14 +224,24 @@ def chunk_plan(schedule, k: int):
     return chunks, w, U
 
 
+def ref_threads() -> int:
+    """OpenMP threads for the reference's loops: every host core.  Under
+    torch.distributed.run, which sets OMP_NUM_THREADS=1 for each process, the
+    reference runs on rank 0 alone and takes all cores back (must run before
+    the reference build is loaded)."""
+    omp = os.environ.get("OMP_NUM_THREADS", "")
+    if not omp or (int(os.environ.get("WORLD_SIZE", "1")) > 1 and omp == "1"):
+        os.environ["OMP_NUM_THREADS"] = str(host_cores())
+    return int(os.environ["OMP_NUM_THREADS"])
+
+
 def cpu_sample(n: int, budget_s: float = 20.0):
     """cpu_baseline: the reference core (oracle/_ref) on the same problem, a
     systematic sample of its cycle's schedule steps (every m-th step, m odd so
     both step kinds are sampled) sized for ~budget_s; the C port's single
     cycles at 129^3 if the reference build is absent."""
+    cores = ref_threads()  # the threads the reference's OpenMP loops use
     from oracle import oracle as O  # checker / baseline only
-    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
-    cores = int(os.environ["OMP_NUM_THREADS"])  # the threads the reference's OpenMP loops use
     if O.ref_lib() is None:
         g = O.make_grid(3, 7)
         f = O.fill("poisson3d", g)
@@ -268,8 +278,7 @@ def run_reference(args, dist):
     box's host cores, one full cycle in K consecutive chunks (one per step)."""
     if dist.rank != 0:
         return None
-    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
-    cores = int(os.environ["OMP_NUM_THREADS"])
+    cores = ref_threads()
     O, g, sess = ref_session(args.n)
     chunks, w, U = chunk_plan(sess.schedule, args.steps)
     T = g.total

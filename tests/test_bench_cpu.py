@@ -89,7 +89,8 @@ def test_reference_arm_runs_one_full_cycle_of_the_same_problem():
 def test_reference_arm_under_torchrun_prints_one_line_from_rank_0():
     # the driver launches the reference arm like our own (torchrun, N ranks):
     # rank 0 alone runs and prints; no GPU per rank, no process group needed
-    env = dict(os.environ, OMP_NUM_THREADS="2", CUDA_VISIBLE_DEVICES="")
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    env.pop("OMP_NUM_THREADS", None)  # (torch.distributed.run then sets 1 per process)
     p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", f"--master-port={bench.free_port()}",
                         os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--grid-n", "4",
@@ -99,6 +100,9 @@ def test_reference_arm_under_torchrun_prints_one_line_from_rank_0():
     assert len(lines) == 1
     line = json.loads(lines[0])
     assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+    # torch.distributed.run sets OMP_NUM_THREADS=1 per process; rank 0 takes
+    # the host's cores back
+    assert line["cpu_baseline"]["cores"] == bench.host_cores()
 
 
 @pytest.mark.skipif(O.ref_lib() is None, reason="reference build unavailable")
